@@ -1,0 +1,122 @@
+"""p-multigrid pieces (oracle): transfer, Chebyshev-Jacobi smoother, V-cycle, Lanczos,
+diagonal.  Test infrastructure only — see oracle/__init__.py.
+
+PAPER.md:1531-1541 (§5.3): hp-multigrid, polynomial degree lowered level by level
+(p-coarsening); readings G17 (5 -> 3 -> 2 -> 1), G18 (P = exact DG embedding, R = P^T).
+PAPER.md:1553-1557: V-cycles with a Chebyshev-accelerated Jacobi smoother (Adams 2003),
+inverse diagonal precomputed per level, residual via the level operator.
+Readings G12-G15: degree 5, range [lambda_hi/20, lambda_hi], lambda_hi = 1.2 lambda_hat,
+1 pre- + 1 post-smoothing, coarsest level = Chebyshev(5) from 0.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import basis as B
+
+
+def transfer_1d(kf: int, kc: int) -> np.ndarray:
+    """P1[i_f, j_c] = l^(kc)_j(xi^(kf)_i): coarse Lagrange basis (on the kc+1 Gauss points)
+    evaluated at the fine Gauss points (G18)."""
+    xf, _ = B.gauss01(kf + 1)
+    xc, _ = B.gauss01(kc + 1)
+    return B.lagrange(xc, xf)
+
+
+def transfer_3d(kf: int, kc: int) -> np.ndarray:
+    """Per-cell prolongation (n_f^3 x n_c^3), lexicographic x fastest: kron(P1, P1, P1)."""
+    P1 = transfer_1d(kf, kc)
+    return np.kron(P1, np.kron(P1, P1))
+
+
+def prolongate(coarse, kf, kc, n_cells, ncomp=1):
+    P = transfer_3d(kf, kc)
+    C = coarse.reshape(n_cells * ncomp, -1)
+    return (C @ P.T).reshape(-1)
+
+
+def restrict(fine, kf, kc, n_cells, ncomp=1):
+    P = transfer_3d(kf, kc)
+    F = fine.reshape(n_cells * ncomp, -1)
+    return (F @ P).reshape(-1)
+
+
+def chebyshev(apply, Dinv, b, x0, lam_lo, lam_hi, m=5):
+    """Chebyshev semi-iteration on D^-1 A (Adams 2003 via PAPER.md:1555):
+      theta = (hi+lo)/2, delta = (hi-lo)/2, sigma = theta/delta, rho_0 = 1/sigma
+      r_0 = b - A x_0; d_0 = D^-1 r_0 / theta; x_1 = x_0 + d_0
+      j = 1..m-1: r_j = b - A x_j; rho_j = 1/(2 sigma - rho_{j-1});
+                  d_j = rho_j rho_{j-1} d_{j-1} + (2 rho_j/delta) D^-1 r_j; x_{j+1} = x_j + d_j
+    Returns x_m."""
+    theta = 0.5 * (lam_hi + lam_lo)
+    delta = 0.5 * (lam_hi - lam_lo)
+    sigma = theta / delta
+    rho = 1.0 / sigma
+    x = np.array(x0, dtype=np.float64, copy=True)
+    r = b - apply(x)
+    dvec = Dinv * r / theta
+    x = x + dvec
+    for _ in range(1, m):
+        r = b - apply(x)
+        rho_new = 1.0 / (2.0 * sigma - rho)
+        dvec = rho_new * rho * dvec + (2.0 * rho_new / delta) * Dinv * r
+        rho = rho_new
+        x = x + dvec
+    return x
+
+
+def vcycle(levels, b, lvl=None, m=5):
+    """V(l, b) per SURVEY.md §8(c) c1.7.  `levels` is finest-first; each entry a dict with
+    apply, Dinv, lam_hi, and (except the coarsest) restrict(r) / prolongate(xc) to the next
+    coarser level.  lam_lo = lam_hi / 20 (G12)."""
+    if lvl is None:
+        lvl = 0
+    L = levels[lvl]
+    lo, hi = L["lam_hi"] / 20.0, L["lam_hi"]
+    zero = np.zeros_like(b)
+    if lvl == len(levels) - 1:
+        return chebyshev(L["apply"], L["Dinv"], b, zero, lo, hi, m)
+    x = chebyshev(L["apply"], L["Dinv"], b, zero, lo, hi, m)
+    r = b - L["apply"](x)
+    xc = vcycle(levels, L["restrict"](r), lvl + 1, m)
+    x = x + L["prolongate"](xc)
+    return chebyshev(L["apply"], L["Dinv"], b, x, lo, hi, m)
+
+
+def lanczos_lambda_max(apply, Dinv, v0, steps=20):
+    """Largest eigenvalue estimate of D^-1 A by `steps` Lanczos steps (reading G12) on the
+    symmetric form D^-1/2 A D^-1/2, start vector D^1/2-weighted v0; Ritz value = largest
+    eigenvalue of the tridiagonal matrix."""
+    s = np.sqrt(Dinv)
+    q = v0 / s
+    q = q / np.linalg.norm(q)
+    q_prev = np.zeros_like(q)
+    alpha, beta = [], []
+    b_prev = 0.0
+    for _ in range(steps):
+        w = s * apply(s * q)
+        a = q @ w
+        w = w - a * q - b_prev * q_prev
+        alpha.append(a)
+        bn = np.linalg.norm(w)
+        if bn == 0.0:
+            break
+        beta.append(bn)
+        q_prev, q = q, w / bn
+        b_prev = bn
+    k = len(alpha)
+    T = np.diag(alpha) + np.diag(beta[:k - 1], 1) + np.diag(beta[:k - 1], -1)
+    return float(np.linalg.eigvalsh(T).max())
+
+
+def diagonal_entries(apply_cells, n_dofs_cell, idx, ncomp=1):
+    """D_ii = a(phi_i, phi_i) = (A e_i)_i for sampled global DoF indices idx, evaluated with
+    the matrix-free oracle restricted to the DoF's own cell: apply_cells(e, cells) -> y rows."""
+    out = np.empty(len(idx))
+    per_cell = ncomp * n_dofs_cell
+    for t, i in enumerate(idx):
+        c = int(i) // per_cell
+        e = np.zeros(per_cell)
+        e[int(i) % per_cell] = 1.0
+        out[t] = apply_cells(c, e)[int(i) % per_cell]
+    return out
