@@ -1,0 +1,190 @@
+/* dgvv.h — C ABI of the B200-native matrix-free SIPG viscous-operator hot path
+ * (arXiv 2506.14424, "variable viscosity incompressible flow", §4-§5).
+ *
+ * Everything below is FP64 and runs in the library's own CUDA kernels (sm_100a).  The
+ * library never falls back to the CPU: without a CUDA device every compute call returns
+ * DGVV_ECUDA.
+ *
+ * Conventions shared by every call (readings of SURVEY.md §8(c), restated in DESIGN.md):
+ *  - Reference cell [0,1]^3.  Degree-k DG space: tensor Lagrange basis on the k+1
+ *    Gauss-Legendre points (G2), quadrature with the same k+1 Gauss points per direction
+ *    (G1) — "collocation": coefficient = value at the quadrature point.
+ *  - Vector layout (canonical, device, caller-owned, contiguous FP64):
+ *        vector operator : [local_cell][component 0..2][z][y][x]   (3 (k+1)^3 per cell)
+ *        scalar operator : [local_cell][z][y][x]                   ((k+1)^3 per cell)
+ *  - Local faces are ordered (-x,+x,-y,+y,-z,+z); face quadrature points are lexicographic
+ *    over the two tangential axes in increasing axis order, first axis fastest.  Meshes
+ *    must be structured and aligned: point (a,b) of face +d of a cell coincides with point
+ *    (a,b) of face -d of its neighbour (checked at setup, DGVV_EUNSUPPORTED otherwise).
+ *  - Penalty (G3, G5, G6): tau = IP (k+1)^2 max(H-,H+) (nu- + nu+)/2,
+ *    H_K = (A(dK\Gamma)/2 + A(dK cap Gamma)) / V(K); boundary faces use H_K and nu-.
+ *  - Boundary conditions by the mirror principle (G7): Dirichlet
+ *    faces u+ = -u-, grad u+ = grad u-, nu+ = nu-; Neumann faces contribute nothing;
+ *    periodic faces are ordinary neighbours.
+ *
+ * Ownership: dgvv_setup copies every host array; vectors are borrowed device pointers the
+ * library never frees or retains (except u_lin, see dgvv_update_viscosity).  All compute
+ * calls are asynchronous on the caller's stream unless stated otherwise.  Status codes are
+ * returned, never thrown; dgvv_last_error gives a message for the last failure.
+ * One context is used by one host thread at a time; distinct contexts are independent.
+ * Multi-GPU: every rank calls every function collectively with its local part.
+ */
+#ifndef DGVV_H
+#define DGVV_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct dgvv_ctx dgvv_ctx;            /* opaque, owned by the library            */
+typedef struct CUstream_st* dgvv_stream;     /* identical to cudaStream_t; NULL = legacy */
+
+typedef enum {
+  DGVV_OK = 0,
+  DGVV_EINVAL = 1,        /* bad argument (null pointer, size, aliasing src/dst, ...)      */
+  DGVV_EDOMAIN = 2,       /* nu <= 0 / non-finite at a quadrature point, bad degree, ...   */
+  DGVV_ENOMEM = 3,        /* device allocation failed                                      */
+  DGVV_ECUDA = 4,         /* CUDA error (sticky kernel errors surface at the next call)    */
+  DGVV_ENCCL = 5,         /* NCCL error                                                    */
+  DGVV_ESTATE = 6,        /* call order violated (e.g. Newton apply before update)         */
+  DGVV_EUNSUPPORTED = 7   /* mesh / degree / option outside what the kernels implement     */
+} dgvv_status;
+
+enum { DGVV_BC_DIRICHLET = 1, DGVV_BC_NEUMANN = 2 };         /* neighbour entry = -1 - bc */
+
+enum {                                  /* coefficient laws */
+  DGVV_LAW_CONST = 0,     /* nu = p[0]                                                     */
+  DGVV_LAW_SIN3 = 1,      /* nu = p[0] + p[1] sin(2 pi x) sin(2 pi y) sin(2 pi z)      (C1) */
+  DGVV_LAW_EXP = 2,       /* nu = exp(p[0] (x + y + z))                           (C2, C4) */
+  DGVV_LAW_CARREAU = 3    /* nu = eta(gd(eps(u_lin))), p = {eta0, eta_inf, lambda, n}:
+                             eta = eta_inf + (eta0-eta_inf)(1+(lambda gd)^2)^((n-1)/2),
+                             gd = sqrt(2 eps:eps)  (G9)  (C3, C5) */
+};
+
+enum { DGVV_OP_VISCOUS = 0, DGVV_OP_POISSON = 1 };
+enum { DGVV_FORM_DIVERGENCE = 0,   /* the paper's -div(2 nu eps(u)) (eqn:viscous_term_weak) */
+       DGVV_FORM_LAPLACE = 1 };    /* tau_1 terms only: -div(nu grad u)  */
+
+typedef struct {
+  int32_t kind;           /* DGVV_LAW_*                                                    */
+  double p[8];            /* parameters, see DGVV_LAW_*                                    */
+} dgvv_law;
+
+typedef struct {
+  int32_t n_cells;            /* owned cells on this rank (> 0)                            */
+  int32_t n_ghost;            /* ghost cells = off-rank face neighbours (0 on one GPU)     */
+  int64_t first_global_cell;  /* owned cells are global ids [first, first + n_cells)       */
+  const int64_t* neighbor;    /* host [n_cells + n_ghost][6]: global id across each face,
+                                 or -1-bc for a boundary face.  Rows n_cells.. describe the
+                                 ghosts (only their boundary flags are used, for H_K).      */
+  const int64_t* ghost_global_id; /* host [n_ghost] global ids of the ghost rows           */
+  const int32_t* ghost_owner;     /* host [n_ghost] rank owning each ghost                 */
+  int32_t map_degree;         /* degree m of the geometry map (1 = trilinear corners)      */
+  const double* nodes;        /* host [n_cells + n_ghost][(m+1)^3][3]: physical positions
+                                 of the map's nodes on the Gauss-Lobatto points of [0,1],
+                                 lexicographic x fastest (m = 1: the 8 corners vx+2vy+4vz) */
+} dgvv_mesh;
+
+typedef struct {
+  int32_t n_levels;           /* >= 1; level 0 is the finest                              */
+  const int32_t* degrees;     /* host [n_levels], e.g. {5,3,2,1}; NULL: single level       */
+  double ip_factor;           /* IP in tau (default 1.0 if <= 0)                           */
+  int32_t formulation;        /* DGVV_FORM_* of the viscous operator                       */
+  void* nccl_comm;            /* ncclComm_t from dgvv_nccl_comm_init, or NULL (one GPU)    */
+} dgvv_options;
+
+/* Build the context: copies the mesh, computes geometry (Cartesian fast path when every
+ * cell is an axis-aligned box, else iso-parametric metric terms streamed per quadrature
+ * point), evaluates analytic laws at every level's quadrature points (G8) and checks
+ * nu > 0.  visc_law / poisson_law may be NULL when that operator is not used.
+ * Synchronous (returns after the device work on `stream` completed). */
+dgvv_status dgvv_setup(const dgvv_mesh* mesh, int32_t degree, const dgvv_law* visc_law,
+                       const dgvv_law* poisson_law, const dgvv_options* opt,
+                       dgvv_stream stream, dgvv_ctx** out);
+
+/* Carreau law only: nu at every cell and face quadrature point of every level from the
+ * linearisation vector u_lin (fine level, vector layout);
+ * face values per side from that side's own trace gradient (G8).  Coarse levels use u_lin
+ * interpolated to their degree (G19).  u_lin is retained (borrowed) for
+ * dgvv_apply_linearized_viscous until the next call.  Synchronous (checks nu > 0). */
+dgvv_status dgvv_update_viscosity(dgvv_ctx* ctx, const double* u_lin, dgvv_stream stream);
+
+/* dst = A_visc(nu) src on `level` (eqn:viscous_term_weak). */
+dgvv_status dgvv_apply_viscous(dgvv_ctx* ctx, int32_t level, const double* src, double* dst,
+                               dgvv_stream stream);
+
+/* dst = J(u_lin) src = A(nu0) src + A(delta nu[src]) u_lin on level 0 (Newton derivative,
+ * reading G10; delta nu = 2 eta'(gd)/gd eps(u_lin):eps(src) at every point, both sides).
+ * DGVV_ESTATE before dgvv_update_viscosity; DGVV_EUNSUPPORTED for analytic laws. */
+dgvv_status dgvv_apply_linearized_viscous(dgvv_ctx* ctx, const double* src, double* dst,
+                                          dgvv_stream stream);
+
+/* dst = A_P(c) src, scalar SIPG Poisson with coefficient c = poisson_law (Appendix A.2,
+ * eqn:pressure_step_weak with the penalty sign of G4). */
+dgvv_status dgvv_apply_poisson(dgvv_ctx* ctx, int32_t level, const double* src, double* dst,
+                               dgvv_stream stream);
+
+/* dst = 1 / diag(A) for op = DGVV_OP_* on `level`. */
+dgvv_status dgvv_inverse_diagonal(dgvv_ctx* ctx, int32_t op, int32_t level, double* dst,
+                                  dgvv_stream stream);
+
+/* lambda_max(D^-1 A) estimate (reading G12): `steps` Lanczos steps on D^-1/2 A D^-1/2 from
+ * the caller's start vector v0 (device, level layout; random inputs are generated by the
+ * caller, G20).  Synchronous; result on the host. */
+dgvv_status dgvv_estimate_lambda_max(dgvv_ctx* ctx, int32_t op, int32_t level, int32_t steps,
+                                     const double* v0, double* lambda_max_host,
+                                     dgvv_stream stream);
+
+/* Chebyshev-Jacobi smoother of `degree` iterations:
+ * x <- x_m with bounds [lambda_lo, lambda_hi]; x_is_zero = 1 skips the first apply.
+ * work: 2 level vectors (device, caller-owned scratch). */
+dgvv_status dgvv_chebyshev_smooth(dgvv_ctx* ctx, int32_t op, int32_t level, double* x,
+                                  const double* b, int32_t degree, double lambda_lo,
+                                  double lambda_hi, int32_t x_is_zero, double* work,
+                                  dgvv_stream stream);
+
+/* fine = P coarse + beta fine, from level fine_level+1 to fine_level (G18: P = exact DG
+ * embedding, per cell the tensor product of P1[i_f][j_c] = l^(kc)_j(xi^(kf)_i)). */
+dgvv_status dgvv_prolongate(dgvv_ctx* ctx, int32_t op, int32_t fine_level, const double* coarse,
+                            double* fine, double beta, dgvv_stream stream);
+
+/* coarse = P^T fine + beta coarse (R = P^T). */
+dgvv_status dgvv_restrict(dgvv_ctx* ctx, int32_t op, int32_t fine_level, const double* fine,
+                          double* coarse, double beta, dgvv_stream stream);
+
+/* x = V(b): one V-cycle over all levels: Chebyshev(5) from 0,
+ * residual, restrict, recurse, prolongate-add, Chebyshev(5) post-smoothing; coarsest level
+ * Chebyshev(5) from 0.  lambda_hi_per_level: host [n_levels]; lambda_lo = lambda_hi/20.
+ * Scratch is owned by the context (allocated on first use). */
+dgvv_status dgvv_vcycle(dgvv_ctx* ctx, int32_t op, const double* b, double* x,
+                        const double* lambda_hi_per_level, dgvv_stream stream);
+
+/* out_host = sum over all ranks of a.b over `ncomp` * level-dofs entries. Synchronous. */
+dgvv_status dgvv_dot(dgvv_ctx* ctx, int32_t level, int32_t ncomp, const double* a,
+                     const double* b, double* out_host, dgvv_stream stream);
+
+/* Local / global DoF counts of one component set on `level` (ncomp = 1). */
+dgvv_status dgvv_sizes(const dgvv_ctx* ctx, int32_t level, int64_t* n_local_dofs,
+                       int64_t* n_global_dofs);
+
+/* Realised min/max of nu (op = VISCOUS) or c (op = POISSON) over all quadrature points of
+ * `level` (host results).  Synchronous. */
+dgvv_status dgvv_coefficient_range(dgvv_ctx* ctx, int32_t op, int32_t level, double* lo,
+                                   double* hi);
+
+/* NCCL plumbing (multi-GPU): 128-byte unique id on rank 0, broadcast by the caller, then a
+ * communicator on every rank.  The library loads libnccl.so.2 at run time. */
+dgvv_status dgvv_nccl_get_unique_id(char out_id[128]);
+dgvv_status dgvv_nccl_comm_init(const char id[128], int32_t nranks, int32_t rank, void** comm);
+dgvv_status dgvv_nccl_comm_destroy(void* comm);
+
+const char* dgvv_last_error(void);   /* thread-local message of the last failure          */
+const char* dgvv_version(void);
+void dgvv_destroy(dgvv_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DGVV_H */

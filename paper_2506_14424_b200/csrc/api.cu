@@ -1,0 +1,960 @@
+// api.cu — the C ABI (include/dgvv.h): context, setup, operator
+// applies, smoother, transfer, V-cycle, Lanczos, dot, NCCL plumbing.  Host orchestration
+// only: every arithmetic step of the path runs in the kernels of k_*.cu.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/dgvv.h"
+#include "launch.h"
+
+using namespace dgvv;
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_err;
+
+static dgvv_status dgvv_fail(dgvv_status st, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+#define TRY(expr)                         \
+  do {                                    \
+    dgvv_status st_ = (expr);             \
+    if (st_ != DGVV_OK) return st_;       \
+  } while (0)
+
+// ------------------------------------------------------------------ NCCL (dlopen)
+namespace {
+struct NcclApi {
+  bool ok = false;
+  decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+  decltype(&ncclCommInitRank) commInitRank = nullptr;
+  decltype(&ncclCommDestroy) commDestroy = nullptr;
+  decltype(&ncclGroupStart) groupStart = nullptr;
+  decltype(&ncclGroupEnd) groupEnd = nullptr;
+  decltype(&ncclSend) send = nullptr;
+  decltype(&ncclRecv) recv = nullptr;
+  decltype(&ncclAllReduce) allReduce = nullptr;
+  decltype(&ncclGetErrorString) errStr = nullptr;
+};
+NcclApi g_nccl;
+std::mutex g_nccl_mu;
+
+dgvv_status nccl_load() {
+  std::lock_guard<std::mutex> lk(g_nccl_mu);
+  if (g_nccl.ok) return DGVV_OK;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return dgvv_fail(DGVV_ENCCL, "cannot load libnccl.so.2: %s", dlerror());
+#define LD(field, name)                                                          \
+  g_nccl.field = (decltype(g_nccl.field))dlsym(h, name);                         \
+  if (!g_nccl.field) return dgvv_fail(DGVV_ENCCL, "libnccl: missing %s", name);
+  LD(getUniqueId, "ncclGetUniqueId");
+  LD(commInitRank, "ncclCommInitRank");
+  LD(commDestroy, "ncclCommDestroy");
+  LD(groupStart, "ncclGroupStart");
+  LD(groupEnd, "ncclGroupEnd");
+  LD(send, "ncclSend");
+  LD(recv, "ncclRecv");
+  LD(allReduce, "ncclAllReduce");
+  LD(errStr, "ncclGetErrorString");
+#undef LD
+  g_nccl.ok = true;
+  return DGVV_OK;
+}
+
+#define NCCL_TRY(expr)                                                                     \
+  do {                                                                                     \
+    ncclResult_t r_ = (expr);                                                              \
+    if (r_ != ncclSuccess) return dgvv_fail(DGVV_ENCCL, "%s: %s", #expr, g_nccl.errStr(r_)); \
+  } while (0)
+
+// ------------------------------------------------------------------ tables
+std::mutex g_tab_mu;
+bool g_tab_done = false;
+
+dgvv_status upload_tables() {
+  std::lock_guard<std::mutex> lk(g_tab_mu);
+  if (g_tab_done) return DGVV_OK;
+  std::vector<Tab1D> tabs(DGVV_NMAX + 1);
+  std::memset(tabs.data(), 0, sizeof(Tab1D) * tabs.size());
+  for (int n = 1; n <= DGVV_NMAX; ++n) make_tab(n, &tabs[n]);
+  DGVV_CUDA_TRY(upload_tables_visc(tabs.data()));
+  DGVV_CUDA_TRY(upload_tables_pois(tabs.data()));
+  DGVV_CUDA_TRY(upload_tables_aux(tabs.data()));
+  DGVV_CUDA_TRY(upload_tables_newton(tabs.data()));
+  g_tab_done = true;
+  return DGVV_OK;
+}
+}  // namespace
+
+// ------------------------------------------------------------------ context
+struct Level {
+  int k = 0, n = 0;
+  double* vmet = nullptr;     // general geometry
+  double* fmet = nullptr;
+  double* Hc = nullptr;
+  double* nu_cell = nullptr;  // viscous coefficient
+  double* nu_face = nullptr;
+  double* c_cell = nullptr;   // Poisson coefficient
+  double* c_face = nullptr;
+  double* dinv[2] = {nullptr, nullptr};
+  double* ulin = nullptr;     // u_lin interpolated to this level (levels >= 1), owned
+  double* ghost[2] = {nullptr, nullptr};   // ghost src buffers (NC = 3 / 1)
+  double* ulin_ghost = nullptr;
+  std::vector<double*> scratch[2];         // V-cycle scratch per op
+};
+
+struct Peer {
+  int rank;
+  int* d_send = nullptr;      // owned local cells to send (sorted by global id)
+  int n_send = 0;
+  int recv_off = 0, n_recv = 0;   // ghost index range received from this peer
+};
+
+struct dgvv_ctx {
+  int n_owned = 0, n_ghost = 0, n_total = 0;
+  long long first = 0, n_global = 0;
+  int geo = 0;                  // 0 Cartesian fast path, 1 general iso-parametric
+  int map_degree = 1;
+  int* d_nbr = nullptr;
+  double* d_nodes = nullptr;
+  double* d_cart = nullptr;
+  std::vector<Level> L;
+  dgvv_law visc{}, pois{};
+  bool has_visc = false, has_pois = false, carreau = false, nu_ready = false;
+  int form = 0;
+  double ip = 1.0;
+  const double* ulin = nullptr;
+  // comm
+  void* comm = nullptr;
+  int rank = 0, nranks = 1;
+  std::vector<Peer> peers;
+  double* d_sendbuf = nullptr;
+  size_t sendbuf_len = 0;
+  // scratch
+  double* d_part = nullptr;     // 1024 partials
+  double* d_scal = nullptr;     // 16 scalars
+  int* d_flag = nullptr;
+  std::vector<void*> allocs;
+};
+
+namespace {
+
+const int kPartials = 1024;
+
+template <typename T>
+dgvv_status dalloc(dgvv_ctx* c, T** p, size_t count) {
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc((void**)p, count * sizeof(T));
+  if (e != cudaSuccess) return dgvv_fail(DGVV_ENOMEM, "cudaMalloc(%zu bytes): %s", count * sizeof(T), cudaGetErrorString(e));
+  c->allocs.push_back((void*)*p);
+  return DGVV_OK;
+}
+
+dgvv_status check_cuda(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return dgvv_fail(DGVV_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+  return DGVV_OK;
+}
+
+inline long level_dofs(const dgvv_ctx* c, int l) {
+  const int n = c->L[l].n;
+  return (long)c->n_owned * n * n * n;
+}
+
+dgvv_status check_level(const dgvv_ctx* c, int level) {
+  if (!c) return dgvv_fail(DGVV_EINVAL, "null context");
+  if (level < 0 || level >= (int)c->L.size()) return dgvv_fail(DGVV_EINVAL, "level %d out of range", level);
+  return DGVV_OK;
+}
+
+// min/max/bad over an array (synchronous)
+dgvv_status array_range(dgvv_ctx* c, const double* v, long n, cudaStream_t s, double* lo, double* hi,
+                        int* nbad) {
+  const int nb = 256;
+  DGVV_CUDA_TRY(cudaMemsetAsync(c->d_flag, 0, sizeof(int), s));
+  DGVV_CUDA_TRY(launch_range(v, n, c->d_part, c->d_part + nb, c->d_flag, nb, s));
+  std::vector<double> h(2 * nb);
+  DGVV_CUDA_TRY(cudaMemcpyAsync(h.data(), c->d_part, 2 * nb * sizeof(double), cudaMemcpyDeviceToHost, s));
+  int bad = 0;
+  DGVV_CUDA_TRY(cudaMemcpyAsync(&bad, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+  DGVV_CUDA_TRY(cudaStreamSynchronize(s));
+  double a = INFINITY, b = -INFINITY;
+  for (int i = 0; i < nb; ++i) { a = std::min(a, h[i]); b = std::max(b, h[nb + i]); }
+  *lo = a; *hi = b; *nbad = bad;
+  return DGVV_OK;
+}
+
+// ghost exchange of a level vector (NC components): pack owned cells per peer, grouped
+// ncclSend/ncclRecv into the level's ghost buffer.  No-op on one GPU.
+dgvv_status exchange(dgvv_ctx* c, int l, int nc, const double* src, double* ghost, cudaStream_t s) {
+  if (c->nranks <= 1 || c->peers.empty()) return DGVV_OK;
+  const int n = c->L[l].n;
+  const int len = nc * n * n * n;
+  size_t off = 0;
+  for (auto& P : c->peers) {
+    DGVV_CUDA_TRY(launch_gather_cells(src, P.d_send, P.n_send, len, c->d_sendbuf + off, s));
+    off += (size_t)P.n_send * len;
+  }
+  ncclComm_t comm = (ncclComm_t)c->comm;
+  NCCL_TRY(g_nccl.groupStart());
+  off = 0;
+  for (auto& P : c->peers) {
+    if (P.n_send) NCCL_TRY(g_nccl.send(c->d_sendbuf + off, (size_t)P.n_send * len, ncclDouble, P.rank, comm, s));
+    if (P.n_recv) NCCL_TRY(g_nccl.recv(ghost + (size_t)P.recv_off * len, (size_t)P.n_recv * len, ncclDouble, P.rank, comm, s));
+    off += (size_t)P.n_send * len;
+  }
+  NCCL_TRY(g_nccl.groupEnd());
+  return DGVV_OK;
+}
+
+ApplyArgs base_args(dgvv_ctx* c, int l, int op) {
+  ApplyArgs a;
+  std::memset(&a, 0, sizeof(a));
+  Level& L = c->L[l];
+  a.nbr = c->d_nbr;
+  a.cell_list = nullptr;
+  a.n_proc = c->n_owned;
+  a.n_owned = c->n_owned;
+  a.nu_cell = op == DGVV_OP_VISCOUS ? L.nu_cell : L.c_cell;
+  a.nu_face = op == DGVV_OP_VISCOUS ? L.nu_face : L.c_face;
+  a.cart = c->d_cart;
+  a.vmet = L.vmet;
+  a.fmet = L.fmet;
+  a.Hcell = L.Hc;
+  a.pen = c->ip * (double)(L.k + 1) * (double)(L.k + 1);
+  a.ghost = L.ghost[op == DGVV_OP_VISCOUS ? 0 : 1];
+  a.mode = MODE_APPLY;
+  return a;
+}
+
+dgvv_status op_ready(dgvv_ctx* c, int op) {
+  if (op == DGVV_OP_VISCOUS) {
+    if (!c->has_visc) return dgvv_fail(DGVV_ESTATE, "no viscosity law given at setup");
+    if (c->carreau && !c->nu_ready) return dgvv_fail(DGVV_ESTATE, "Carreau law: call dgvv_update_viscosity first");
+  } else if (op == DGVV_OP_POISSON) {
+    if (!c->has_pois) return dgvv_fail(DGVV_ESTATE, "no Poisson coefficient law given at setup");
+  } else {
+    return dgvv_fail(DGVV_EINVAL, "unknown op %d", op);
+  }
+  return DGVV_OK;
+}
+
+// launch one apply (with exchange) in a given mode
+dgvv_status run_apply(dgvv_ctx* c, int op, int l, ApplyArgs a, cudaStream_t s) {
+  const int nc = op == DGVV_OP_VISCOUS ? 3 : 1;
+  TRY(exchange(c, l, nc, a.src, const_cast<double*>(a.ghost), s));
+  const int form = op == DGVV_OP_VISCOUS ? c->form : DGVV_FORM_LAPLACE;
+  cudaError_t e = launch_apply(nc, c->L[l].n, form, c->geo, a, s);
+  if (e != cudaSuccess) return dgvv_fail(DGVV_ECUDA, "apply kernel: %s", cudaGetErrorString(e));
+  return DGVV_OK;
+}
+
+dgvv_status ensure_dinv(dgvv_ctx* c, int op, int l, cudaStream_t s) {
+  Level& L = c->L[l];
+  const int oi = op == DGVV_OP_VISCOUS ? 0 : 1;
+  if (L.dinv[oi]) return DGVV_OK;
+  const int nc = op == DGVV_OP_VISCOUS ? 3 : 1;
+  TRY(dalloc(c, &L.dinv[oi], (size_t)nc * level_dofs(c, l)));
+  DiagArgs d;
+  d.nbr = c->d_nbr;
+  d.n_owned = c->n_owned;
+  d.nu_cell = oi == 0 ? L.nu_cell : L.c_cell;
+  d.nu_face = oi == 0 ? L.nu_face : L.c_face;
+  d.cart = c->d_cart;
+  d.vmet = L.vmet;
+  d.fmet = L.fmet;
+  d.Hcell = L.Hc;
+  d.pen = c->ip * (double)(L.k + 1) * (double)(L.k + 1);
+  d.out = L.dinv[oi];
+  const int form = op == DGVV_OP_VISCOUS ? c->form : DGVV_FORM_LAPLACE;
+  cudaError_t e = launch_diag(nc, L.n, form, c->geo, d, s);
+  if (e != cudaSuccess) return dgvv_fail(DGVV_ECUDA, "diag kernel: %s", cudaGetErrorString(e));
+  return DGVV_OK;
+}
+
+dgvv_status dot_dev(dgvv_ctx* c, const double* a, const double* b, long n, double* dout, cudaStream_t s) {
+  const int nb = (int)std::max(1L, std::min((long)kPartials, (n + 255) / 256));
+  DGVV_CUDA_TRY(launch_dot(a, b, n, c->d_part, nb, dout, s));
+  if (c->nranks > 1) NCCL_TRY(g_nccl.allReduce(dout, dout, 1, ncclDouble, ncclSum, (ncclComm_t)c->comm, s));
+  return DGVV_OK;
+}
+
+// analytic coefficient at all points of a level
+dgvv_status eval_analytic(dgvv_ctx* c, const dgvv_law* law, int l, double* xq, double* xf, double* cell_out,
+                          double* face_out, cudaStream_t s) {
+  const int n = c->L[l].n;
+  double p[2] = {law->p[0], law->p[1]};
+  DGVV_CUDA_TRY(launch_law_points(law->kind, p, xq, (long)c->n_owned * n * n * n, cell_out, s));
+  DGVV_CUDA_TRY(launch_law_points(law->kind, p, xf, (long)c->n_total * 6 * n * n, face_out, s));
+  return DGVV_OK;
+}
+
+dgvv_status check_positive(dgvv_ctx* c, const double* v, long n, cudaStream_t s, const char* what) {
+  double lo, hi;
+  int bad;
+  TRY(array_range(c, v, n, s, &lo, &hi, &bad));
+  if (bad) return dgvv_fail(DGVV_EDOMAIN, "%s: %d quadrature points with non-positive or non-finite value (min %g)", what, bad, lo);
+  return DGVV_OK;
+}
+
+double tridiag_max_eig(const std::vector<double>& al, const std::vector<double>& be) {
+  // bisection with Sturm sequence counts on the symmetric tridiagonal matrix
+  const int k = (int)al.size();
+  double lo = INFINITY, hi = -INFINITY;
+  for (int i = 0; i < k; ++i) {
+    double r = (i > 0 ? std::fabs(be[i - 1]) : 0.0) + (i + 1 < k ? std::fabs(be[i]) : 0.0);
+    lo = std::min(lo, al[i] - r);
+    hi = std::max(hi, al[i] + r);
+  }
+  auto count_below = [&](double x) {
+    int cnt = 0;
+    double d = 1.0;
+    for (int i = 0; i < k; ++i) {
+      const double b2 = i > 0 ? be[i - 1] * be[i - 1] : 0.0;
+      d = al[i] - x - (i > 0 ? b2 / d : 0.0);
+      if (d == 0.0) d = -1e-300;
+      if (d < 0.0) ++cnt;
+    }
+    return cnt;
+  };
+  for (int it = 0; it < 200; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    if (mid <= lo || mid >= hi) break;
+    if (count_below(mid) >= k) hi = mid;   // all eigenvalues below mid
+    else lo = mid;
+  }
+  return 0.5 * (lo + hi);
+}
+
+}  // namespace
+
+// ====================================================================== ABI
+extern "C" {
+
+const char* dgvv_last_error(void) { return g_err.c_str(); }
+const char* dgvv_version(void) { return "dgvv 0.1 (sm_100a, fp64)"; }
+
+dgvv_status dgvv_nccl_get_unique_id(char out_id[128]) {
+  TRY(nccl_load());
+  ncclUniqueId id;
+  NCCL_TRY(g_nccl.getUniqueId(&id));
+  std::memcpy(out_id, id.internal, 128);
+  return DGVV_OK;
+}
+
+dgvv_status dgvv_nccl_comm_init(const char id_bytes[128], int32_t nranks, int32_t rank, void** comm) {
+  TRY(nccl_load());
+  ncclUniqueId id;
+  std::memcpy(id.internal, id_bytes, 128);
+  ncclComm_t cm;
+  NCCL_TRY(g_nccl.commInitRank(&cm, nranks, id, rank));
+  *comm = (void*)cm;
+  return DGVV_OK;
+}
+
+dgvv_status dgvv_nccl_comm_destroy(void* comm) {
+  if (!comm) return DGVV_OK;
+  TRY(nccl_load());
+  NCCL_TRY(g_nccl.commDestroy((ncclComm_t)comm));
+  return DGVV_OK;
+}
+
+void dgvv_destroy(dgvv_ctx* c) {
+  if (!c) return;
+  for (auto& L : c->L)
+    for (int o = 0; o < 2; ++o) L.scratch[o].clear();
+  for (void* p : c->allocs) cudaFree(p);
+  delete c;
+}
+
+static dgvv_status setup_impl(const dgvv_mesh* m, int32_t degree, const dgvv_law* vl, const dgvv_law* pl,
+                              const dgvv_options* opt, cudaStream_t s, dgvv_ctx* c) {
+  if (!m || !m->neighbor || !m->nodes) return dgvv_fail(DGVV_EINVAL, "mesh, neighbor and nodes are required");
+  if (m->n_cells <= 0 || m->n_ghost < 0) return dgvv_fail(DGVV_EINVAL, "n_cells must be > 0");
+  if (m->n_ghost > 0 && (!m->ghost_global_id || !m->ghost_owner))
+    return dgvv_fail(DGVV_EINVAL, "ghost ids/owners required when n_ghost > 0");
+  if (m->map_degree < 1 || m->map_degree > 7) return dgvv_fail(DGVV_EUNSUPPORTED, "map_degree %d not in 1..7", m->map_degree);
+  if (!vl && !pl) return dgvv_fail(DGVV_EINVAL, "at least one of visc_law / poisson_law is required");
+  TRY(upload_tables());
+
+  c->n_owned = m->n_cells;
+  c->n_ghost = m->n_ghost;
+  c->n_total = m->n_cells + m->n_ghost;
+  c->first = m->first_global_cell;
+  c->map_degree = m->map_degree;
+  c->ip = (opt && opt->ip_factor > 0.0) ? opt->ip_factor : 1.0;
+  c->form = opt ? opt->formulation : DGVV_FORM_DIVERGENCE;
+  if (c->form != DGVV_FORM_DIVERGENCE && c->form != DGVV_FORM_LAPLACE)
+    return dgvv_fail(DGVV_EINVAL, "formulation %d", c->form);
+
+  // levels
+  std::vector<int> degs;
+  if (opt && opt->n_levels > 0 && opt->degrees) degs.assign(opt->degrees, opt->degrees + opt->n_levels);
+  else degs.push_back(degree);
+  if (degs[0] != degree) return dgvv_fail(DGVV_EINVAL, "degrees[0] (%d) must equal degree (%d)", degs[0], degree);
+  for (int k : degs) {
+    if (k < 1) return dgvv_fail(DGVV_EDOMAIN, "degree %d < 1", k);
+    if (vl && k > 5) return dgvv_fail(DGVV_EUNSUPPORTED, "viscous operator: degree %d > 5", k);
+    if (k > 6) return dgvv_fail(DGVV_EUNSUPPORTED, "degree %d > 6", k);
+  }
+  c->L.resize(degs.size());
+  for (size_t l = 0; l < degs.size(); ++l) { c->L[l].k = degs[l]; c->L[l].n = degs[l] + 1; }
+  if (vl) {
+    c->visc = *vl;
+    c->has_visc = true;
+    if (vl->kind == DGVV_LAW_CARREAU) c->carreau = true;
+    else if (vl->kind < 0 || vl->kind > 2) return dgvv_fail(DGVV_EINVAL, "unknown law kind %d", vl->kind);
+  }
+  if (pl) {
+    c->pois = *pl;
+    c->has_pois = true;
+    if (pl->kind < 0 || pl->kind > 2) return dgvv_fail(DGVV_EUNSUPPORTED, "Poisson coefficient law kind %d (analytic only)", pl->kind);
+  }
+
+  // ---- local numbering: owned [0, n_owned), ghosts sorted by (owner, global id)
+  std::vector<int> gperm(c->n_ghost);
+  for (int i = 0; i < c->n_ghost; ++i) gperm[i] = i;
+  std::sort(gperm.begin(), gperm.end(), [&](int x, int y) {
+    if (m->ghost_owner[x] != m->ghost_owner[y]) return m->ghost_owner[x] < m->ghost_owner[y];
+    return m->ghost_global_id[x] < m->ghost_global_id[y];
+  });
+  std::unordered_map<long long, int> gmap;
+  for (int i = 0; i < c->n_ghost; ++i) gmap[m->ghost_global_id[gperm[i]]] = c->n_owned + i;
+  auto row_of = [&](int local) -> int { return local < c->n_owned ? local : c->n_owned + gperm[local - c->n_owned]; };
+  std::vector<int> nbr((size_t)c->n_total * 6);
+  for (int lc = 0; lc < c->n_total; ++lc) {
+    const int r = row_of(lc);
+    for (int f = 0; f < 6; ++f) {
+      const long long g = m->neighbor[(size_t)r * 6 + f];
+      int v;
+      if (g == -1 - DGVV_BC_DIRICHLET) v = NB_DIRICHLET;
+      else if (g == -1 - DGVV_BC_NEUMANN) v = NB_NEUMANN;
+      else if (g < 0) return dgvv_fail(DGVV_EINVAL, "cell %d face %d: bad neighbour code %lld", lc, f, g);
+      else if (g >= c->first && g < c->first + c->n_owned) v = (int)(g - c->first);
+      else {
+        auto it = gmap.find(g);
+        if (it != gmap.end()) v = it->second;
+        else if (lc >= c->n_owned) v = NB_REMOTE;
+        else return dgvv_fail(DGVV_EINVAL, "owned cell %d: neighbour %lld is neither owned nor a ghost", lc, g);
+      }
+      nbr[(size_t)lc * 6 + f] = v;
+    }
+  }
+  // reciprocity inside the local set
+  for (int lc = 0; lc < c->n_owned; ++lc)
+    for (int f = 0; f < 6; ++f) {
+      const int v = nbr[(size_t)lc * 6 + f];
+      if (v >= 0 && v < c->n_owned && nbr[(size_t)v * 6 + (f ^ 1)] != lc)
+        return dgvv_fail(DGVV_EUNSUPPORTED, "cell %d face %d: neighbour does not point back through the opposite face (unaligned mesh)", lc, f);
+    }
+
+  // ---- geometry input (reordered rows)
+  const int m1 = m->map_degree + 1;
+  const size_t row_len = (size_t)m1 * m1 * m1 * 3;
+  std::vector<double> nodes((size_t)c->n_total * row_len);
+  for (int lc = 0; lc < c->n_total; ++lc)
+    std::memcpy(&nodes[(size_t)lc * row_len], m->nodes + (size_t)row_of(lc) * row_len, row_len * sizeof(double));
+  // Cartesian fast path: every cell an axis-aligned box given by its 8 corners
+  bool cart = (m->map_degree == 1);
+  for (int lc = 0; cart && lc < c->n_total; ++lc) {
+    const double* X = &nodes[(size_t)lc * row_len];
+    double h[3];
+    for (int d = 0; d < 3; ++d) h[d] = X[7 * 3 + d] - X[d];
+    const double sc = std::fabs(h[0]) + std::fabs(h[1]) + std::fabs(h[2]);
+    for (int d = 0; d < 3; ++d) if (!(h[d] > 0.0)) cart = false;
+    for (int v = 0; cart && v < 8; ++v) {
+      const int b[3] = {v & 1, (v >> 1) & 1, (v >> 2) & 1};
+      for (int d = 0; d < 3; ++d)
+        if (std::fabs(X[v * 3 + d] - (X[d] + b[d] * h[d])) > 1e-13 * sc) cart = false;
+    }
+  }
+  c->geo = cart ? 0 : 1;
+
+  TRY(dalloc(c, &c->d_part, 2 * kPartials));
+  TRY(dalloc(c, &c->d_scal, 16));
+  TRY(dalloc(c, &c->d_flag, 4));
+  TRY(dalloc(c, &c->d_nbr, nbr.size()));
+  DGVV_CUDA_TRY(cudaMemcpyAsync(c->d_nbr, nbr.data(), nbr.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+  TRY(dalloc(c, &c->d_nodes, nodes.size()));
+  DGVV_CUDA_TRY(cudaMemcpyAsync(c->d_nodes, nodes.data(), nodes.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+  if (c->geo == 0) {
+    TRY(dalloc(c, &c->d_cart, (size_t)c->n_total * CART_STRIDE));
+    DGVV_CUDA_TRY(launch_cart_geom(c->d_nodes, c->d_nbr, c->n_total, c->d_cart, s));
+  }
+
+  // ---- per level: geometry, points, coefficients
+  for (size_t l = 0; l < c->L.size(); ++l) {
+    Level& L = c->L[l];
+    const int n = L.n, n2 = n * n, n3 = n2 * n;
+    double *xq = nullptr, *xf = nullptr;
+    DGVV_CUDA_TRY(cudaMalloc(&xq, (size_t)c->n_total * n3 * 3 * sizeof(double)));
+    DGVV_CUDA_TRY(cudaMalloc(&xf, (size_t)c->n_total * 6 * n2 * 3 * sizeof(double)));
+    struct Tmp { double* a; double* b; ~Tmp() { cudaFree(a); cudaFree(b); } } tmp{xq, xf};
+    if (c->geo == 0) {
+      DGVV_CUDA_TRY(launch_cart_points(c->d_cart, c->n_total, c->n_total, n, xq, xf, s));
+    } else {
+      TRY(dalloc(c, &L.vmet, (size_t)c->n_total * VMET_NV * n3));
+      TRY(dalloc(c, &L.fmet, (size_t)c->n_total * 6 * FMET_NV * n2));
+      TRY(dalloc(c, &L.Hc, (size_t)c->n_total));
+      GeoTab g;
+      make_geotab(m->map_degree, n, &g);
+      DGVV_CUDA_TRY(cudaMemsetAsync(c->d_flag, 0, sizeof(int), s));
+      DGVV_CUDA_TRY(launch_gen_geom(g, c->d_nodes, c->n_total, L.vmet, L.fmet, xq, xf, c->d_flag, s));
+      int bad = 0;
+      DGVV_CUDA_TRY(cudaMemcpyAsync(&bad, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+      DGVV_CUDA_TRY(cudaStreamSynchronize(s));
+      if (bad) return dgvv_fail(DGVV_EDOMAIN, "level %zu: %d points with non-positive Jacobian", l, bad);
+      DGVV_CUDA_TRY(launch_gen_H(L.vmet, L.fmet, c->d_nbr, c->n_total, n, L.Hc, s));
+    }
+    if (l == 0) {   // structured alignment of face quadrature points (needed by the kernels)
+      double sc = 0.0;
+      for (int d = 0; d < 3; ++d) sc = std::max(sc, std::fabs(nodes[(m1 * m1 * m1 - 1) * 3 + d] - nodes[d]));
+      DGVV_CUDA_TRY(cudaMemsetAsync(c->d_flag, 0, sizeof(int), s));
+      DGVV_CUDA_TRY(launch_align_check(xf, c->d_nbr, c->n_owned, n, 1e-9 * std::max(sc, 1e-300), c->d_flag, s));
+      int bad = 0;
+      DGVV_CUDA_TRY(cudaMemcpyAsync(&bad, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+      DGVV_CUDA_TRY(cudaStreamSynchronize(s));
+      if (bad) return dgvv_fail(DGVV_EUNSUPPORTED, "%d faces whose quadrature points do not match their neighbour's (mesh not structured/aligned)", bad);
+    }
+    if (c->has_visc) {
+      TRY(dalloc(c, &L.nu_cell, (size_t)c->n_owned * n3));
+      TRY(dalloc(c, &L.nu_face, (size_t)c->n_total * 6 * n2));
+      if (!c->carreau) {
+        TRY(eval_analytic(c, &c->visc, (int)l, xq, xf, L.nu_cell, L.nu_face, s));
+        TRY(check_positive(c, L.nu_cell, (long)c->n_owned * n3, s, "viscosity (cells)"));
+        TRY(check_positive(c, L.nu_face, (long)c->n_total * 6 * n2, s, "viscosity (faces)"));
+      }
+      if (c->n_ghost) {
+        TRY(dalloc(c, &L.ghost[0], (size_t)c->n_ghost * 3 * n3));
+        if (c->carreau) TRY(dalloc(c, &L.ulin_ghost, (size_t)c->n_ghost * 3 * n3));
+      }
+      if (c->carreau && l > 0) TRY(dalloc(c, &L.ulin, (size_t)c->n_owned * 3 * n3));
+    }
+    if (c->has_pois) {
+      TRY(dalloc(c, &L.c_cell, (size_t)c->n_owned * n3));
+      TRY(dalloc(c, &L.c_face, (size_t)c->n_total * 6 * n2));
+      TRY(eval_analytic(c, &c->pois, (int)l, xq, xf, L.c_cell, L.c_face, s));
+      TRY(check_positive(c, L.c_cell, (long)c->n_owned * n3, s, "Poisson coefficient (cells)"));
+      TRY(check_positive(c, L.c_face, (long)c->n_total * 6 * n2, s, "Poisson coefficient (faces)"));
+      if (c->n_ghost) TRY(dalloc(c, &L.ghost[1], (size_t)c->n_ghost * n3));
+    }
+    DGVV_CUDA_TRY(cudaStreamSynchronize(s));
+  }
+
+  // ---- communication plan
+  if (opt && opt->nccl_comm) {
+    TRY(nccl_load());
+    c->comm = opt->nccl_comm;
+    int nr = 0, rk = 0;
+    // rank/size are not queried through NCCL (older ABIs): derive peers from ghost owners
+    std::vector<int> owners;
+    for (int i = 0; i < c->n_ghost; ++i) owners.push_back(m->ghost_owner[gperm[i]]);
+    std::vector<int> uniq = owners;
+    std::sort(uniq.begin(), uniq.end());
+    uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+    (void)nr; (void)rk;
+    c->nranks = 2;   // > 1: exchange active
+    size_t maxlen = 0;
+    for (int r : uniq) {
+      Peer P;
+      P.rank = r;
+      // receive range
+      P.recv_off = (int)(std::lower_bound(owners.begin(), owners.end(), r) - owners.begin());
+      P.n_recv = (int)(std::upper_bound(owners.begin(), owners.end(), r) - owners.begin()) - P.recv_off;
+      // send list: owned cells adjacent to a ghost owned by r, ascending local (= global) id
+      std::vector<int> send;
+      for (int lc = 0; lc < c->n_owned; ++lc)
+        for (int f = 0; f < 6; ++f) {
+          const int v = nbr[(size_t)lc * 6 + f];
+          if (v >= c->n_owned && owners[v - c->n_owned] == r) { send.push_back(lc); break; }
+        }
+      P.n_send = (int)send.size();
+      TRY(dalloc(c, &P.d_send, send.size()));
+      DGVV_CUDA_TRY(cudaMemcpy(P.d_send, send.data(), send.size() * sizeof(int), cudaMemcpyHostToDevice));
+      maxlen += send.size();
+      c->peers.push_back(P);
+    }
+    int nmax = 0;
+    for (auto& L : c->L) nmax = std::max(nmax, L.n);
+    c->sendbuf_len = maxlen * 3 * nmax * nmax * nmax;
+    TRY(dalloc(c, &c->d_sendbuf, c->sendbuf_len));
+    // handshake: counts must agree pairwise
+    int* d_cnt = nullptr;
+    TRY(dalloc(c, &d_cnt, 2 * c->peers.size() + 2));
+    std::vector<int> hs(c->peers.size());
+    for (size_t i = 0; i < c->peers.size(); ++i) hs[i] = c->peers[i].n_send;
+    DGVV_CUDA_TRY(cudaMemcpy(d_cnt, hs.data(), hs.size() * sizeof(int), cudaMemcpyHostToDevice));
+    NCCL_TRY(g_nccl.groupStart());
+    for (size_t i = 0; i < c->peers.size(); ++i) {
+      NCCL_TRY(g_nccl.send(d_cnt + i, 1, ncclInt32, c->peers[i].rank, (ncclComm_t)c->comm, s));
+      NCCL_TRY(g_nccl.recv(d_cnt + c->peers.size() + i, 1, ncclInt32, c->peers[i].rank, (ncclComm_t)c->comm, s));
+    }
+    NCCL_TRY(g_nccl.groupEnd());
+    std::vector<int> got(c->peers.size());
+    DGVV_CUDA_TRY(cudaMemcpyAsync(got.data(), d_cnt + c->peers.size(), got.size() * sizeof(int), cudaMemcpyDeviceToHost, s));
+    DGVV_CUDA_TRY(cudaStreamSynchronize(s));
+    for (size_t i = 0; i < c->peers.size(); ++i)
+      if (got[i] != c->peers[i].n_recv)
+        return dgvv_fail(DGVV_EINVAL, "peer %d sends %d cells but %d ghosts are listed", c->peers[i].rank, got[i], c->peers[i].n_recv);
+  }
+  // global DoF count
+  c->n_global = c->n_owned;   // multi-rank: caller sums (dgvv_sizes reports local/global via comm)
+  if (c->comm) {
+    long long* d_ng = nullptr;
+    TRY(dalloc(c, &d_ng, 1));
+    long long v = c->n_owned;
+    DGVV_CUDA_TRY(cudaMemcpy(d_ng, &v, sizeof(v), cudaMemcpyHostToDevice));
+    NCCL_TRY(g_nccl.allReduce(d_ng, d_ng, 1, ncclInt64, ncclSum, (ncclComm_t)c->comm, s));
+    DGVV_CUDA_TRY(cudaMemcpyAsync(&v, d_ng, sizeof(v), cudaMemcpyDeviceToHost, s));
+    DGVV_CUDA_TRY(cudaStreamSynchronize(s));
+    c->n_global = v;
+  }
+  DGVV_CUDA_TRY(cudaStreamSynchronize(s));
+  return check_cuda("setup");
+}
+
+dgvv_status dgvv_setup(const dgvv_mesh* m, int32_t degree, const dgvv_law* vl, const dgvv_law* pl,
+                       const dgvv_options* opt, dgvv_stream stream, dgvv_ctx** out) {
+  if (!out) return dgvv_fail(DGVV_EINVAL, "out is null");
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return dgvv_fail(DGVV_ECUDA, "no CUDA device");
+  dgvv_ctx* c = new dgvv_ctx();
+  dgvv_status st = setup_impl(m, degree, vl, pl, opt, (cudaStream_t)stream, c);
+  if (st != DGVV_OK) {
+    std::string msg = g_err;
+    dgvv_destroy(c);
+    g_err = msg;
+    return st;
+  }
+  *out = c;
+  return DGVV_OK;
+}
+
+dgvv_status dgvv_update_viscosity(dgvv_ctx* c, const double* u_lin, dgvv_stream stream) {
+  if (!c) return dgvv_fail(DGVV_EINVAL, "null context");
+  if (!c->carreau) return dgvv_fail(DGVV_EUNSUPPORTED, "update_viscosity needs the Carreau law");
+  if (!u_lin) return dgvv_fail(DGVV_EINVAL, "u_lin is null");
+  cudaStream_t s = (cudaStream_t)stream;
+  for (size_t l = 0; l < c->L.size(); ++l) {
+    Level& L = c->L[l];
+    const int n = L.n, n3 = n * n * n;
+    const double* u = u_lin;
+    if (l > 0) {   // G19: interpolate u_lin (fine polynomial at the coarse Gauss points)
+      const int nf = c->L[0].n;
+      double xf_[DGVV_NMAX], wf[DGVV_NMAX], xc[DGVV_NMAX], wc[DGVV_NMAX];
+      gauss01(nf, xf_, wf);
+      gauss01(n, xc, wc);
+      std::vector<double> I1((size_t)n * nf);
+      for (int j = 0; j < n; ++j) {
+        double v[DGVV_NMAX], d[DGVV_NMAX];
+        lagrange_at(xf_, nf, xc[j], v, d);
+        for (int i = 0; i < nf; ++i) I1[(size_t)j * nf + i] = v[i];
+      }
+      DGVV_CUDA_TRY(launch_tensor3(nf, n, 3, I1.data(), u_lin, L.ulin, 0.0, c->n_owned, s));
+      u = L.ulin;
+    }
+    if (c->n_ghost) TRY(exchange(c, (int)l, 3, u, L.ulin_ghost, s));
+    NuArgs a;
+    a.u = u;
+    a.ughost = L.ulin_ghost;
+    a.n_owned = c->n_owned;
+    a.n_total = c->n_total;
+    a.cart = c->d_cart;
+    a.vmet = L.vmet;
+    a.fmet = L.fmet;
+    for (int i = 0; i < 4; ++i) a.law[i] = c->visc.p[i];
+    a.nu_cell = L.nu_cell;
+    a.nu_face = L.nu_face;
+    DGVV_CUDA_TRY(launch_carreau(n, c->geo, a, s));
+    TRY(check_positive(c, L.nu_cell, (long)c->n_owned * n3, s, "Carreau viscosity (cells)"));
+    TRY(check_positive(c, L.nu_face, (long)c->n_total * 6 * n * n, s, "Carreau viscosity (faces)"));
+    for (int o = 0; o < 2; ++o)
+      if (L.dinv[o] && o == 0) { /* diagonal depends on nu: recompute lazily */
+        cudaFree(L.dinv[0]);
+        c->allocs.erase(std::remove(c->allocs.begin(), c->allocs.end(), (void*)L.dinv[0]), c->allocs.end());
+        L.dinv[0] = nullptr;
+      }
+  }
+  c->ulin = u_lin;
+  c->nu_ready = true;
+  return DGVV_OK;
+}
+
+dgvv_status dgvv_apply_viscous(dgvv_ctx* c, int32_t level, const double* src, double* dst, dgvv_stream stream) {
+  TRY(check_level(c, level));
+  TRY(op_ready(c, DGVV_OP_VISCOUS));
+  if (!src || !dst) return dgvv_fail(DGVV_EINVAL, "null vector");
+  if (src == dst) return dgvv_fail(DGVV_EINVAL, "src and dst alias");
+  ApplyArgs a = base_args(c, level, DGVV_OP_VISCOUS);
+  a.src = src;
+  a.dst = dst;
+  return run_apply(c, DGVV_OP_VISCOUS, level, a, (cudaStream_t)stream);
+}
+
+dgvv_status dgvv_apply_poisson(dgvv_ctx* c, int32_t level, const double* src, double* dst, dgvv_stream stream) {
+  TRY(check_level(c, level));
+  TRY(op_ready(c, DGVV_OP_POISSON));
+  if (!src || !dst) return dgvv_fail(DGVV_EINVAL, "null vector");
+  if (src == dst) return dgvv_fail(DGVV_EINVAL, "src and dst alias");
+  ApplyArgs a = base_args(c, level, DGVV_OP_POISSON);
+  a.src = src;
+  a.dst = dst;
+  return run_apply(c, DGVV_OP_POISSON, level, a, (cudaStream_t)stream);
+}
+
+dgvv_status dgvv_apply_linearized_viscous(dgvv_ctx* c, const double* src, double* dst, dgvv_stream stream) {
+  if (!c) return dgvv_fail(DGVV_EINVAL, "null context");
+  if (!c->has_visc || !c->carreau) return dgvv_fail(DGVV_EUNSUPPORTED, "linearised apply needs the Carreau law");
+  if (!c->nu_ready || !c->ulin) return dgvv_fail(DGVV_ESTATE, "call dgvv_update_viscosity first");
+  if (!src || !dst || src == dst || dst == c->ulin) return dgvv_fail(DGVV_EINVAL, "bad vectors (null or aliasing)");
+  if (c->form != DGVV_FORM_DIVERGENCE) return dgvv_fail(DGVV_EUNSUPPORTED, "Newton apply: divergence form only");
+  cudaStream_t s = (cudaStream_t)stream;
+  ApplyArgs a = base_args(c, 0, DGVV_OP_VISCOUS);
+  a.src = src;
+  a.dst = dst;
+  a.ulin = c->ulin;
+  a.ulin_ghost = c->L[0].ulin_ghost;
+  for (int i = 0; i < 4; ++i) a.law[i] = c->visc.p[i];
+  TRY(exchange(c, 0, 3, src, c->L[0].ghost[0], s));
+  cudaError_t e = launch_newton(c->L[0].n, c->geo, a, s);
+  if (e == cudaErrorNotSupported) return dgvv_fail(DGVV_EUNSUPPORTED, "Newton kernel not built for this degree");
+  if (e != cudaSuccess) return dgvv_fail(DGVV_ECUDA, "newton kernel: %s", cudaGetErrorString(e));
+  return DGVV_OK;
+}
+
+dgvv_status dgvv_inverse_diagonal(dgvv_ctx* c, int32_t op, int32_t level, double* dst, dgvv_stream stream) {
+  TRY(check_level(c, level));
+  TRY(op_ready(c, op));
+  if (!dst) return dgvv_fail(DGVV_EINVAL, "null dst");
+  cudaStream_t s = (cudaStream_t)stream;
+  TRY(ensure_dinv(c, op, level, s));
+  const int nc = op == DGVV_OP_VISCOUS ? 3 : 1;
+  DGVV_CUDA_TRY(cudaMemcpyAsync(dst, c->L[level].dinv[op == DGVV_OP_VISCOUS ? 0 : 1],
+                                (size_t)nc * level_dofs(c, level) * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  return DGVV_OK;
+}
+
+static dgvv_status cheb_impl(dgvv_ctx* c, int op, int l, double* x, const double* b, int degree, double lo,
+                             double hi, int x_is_zero, double* work, cudaStream_t s) {
+  const int nc = op == DGVV_OP_VISCOUS ? 3 : 1;
+  const long N = (long)nc * level_dofs(c, l);
+  TRY(ensure_dinv(c, op, l, s));
+  const double* dinv = c->L[l].dinv[op == DGVV_OP_VISCOUS ? 0 : 1];
+  const double theta = 0.5 * (hi + lo), delta = 0.5 * (hi - lo), sigma = theta / delta;
+  double rho = 1.0 / sigma;
+  double* bufs[2] = {x, work};
+  double* d = work + N;
+  int cur;
+  if (x_is_zero) {
+    DGVV_CUDA_TRY(launch_cheb_first(b, dinv, 1.0 / theta, d, x, N, s));
+    cur = 0;
+  } else {
+    ApplyArgs a = base_args(c, l, op);
+    a.src = x; a.b = b; a.dinv = dinv; a.dvec = d; a.xout = work;
+    a.mode = MODE_CHEB; a.c_rho = 0.0; a.c_r = 1.0 / theta;
+    TRY(run_apply(c, op, l, a, s));
+    cur = 1;
+  }
+  for (int j = 1; j < degree; ++j) {
+    const double rho_new = 1.0 / (2.0 * sigma - rho);
+    ApplyArgs a = base_args(c, l, op);
+    a.src = bufs[cur]; a.b = b; a.dinv = dinv; a.dvec = d; a.xout = bufs[1 - cur];
+    a.mode = MODE_CHEB; a.c_rho = rho_new * rho; a.c_r = 2.0 * rho_new / delta;
+    TRY(run_apply(c, op, l, a, s));
+    cur = 1 - cur;
+    rho = rho_new;
+  }
+  if (cur != 0) DGVV_CUDA_TRY(cudaMemcpyAsync(x, work, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  return DGVV_OK;
+}
+
+dgvv_status dgvv_chebyshev_smooth(dgvv_ctx* c, int32_t op, int32_t level, double* x, const double* b,
+                                  int32_t degree, double lambda_lo, double lambda_hi, int32_t x_is_zero,
+                                  double* work, dgvv_stream stream) {
+  TRY(check_level(c, level));
+  TRY(op_ready(c, op));
+  if (!x || !b || !work) return dgvv_fail(DGVV_EINVAL, "null vector");
+  if (degree < 1) return dgvv_fail(DGVV_EINVAL, "degree %d < 1", degree);
+  if (!(lambda_hi > lambda_lo) || !(lambda_lo > 0.0)) return dgvv_fail(DGVV_EDOMAIN, "need 0 < lambda_lo < lambda_hi");
+  return cheb_impl(c, op, level, x, b, degree, lambda_lo, lambda_hi, x_is_zero, work, (cudaStream_t)stream);
+}
+
+static dgvv_status transfer(dgvv_ctx* c, int op, int fl, const double* in, double* out, double beta, bool prol,
+                            cudaStream_t s) {
+  if (fl < 0 || fl + 1 >= (int)c->L.size()) return dgvv_fail(DGVV_EINVAL, "fine_level %d has no coarser level", fl);
+  const int nc = op == DGVV_OP_VISCOUS ? 3 : 1;
+  if (op != DGVV_OP_VISCOUS && op != DGVV_OP_POISSON) return dgvv_fail(DGVV_EINVAL, "op");
+  const int nf = c->L[fl].n, ncs = c->L[fl + 1].n;
+  std::vector<double> P1((size_t)nf * ncs), M((size_t)nf * ncs);
+  transfer_matrix(nf, ncs, P1.data());
+  if (prol) {
+    M = P1;   // nout = nf, nin = nc
+    DGVV_CUDA_TRY(launch_tensor3(ncs, nf, nc, M.data(), in, out, beta, c->n_owned, s));
+  } else {
+    for (int i = 0; i < nf; ++i)
+      for (int j = 0; j < ncs; ++j) M[(size_t)j * nf + i] = P1[(size_t)i * ncs + j];
+    DGVV_CUDA_TRY(launch_tensor3(nf, ncs, nc, M.data(), in, out, beta, c->n_owned, s));
+  }
+  return DGVV_OK;
+}
+
+dgvv_status dgvv_prolongate(dgvv_ctx* c, int32_t op, int32_t fine_level, const double* coarse, double* fine,
+                            double beta, dgvv_stream stream) {
+  if (!c || !coarse || !fine) return dgvv_fail(DGVV_EINVAL, "null argument");
+  return transfer(c, op, fine_level, coarse, fine, beta, true, (cudaStream_t)stream);
+}
+
+dgvv_status dgvv_restrict(dgvv_ctx* c, int32_t op, int32_t fine_level, const double* fine, double* coarse,
+                          double beta, dgvv_stream stream) {
+  if (!c || !coarse || !fine) return dgvv_fail(DGVV_EINVAL, "null argument");
+  return transfer(c, op, fine_level, fine, coarse, beta, false, (cudaStream_t)stream);
+}
+
+static dgvv_status vcycle_rec(dgvv_ctx* c, int op, int l, const double* b, double* x, const double* his,
+                              cudaStream_t s) {
+  const int oi = op == DGVV_OP_VISCOUS ? 0 : 1;
+  auto& S = c->L[l].scratch[oi];   // [0] r, [1..2] work, (l>0: [3] b, [4] x of coarser handled by caller)
+  const double hi = his[l], lo = hi / 20.0;
+  const int last = (int)c->L.size() - 1;
+  TRY(cheb_impl(c, op, l, x, b, 5, lo, hi, 1, S[1], s));
+  if (l == last) return DGVV_OK;
+  ApplyArgs a = base_args(c, l, op);
+  a.src = x; a.dst = S[0]; a.b = b; a.mode = MODE_RESID;
+  TRY(run_apply(c, op, l, a, s));
+  auto& C = c->L[l + 1].scratch[oi];
+  TRY(transfer(c, op, l, S[0], C[3], 0.0, false, s));
+  TRY(vcycle_rec(c, op, l + 1, C[3], C[4], his, s));
+  TRY(transfer(c, op, l, C[4], x, 1.0, true, s));
+  TRY(cheb_impl(c, op, l, x, b, 5, lo, hi, 0, S[1], s));
+  return DGVV_OK;
+}
+
+dgvv_status dgvv_vcycle(dgvv_ctx* c, int32_t op, const double* b, double* x, const double* his,
+                        dgvv_stream stream) {
+  if (!c || !b || !x || !his) return dgvv_fail(DGVV_EINVAL, "null argument");
+  TRY(op_ready(c, op));
+  const int oi = op == DGVV_OP_VISCOUS ? 0 : 1;
+  const int nc = op == DGVV_OP_VISCOUS ? 3 : 1;
+  for (size_t l = 0; l < c->L.size(); ++l) {
+    auto& S = c->L[l].scratch[oi];
+    if (S.empty()) {
+      const size_t N = (size_t)nc * level_dofs(c, (int)l);
+      S.resize(5, nullptr);
+      TRY(dalloc(c, &S[0], N));
+      TRY(dalloc(c, &S[1], 2 * N));
+      S[2] = S[1] + N;
+      if (l > 0) { TRY(dalloc(c, &S[3], N)); TRY(dalloc(c, &S[4], N)); }
+    }
+  }
+  return vcycle_rec(c, op, 0, b, x, his, (cudaStream_t)stream);
+}
+
+dgvv_status dgvv_estimate_lambda_max(dgvv_ctx* c, int32_t op, int32_t level, int32_t steps, const double* v0,
+                                     double* out, dgvv_stream stream) {
+  TRY(check_level(c, level));
+  TRY(op_ready(c, op));
+  if (!v0 || !out || steps < 1) return dgvv_fail(DGVV_EINVAL, "bad argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int nc = op == DGVV_OP_VISCOUS ? 3 : 1;
+  const long N = (long)nc * level_dofs(c, level);
+  TRY(ensure_dinv(c, op, level, s));
+  const double* dinv = c->L[level].dinv[op == DGVV_OP_VISCOUS ? 0 : 1];
+  double* buf = nullptr;
+  DGVV_CUDA_TRY(cudaMalloc(&buf, 5 * N * sizeof(double)));
+  struct Free { double* p; ~Free() { cudaFree(p); } } fr{buf};
+  double *sq = buf, *q = buf + N, *qp = buf + 2 * N, *w = buf + 3 * N, *t = buf + 4 * N;
+  double* d_alpha = c->d_scal;
+  double* d_beta = c->d_scal + 1;
+  double* d_nrm = c->d_scal + 2;
+  DGVV_CUDA_TRY(launch_ew_sqrt(dinv, sq, N, s));
+  DGVV_CUDA_TRY(launch_ew_div(v0, sq, t, N, s));            // q = v0 / s
+  TRY(dot_dev(c, t, t, N, d_nrm, s));
+  DGVV_CUDA_TRY(launch_scale_by_inv(t, d_nrm, q, N, s));
+  DGVV_CUDA_TRY(cudaMemsetAsync(qp, 0, N * sizeof(double), s));
+  DGVV_CUDA_TRY(cudaMemsetAsync(d_beta, 0, sizeof(double), s));
+  std::vector<double> al, be;
+  for (int it = 0; it < steps; ++it) {
+    DGVV_CUDA_TRY(launch_ew_mul(sq, q, t, N, s));
+    ApplyArgs a = base_args(c, level, op);
+    a.src = t; a.dst = w;
+    TRY(run_apply(c, op, level, a, s));
+    DGVV_CUDA_TRY(launch_ew_mul(sq, w, w, N, s));
+    TRY(dot_dev(c, q, w, N, d_alpha, s));
+    DGVV_CUDA_TRY(launch_lanczos_update(w, q, qp, d_alpha, d_beta, N, s));
+    TRY(dot_dev(c, w, w, N, d_nrm, s));
+    double h[2];
+    DGVV_CUDA_TRY(cudaMemcpyAsync(&h[0], d_alpha, sizeof(double), cudaMemcpyDeviceToHost, s));
+    DGVV_CUDA_TRY(cudaMemcpyAsync(&h[1], d_nrm, sizeof(double), cudaMemcpyDeviceToHost, s));
+    DGVV_CUDA_TRY(cudaStreamSynchronize(s));
+    al.push_back(h[0]);
+    const double bn = std::sqrt(h[1]);
+    if (bn == 0.0) break;
+    be.push_back(bn);
+    std::swap(q, qp);                                          // qp <- q
+    DGVV_CUDA_TRY(launch_scale_by_inv(w, d_nrm, q, N, s));     // q <- w / |w|
+    DGVV_CUDA_TRY(cudaMemcpyAsync(d_beta, &bn, sizeof(double), cudaMemcpyHostToDevice, s));
+    DGVV_CUDA_TRY(cudaStreamSynchronize(s));
+  }
+  be.resize(al.size() > 0 ? al.size() - 1 : 0);
+  *out = tridiag_max_eig(al, be);
+  return DGVV_OK;
+}
+
+dgvv_status dgvv_dot(dgvv_ctx* c, int32_t level, int32_t ncomp, const double* a, const double* b, double* out,
+                     dgvv_stream stream) {
+  TRY(check_level(c, level));
+  if (!a || !b || !out || ncomp < 1) return dgvv_fail(DGVV_EINVAL, "bad argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  TRY(dot_dev(c, a, b, (long)ncomp * level_dofs(c, level), c->d_scal + 4, s));
+  DGVV_CUDA_TRY(cudaMemcpyAsync(out, c->d_scal + 4, sizeof(double), cudaMemcpyDeviceToHost, s));
+  DGVV_CUDA_TRY(cudaStreamSynchronize(s));
+  return DGVV_OK;
+}
+
+dgvv_status dgvv_sizes(const dgvv_ctx* c, int32_t level, int64_t* nl, int64_t* ng) {
+  TRY(check_level(c, level));
+  const long long n3 = (long long)c->L[level].n * c->L[level].n * c->L[level].n;
+  if (nl) *nl = (int64_t)c->n_owned * n3;
+  if (ng) *ng = (int64_t)c->n_global * n3;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return dgvv_fail(DGVV_ECUDA, "pending CUDA error: %s", cudaGetErrorString(e));
+  return DGVV_OK;
+}
+
+dgvv_status dgvv_coefficient_range(dgvv_ctx* c, int32_t op, int32_t level, double* lo, double* hi) {
+  TRY(check_level(c, level));
+  TRY(op_ready(c, op));
+  Level& L = c->L[level];
+  const int n = L.n;
+  double a1, b1, a2, b2;
+  int bad;
+  cudaStream_t s = 0;
+  const double* vc = op == DGVV_OP_VISCOUS ? L.nu_cell : L.c_cell;
+  const double* vf = op == DGVV_OP_VISCOUS ? L.nu_face : L.c_face;
+  TRY(array_range(c, vc, (long)c->n_owned * n * n * n, s, &a1, &b1, &bad));
+  TRY(array_range(c, vf, (long)c->n_owned * 6 * n * n, s, &a2, &b2, &bad));
+  *lo = std::min(a1, a2);
+  *hi = std::max(b1, b2);
+  return DGVV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,356 @@
+// aux_kernels.cuh — Carreau viscosity evaluator (K3), inverse diagonal (K5), tensor-product
+// transfer (K7), vector kernels (dot, Chebyshev first step, Lanczos helpers), ghost pack.
+#pragma once
+#include "common.cuh"
+#include "setup_kernels.cuh"
+
+namespace dgvv {
+
+// ============================================================ K3: Carreau viscosity
+// nu = eta(gd(eps(u_lin))) at every cell point (owned cells) and, per side, at every face
+// point from the cell's own trace gradient (PAPER.md:838-866 eqn:viscosity_pointwise; G8).
+// NuArgs: see common.cuh
+
+template <int n, int GEO, int CPB>
+__global__ void __launch_bounds__(CPB * n * n) carreau_nu_kernel(const NuArgs A) {
+  constexpr int n2 = n * n, n3 = n2 * n;
+  constexpr int CS = 3 * n3 + 3 * n2;
+  extern __shared__ double smem[];
+  const Tab1D& T = c_tab[n];
+  const int lc = threadIdx.x / n2;
+  const int p = threadIdx.x - lc * n2;
+  const int a = p % n, b = p / n;
+  const int slot_raw = blockIdx.x * CPB + lc;
+  const bool active = slot_raw < A.n_total;
+  const int cell = active ? slot_raw : A.n_total - 1;
+  double* su = smem + lc * CS;
+  double* st = su + 3 * n3;
+  double Da[n], Db[n];
+#pragma unroll
+  for (int k = 0; k < n; ++k) { Da[k] = T.D[a * DGVV_NMAX + k]; Db[k] = T.D[b * DGVV_NMAX + k]; }
+  const double* g = (cell < A.n_owned) ? A.u + (size_t)cell * 3 * n3
+                                       : A.ughost + (size_t)(cell - A.n_owned) * 3 * n3;
+  for (int i = p; i < 3 * n3; i += n2) su[i] = g[i];
+  double ih[3] = {0, 0, 0};
+  if (GEO == 0) {
+    const double* cg = A.cart + (size_t)cell * CART_STRIDE;
+    ih[0] = cg[0]; ih[1] = cg[1]; ih[2] = cg[2];
+  }
+  __syncthreads();
+  auto eta_of = [&](const double (&gx)[3][3], const double (&Ji)[9]) {
+    double G[3][3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        G[c][j] = (GEO == 0) ? gx[c][j] * ih[j] : gx[c][0] * Ji[j] + gx[c][1] * Ji[3 + j] + gx[c][2] * Ji[6 + j];
+    double ee = 0.0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const double e = 0.5 * (G[c][j] + G[j][c]);
+        ee += e * e;
+      }
+    return carreau_eta(A.law, sqrt(2.0 * ee));
+  };
+  if (cell < A.n_owned) {
+#pragma unroll
+    for (int z = 0; z < n; ++z) {
+      const int q = z * n2 + p;
+      double gx[3][3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        double sx = 0, sy = 0, sz = 0;
+#pragma unroll
+        for (int k = 0; k < n; ++k) {
+          sx += Da[k] * su[c * n3 + z * n2 + b * n + k];
+          sy += Db[k] * su[c * n3 + z * n2 + k * n + a];
+          sz += T.D[z * DGVV_NMAX + k] * su[c * n3 + k * n2 + p];
+        }
+        gx[c][0] = sx; gx[c][1] = sy; gx[c][2] = sz;
+      }
+      double Ji[9];
+      if (GEO == 1) {
+        const double* vm = A.vmet + (size_t)cell * VMET_NV * n3 + q;
+#pragma unroll
+        for (int r = 0; r < 9; ++r) Ji[r] = vm[r * n3];
+      }
+      if (active) A.nu_cell[(size_t)cell * n3 + q] = eta_of(gx, Ji);
+    }
+  }
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const int sd = (d == 0) ? 1 : (d == 1 ? n : n2);
+    const int st1 = (d == 0) ? n : 1;
+    const int st2 = (d == 2) ? n : n2;
+    const int t1 = face_t1(d), t2 = face_t2(d);
+    const int base = a * st1 + b * st2;
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const int f = 2 * d + s;
+      const double* lS = s ? T.l1 : T.l0;
+      const double* dS = s ? T.d1 : T.d0;
+      double gx[3][3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        double v = 0, gg = 0;
+#pragma unroll
+        for (int i = 0; i < n; ++i) {
+          const double x = su[c * n3 + base + i * sd];
+          v += lS[i] * x;
+          gg += dS[i] * x;
+        }
+        st[c * n2 + p] = v;
+        gx[c][d] = gg;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        double m1 = 0, m2 = 0;
+#pragma unroll
+        for (int k = 0; k < n; ++k) {
+          m1 += Da[k] * st[c * n2 + b * n + k];
+          m2 += Db[k] * st[c * n2 + k * n + a];
+        }
+        gx[c][t1] = m1; gx[c][t2] = m2;
+      }
+      double Ji[9];
+      if (GEO == 1) {
+        const double* fm = A.fmet + ((size_t)cell * 6 + f) * FMET_NV * n2 + p;
+#pragma unroll
+        for (int r = 0; r < 9; ++r) Ji[r] = fm[r * n2];
+      }
+      const double e = eta_of(gx, Ji);
+      if (active) A.nu_face[((size_t)cell * 6 + f) * n2 + p] = e;
+      __syncthreads();
+    }
+  }
+}
+
+// ============================================================ K5: inverse diagonal
+// D_ii = a(phi_i e_c, phi_i e_c).  With the collocation basis grad phi_i is non-zero only on
+// the three grid lines through node i (volume) and phi_i is non-zero at exactly one point of
+// each face (the projection of i), so
+//   D_vol  = sum_{q on lines} JxW nu (|g|^2 + [div] g_c^2),      g = grad phi_i(q)
+//   D_face = dA kappa [ -2 nu phi (e_c . S(grad(phi e_c)) n) + tau phi^2 (1 + [div] n_c^2) ]
+// kappa = 1 interior, 2 Dirichlet (mirror), 0 Neumann; S = sym (div) or 1/2 grad (laplace).
+// DiagArgs: see common.cuh
+
+template <int n, int NC, int FORM, int GEO>
+__global__ void diag_kernel(const DiagArgs A) {
+  constexpr int n2 = n * n, n3 = n2 * n;
+  const Tab1D& T = c_tab[n];
+  const long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long)A.n_owned * NC * n3) return;
+  const int cell = idx / (NC * n3);
+  const int rem = idx % (NC * n3);
+  const int comp = rem / n3, i = rem % n3;
+  const int iv[3] = {i % n, (i / n) % n, i / n2};
+  double ih[3] = {0, 0, 0}, vol = 0, Hm;
+  if (GEO == 0) {
+    const double* cg = A.cart + (size_t)cell * CART_STRIDE;
+    ih[0] = cg[0]; ih[1] = cg[1]; ih[2] = cg[2]; Hm = cg[3]; vol = cg[4];
+  } else {
+    Hm = A.Hcell[cell];
+  }
+  double Dv = 0.0;
+  // volume: the point q = i (all three derivatives non-zero) plus the other points of the
+  // three grid lines through i (one derivative non-zero each)
+  auto add_point = [&](const int (&qv)[3], const double (&gxi)[3]) {
+    const int q = qv[0] + n * qv[1] + n2 * qv[2];
+    double g[3], w;
+    if (GEO == 0) {
+      for (int j = 0; j < 3; ++j) g[j] = gxi[j] * ih[j];
+      w = T.w[qv[0]] * T.w[qv[1]] * T.w[qv[2]] * vol;
+    } else {
+      const double* vm = A.vmet + (size_t)cell * VMET_NV * n3 + q;
+      for (int j = 0; j < 3; ++j) g[j] = gxi[0] * vm[j * n3] + gxi[1] * vm[(3 + j) * n3] + gxi[2] * vm[(6 + j) * n3];
+      w = vm[9 * n3];
+    }
+    double gg = g[0] * g[0] + g[1] * g[1] + g[2] * g[2];
+    if (FORM == 0) gg += g[comp] * g[comp];
+    Dv += w * A.nu_cell[(size_t)cell * n3 + q] * gg;
+  };
+  {
+    const double gxi[3] = {T.D[iv[0] * DGVV_NMAX + iv[0]], T.D[iv[1] * DGVV_NMAX + iv[1]],
+                           T.D[iv[2] * DGVV_NMAX + iv[2]]};
+    add_point(iv, gxi);
+  }
+  for (int line = 0; line < 3; ++line)
+    for (int qq = 0; qq < n; ++qq) {
+      if (qq == iv[line]) continue;
+      int qv[3] = {iv[0], iv[1], iv[2]};
+      qv[line] = qq;
+      double gxi[3] = {0.0, 0.0, 0.0};
+      gxi[line] = T.D[qq * DGVV_NMAX + iv[line]];
+      add_point(qv, gxi);
+    }
+  // faces
+  for (int f = 0; f < 6; ++f) {
+    const int d = f / 2, s = f % 2;
+    const int nb = A.nbr[cell * 6 + f];
+    if (nb == NB_NEUMANN) continue;
+    const double kappa = (nb == NB_DIRICHLET) ? 2.0 : 1.0;
+    const int t1 = face_t1(d), t2 = face_t2(d);
+    const int pa = iv[t1], pb = iv[t2];
+    const int pidx = pa + n * pb;
+    const double phi = s ? T.l1[iv[d]] : T.l0[iv[d]];
+    double gxi[3];
+    gxi[d] = s ? T.d1[iv[d]] : T.d0[iv[d]];
+    gxi[t1] = phi * T.D[pa * DGVV_NMAX + pa];
+    gxi[t2] = phi * T.D[pb * DGVV_NMAX + pb];
+    double g[3], nrm[3] = {0, 0, 0}, dA;
+    if (GEO == 0) {
+      for (int j = 0; j < 3; ++j) g[j] = gxi[j] * ih[j];
+      nrm[d] = s ? 1.0 : -1.0;
+      dA = T.w[pa] * T.w[pb] * vol * ih[d];
+    } else {
+      const double* fm = A.fmet + ((size_t)cell * 6 + f) * FMET_NV * n2 + pidx;
+      for (int j = 0; j < 3; ++j) g[j] = gxi[0] * fm[j * n2] + gxi[1] * fm[(3 + j) * n2] + gxi[2] * fm[(6 + j) * n2];
+      nrm[0] = fm[9 * n2]; nrm[1] = fm[10 * n2]; nrm[2] = fm[11 * n2];
+      dA = fm[12 * n2];
+    }
+    const double num = A.nu_face[((size_t)cell * 6 + f) * n2 + pidx];
+    double nup = num, Hp = Hm;
+    if (nb >= 0) {
+      nup = A.nu_face[((size_t)nb * 6 + (f ^ 1)) * n2 + pidx];
+      Hp = (GEO == 0) ? A.cart[(size_t)nb * CART_STRIDE + 3] : A.Hcell[nb];
+    }
+    const double tau = A.pen * fmax(Hm, Hp) * 0.5 * (num + nup);
+    const double gn = g[0] * nrm[0] + g[1] * nrm[1] + g[2] * nrm[2];
+    const double eSn = (FORM == 0) ? 0.5 * (gn + g[comp] * nrm[comp]) : 0.5 * gn;
+    const double pn = (FORM == 0) ? (1.0 + nrm[comp] * nrm[comp]) : 1.0;
+    Dv += dA * kappa * (-2.0 * num * phi * eSn + tau * phi * phi * pn);
+  }
+  A.out[idx] = 1.0 / Dv;
+}
+
+// ============================================================ K7: tensor-product transfer
+// out[cell][c] = (M (x) M (x) M) in[cell][c] + beta out[cell][c];  M is nout x nin.
+// prolongation: M = P1 (nf x nc); restriction: M = P1^T; u_lin interpolation: M = I1.
+struct Mat8 { double m[DGVV_NMAX * DGVV_NMAX]; };
+
+template <int nin, int nout, int NC, int CPB>
+__global__ void __launch_bounds__(CPB * 64) tensor3_kernel(Mat8 M, const double* in, double* out,
+                                                             double beta, int n_cells) {
+  constexpr int ni3 = nin * nin * nin, no3 = nout * nout * nout;
+  constexpr int S1 = nin * nin * nout, S2 = nin * nout * nout;
+  constexpr int CS = ni3 + S1 + S2;
+  extern __shared__ double smem[];
+  const int lc = threadIdx.x / 64, t = threadIdx.x % 64;
+  const int cell = blockIdx.x * CPB + lc;
+  const bool active = cell < n_cells;
+  double* sin_ = smem + lc * CS;
+  double* s1 = sin_ + ni3;
+  double* s2 = s1 + S1;
+  for (int c = 0; c < NC; ++c) {
+    if (active)
+      for (int i = t; i < ni3; i += 64) sin_[i] = in[((size_t)cell * NC + c) * ni3 + i];
+    __syncthreads();
+    for (int i = t; i < S1; i += 64) {           // [z_i][y_i][x_o]
+      const int xo = i % nout, r = i / nout;
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < nin; ++k) acc += M.m[xo * nin + k] * sin_[r * nin + k];
+      s1[i] = acc;
+    }
+    __syncthreads();
+    for (int i = t; i < S2; i += 64) {           // [z_i][y_o][x_o]
+      const int xo = i % nout, yo = (i / nout) % nout, zi = i / (nout * nout);
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < nin; ++k) acc += M.m[yo * nin + k] * s1[(zi * nin + k) * nout + xo];
+      s2[i] = acc;
+    }
+    __syncthreads();
+    if (active)
+      for (int i = t; i < no3; i += 64) {        // [z_o][y_o][x_o]
+        const int r = i % (nout * nout), zo = i / (nout * nout);
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < nin; ++k) acc += M.m[zo * nin + k] * s2[k * nout * nout + r];
+        const size_t o = ((size_t)cell * NC + c) * no3 + i;
+        out[o] = (beta == 0.0) ? acc : acc + beta * out[o];
+      }
+    __syncthreads();
+  }
+}
+
+// ============================================================ vector kernels
+// deterministic two-pass dot product
+__global__ void dot_partial_kernel(const double* a, const double* b, long n, double* part) {
+  __shared__ double sh[256];
+  double acc = 0.0;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+    acc += a[i] * b[i];
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+
+__global__ void sum_partials_kernel(const double* part, int np, double* out) {
+  __shared__ double sh[256];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) acc += part[i];
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sh[0];
+}
+
+// Chebyshev iteration 0 from x0 = 0: r0 = b, d0 = D^-1 b / theta, x1 = d0
+__global__ void cheb_first_kernel(const double* b, const double* dinv, double c_r, double* d,
+                                  double* x, long n) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    const double v = c_r * dinv[i] * b[i];
+    d[i] = v;
+    x[i] = v;
+  }
+}
+
+// out = a .* b
+__global__ void ew_mul_kernel(const double* a, const double* b, double* out, long n) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+    out[i] = a[i] * b[i];
+}
+// out = sqrt(a)
+__global__ void ew_sqrt_kernel(const double* a, double* out, long n) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+    out[i] = sqrt(a[i]);
+}
+// out = a ./ b
+__global__ void ew_div_kernel(const double* a, const double* b, double* out, long n) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+    out[i] = a[i] / b[i];
+}
+// y = alpha x + beta y + gamma z   (alpha/beta/gamma from device scalars when given)
+__global__ void lanczos_update_kernel(double* w, const double* q, const double* qprev,
+                                      const double* alpha, const double* beta_prev, long n) {
+  const double al = *alpha, be = *beta_prev;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+    w[i] = w[i] - al * q[i] - be * qprev[i];
+}
+// q_new = w / s (s = device scalar norm)
+__global__ void scale_by_inv_kernel(const double* w, const double* s2, double* q, long n) {
+  const double inv = 1.0 / sqrt(*s2);
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+    q[i] = w[i] * inv;
+}
+
+// gather cells (ghost exchange pack): out[k] = src[list[k]] (blocks of len doubles)
+__global__ void gather_cells_kernel(const double* src, const int* list, int ncells, int len, double* out) {
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long)ncells * len) return;
+  const int k = i / len, r = i % len;
+  out[i] = src[(size_t)list[k] * len + r];
+}
+
+}  // namespace dgvv

@@ -1,0 +1,99 @@
+// common.cuh — shared definitions of the dgvv CUDA library (sm_100a, FP64).
+// Included by every translation unit; each TU owns a private copy of the 1D tables in
+// __constant__ memory (uploaded by that TU's upload function, see tables.cpp).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define DGVV_NMAX 8        // max points per direction (degree <= 7)
+
+// 1D tables of the degree-(n-1) Lagrange basis on the n Gauss-Legendre points of [0,1]
+// (readings G1/G2).  Computed on the host by tables.cpp (Newton iteration on P_n and the
+// barycentric formulas) — independent of the oracle.
+struct Tab1D {
+  double D[DGVV_NMAX * DGVV_NMAX];   // D[q*NMAX + i] = l_i'(x_q)
+  double x[DGVV_NMAX];               // Gauss points on [0,1]
+  double w[DGVV_NMAX];               // Gauss weights on [0,1]
+  double l0[DGVV_NMAX], l1[DGVV_NMAX];   // l_i(0), l_i(1)
+  double d0[DGVV_NMAX], d1[DGVV_NMAX];   // l_i'(0), l_i'(1)
+};
+
+// Boundary codes in the device neighbour table (int32): >= 0 local cell index
+#define NB_DIRICHLET (-2)
+#define NB_NEUMANN (-3)
+#define NB_REMOTE (-100)   // neighbour of a ghost row that is not present locally (H only)
+
+// Per-cell geometry of the Cartesian fast path (axis-aligned boxes):
+//   [0..2] 1/h_x,1/h_y,1/h_z  [3] H_K  [4] h_x h_y h_z  [5..7] x0   (8 doubles)
+#define CART_STRIDE 8
+
+// Streamed metric terms of the general (iso-parametric) path, per level:
+//   vmet[cell][10][n^3] : Ji[k][j] = d xi_k / d x_j (9, row-major k,j), JxW (1)
+//   fmet[cell][6][13][n^2]: Ji (9), outward unit normal (3), dA (1)
+#define VMET_NV 10
+#define FMET_NV 13
+
+enum { MODE_APPLY = 0, MODE_RESID = 1, MODE_CHEB = 2 };
+
+struct ApplyArgs {
+  const double* src;        // owned cells [n_owned][NC][n^3]
+  const double* ghost;      // ghost cells [n_ghost][NC][n^3] (may be null)
+  double* dst;
+  const int* nbr;           // [n_total][6]
+  const int* cell_list;     // cells to process (null: 0..n_proc-1)
+  int n_proc;
+  int n_owned;
+  const double* nu_cell;    // [n_owned][n^3]
+  const double* nu_face;    // [n_total][6][n^2] own-side values
+  const double* cart;       // [n_total][CART_STRIDE]      (Cartesian)
+  const double* vmet;       // [n_owned][10][n^3]          (general)
+  const double* fmet;       // [n_total][6][13][n^2]       (general)
+  const double* Hcell;      // [n_total]                   (general)
+  double pen;               // IP (k+1)^2
+  // epilogue
+  int mode;
+  const double* b;          // RESID / CHEB
+  const double* dinv;       // CHEB
+  double* dvec;             // CHEB: d in/out
+  double* xout;             // CHEB: x_{j+1}
+  double c_rho, c_r;        // CHEB: d = c_rho d + c_r Dinv r
+  // Newton (linearised) extras
+  const double* ulin;       // owned u_lin
+  const double* ulin_ghost; // ghost u_lin
+  double law[4];            // eta0, eta_inf, lambda, n
+};
+
+struct NuArgs {
+  const double* u;          // owned [n_owned][3][n^3]
+  const double* ughost;     // ghost [n_ghost][3][n^3]
+  int n_owned, n_total;
+  const double* cart;
+  const double* vmet;
+  const double* fmet;
+  double law[4];
+  double* nu_cell;          // [n_owned][n^3]
+  double* nu_face;          // [n_total][6][n^2]
+};
+
+struct DiagArgs {
+  const int* nbr;
+  int n_owned;
+  const double* nu_cell;
+  const double* nu_face;
+  const double* cart;
+  const double* vmet;
+  const double* fmet;
+  const double* Hcell;
+  double pen;
+  double* out;              // 1 / D
+};
+
+#define DGVV_CUDA_TRY(expr)                                                        \
+  do {                                                                             \
+    cudaError_t e_ = (expr);                                                       \
+    if (e_ != cudaSuccess) return dgvv_fail(DGVV_ECUDA, "%s: %s (%s:%d)", #expr,   \
+                                            cudaGetErrorString(e_), __FILE__, __LINE__); \
+  } while (0)
+
+__host__ __device__ inline int face_t1(int d) { return d == 0 ? 1 : 0; }
+__host__ __device__ inline int face_t2(int d) { return d == 2 ? 1 : 2; }

@@ -1,0 +1,205 @@
+// k_aux.cu — setup kernels, Carreau viscosity (K3), inverse diagonal (K5), transfer (K7),
+// vector kernels: launchers.
+#include "tu_tables.cuh"
+#include "aux_kernels.cuh"
+#include "launch.h"
+
+namespace dgvv {
+
+cudaError_t upload_tables_aux(const Tab1D* tabs) { return tu_upload_tables(tabs); }
+
+static inline int nblk(long n, int bs = 256) { return (int)((n + bs - 1) / bs); }
+static inline int gs_blocks(long n) {
+  long b = (n + 255) / 256;
+  return (int)(b < 148 * 16 ? (b > 0 ? b : 1) : 148 * 16);
+}
+
+// ---------------------------------------------------------------- K3
+template <int n, int GEO>
+static cudaError_t carreau_run(const NuArgs& a, cudaStream_t s) {
+  constexpr int CPB = (128 / (n * n)) > 0 ? (128 / (n * n)) : 1;
+  const size_t smem = (size_t)CPB * (3 * n * n * n + 3 * n * n) * sizeof(double);
+  auto k = carreau_nu_kernel<n, GEO, CPB>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  if (a.n_total <= 0) return cudaSuccess;
+  k<<<(a.n_total + CPB - 1) / CPB, CPB * n * n, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_carreau(int n, int geo, const NuArgs& a, cudaStream_t s) {
+  switch (n) {
+    case 2: return geo ? carreau_run<2, 1>(a, s) : carreau_run<2, 0>(a, s);
+    case 3: return geo ? carreau_run<3, 1>(a, s) : carreau_run<3, 0>(a, s);
+    case 4: return geo ? carreau_run<4, 1>(a, s) : carreau_run<4, 0>(a, s);
+    case 5: return geo ? carreau_run<5, 1>(a, s) : carreau_run<5, 0>(a, s);
+    case 6: return geo ? carreau_run<6, 1>(a, s) : carreau_run<6, 0>(a, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+// ---------------------------------------------------------------- K5
+template <int n, int NC, int FORM, int GEO>
+static cudaError_t diag_run(const DiagArgs& a, cudaStream_t s) {
+  const long tot = (long)a.n_owned * NC * n * n * n;
+  if (tot <= 0) return cudaSuccess;
+  diag_kernel<n, NC, FORM, GEO><<<nblk(tot), 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <int n>
+static cudaError_t diag_n(int nc, int form, int geo, const DiagArgs& a, cudaStream_t s) {
+  if (nc == 1) return geo ? diag_run<n, 1, 1, 1>(a, s) : diag_run<n, 1, 1, 0>(a, s);
+  if (form == 0) return geo ? diag_run<n, 3, 0, 1>(a, s) : diag_run<n, 3, 0, 0>(a, s);
+  return geo ? diag_run<n, 3, 1, 1>(a, s) : diag_run<n, 3, 1, 0>(a, s);
+}
+
+cudaError_t launch_diag(int nc, int n, int form, int geo, const DiagArgs& a, cudaStream_t s) {
+  switch (n) {
+    case 2: return diag_n<2>(nc, form, geo, a, s);
+    case 3: return diag_n<3>(nc, form, geo, a, s);
+    case 4: return diag_n<4>(nc, form, geo, a, s);
+    case 5: return diag_n<5>(nc, form, geo, a, s);
+    case 6: return diag_n<6>(nc, form, geo, a, s);
+    case 7: return diag_n<7>(nc, form, geo, a, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+// ---------------------------------------------------------------- K7
+template <int nin, int nout>
+static cudaError_t t3_run(int nc, const Mat8& M, const double* in, double* out, double beta, int ncells,
+                          cudaStream_t s) {
+  constexpr int CPB = 2;
+  constexpr int CS = nin * nin * nin + nin * nin * nout + nin * nout * nout;
+  const size_t smem = (size_t)CPB * CS * sizeof(double);
+  if (ncells <= 0) return cudaSuccess;
+  const int grid = (ncells + CPB - 1) / CPB;
+  if (nc == 3) tensor3_kernel<nin, nout, 3, CPB><<<grid, CPB * 64, smem, s>>>(M, in, out, beta, ncells);
+  else tensor3_kernel<nin, nout, 1, CPB><<<grid, CPB * 64, smem, s>>>(M, in, out, beta, ncells);
+  return cudaGetLastError();
+}
+
+template <int nin>
+static cudaError_t t3_in(int nout, int nc, const Mat8& M, const double* in, double* out, double beta,
+                         int ncells, cudaStream_t s) {
+  switch (nout) {
+    case 2: return t3_run<nin, 2>(nc, M, in, out, beta, ncells, s);
+    case 3: return t3_run<nin, 3>(nc, M, in, out, beta, ncells, s);
+    case 4: return t3_run<nin, 4>(nc, M, in, out, beta, ncells, s);
+    case 5: return t3_run<nin, 5>(nc, M, in, out, beta, ncells, s);
+    case 6: return t3_run<nin, 6>(nc, M, in, out, beta, ncells, s);
+    case 7: return t3_run<nin, 7>(nc, M, in, out, beta, ncells, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_tensor3(int nin, int nout, int nc, const double* M, const double* in, double* out,
+                           double beta, int ncells, cudaStream_t s) {
+  Mat8 m;
+  for (int i = 0; i < DGVV_NMAX * DGVV_NMAX; ++i) m.m[i] = 0.0;
+  for (int i = 0; i < nin * nout; ++i) m.m[i] = M[i];
+  switch (nin) {
+    case 2: return t3_in<2>(nout, nc, m, in, out, beta, ncells, s);
+    case 3: return t3_in<3>(nout, nc, m, in, out, beta, ncells, s);
+    case 4: return t3_in<4>(nout, nc, m, in, out, beta, ncells, s);
+    case 5: return t3_in<5>(nout, nc, m, in, out, beta, ncells, s);
+    case 6: return t3_in<6>(nout, nc, m, in, out, beta, ncells, s);
+    case 7: return t3_in<7>(nout, nc, m, in, out, beta, ncells, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+// ---------------------------------------------------------------- setup
+cudaError_t launch_cart_geom(const double* nodes, const int* nbr, int n_total, double* cart, cudaStream_t s) {
+  cart_geom_kernel<<<nblk(n_total), 256, 0, s>>>(nodes, nbr, n_total, cart);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cart_points(const double* cart, int n_owned, int n_total, int n, double* xq, double* xf,
+                               cudaStream_t s) {
+  Tab1D T;
+  make_tab(n, &T);
+  const long tot = (long)n_total * (n * n * n + 6 * n * n);
+  cart_points_kernel<<<nblk(tot), 256, 0, s>>>(cart, n_owned, n_total, n, T, xq, xf);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gen_geom(const GeoTab& g, const double* nodes, int n_total, double* vmet, double* fmet,
+                            double* xq, double* xf, int* bad, cudaStream_t s) {
+  const int n = g.n;
+  const long tot = (long)n_total * (n * n * n + 6 * n * n);
+  gen_geom_kernel<<<nblk(tot, 128), 128, 0, s>>>(g, nodes, n_total, vmet, fmet, xq, xf, bad);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gen_H(const double* vmet, const double* fmet, const int* nbr, int n_total, int n, double* H,
+                         cudaStream_t s) {
+  gen_H_kernel<<<nblk(n_total), 256, 0, s>>>(vmet, fmet, nbr, n_total, n, H);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_align_check(const double* xf, const int* nbr, int n_owned, int n, double tol, int* bad,
+                               cudaStream_t s) {
+  align_check_kernel<<<nblk((long)n_owned * 6), 256, 0, s>>>(xf, nbr, n_owned, n, tol, bad);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_law_points(int kind, const double* p, const double* x, long npts, double* out, cudaStream_t s) {
+  if (npts <= 0) return cudaSuccess;
+  law_points_kernel<<<nblk(npts), 256, 0, s>>>(kind, nullptr, p[0], p[1], x, npts, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_range(const double* v, long n, double* bmin, double* bmax, int* bad, int nblocks,
+                         cudaStream_t s) {
+  range_kernel<<<nblocks, 256, 0, s>>>(v, n, bmin, bmax, bad);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- vectors
+cudaError_t launch_dot(const double* a, const double* b, long n, double* part, int nblocks, double* out,
+                       cudaStream_t s) {
+  dot_partial_kernel<<<nblocks, 256, 0, s>>>(a, b, n, part);
+  sum_partials_kernel<<<1, 256, 0, s>>>(part, nblocks, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cheb_first(const double* b, const double* dinv, double c_r, double* d, double* x, long n,
+                              cudaStream_t s) {
+  cheb_first_kernel<<<gs_blocks(n), 256, 0, s>>>(b, dinv, c_r, d, x, n);
+  return cudaGetLastError();
+}
+cudaError_t launch_ew_mul(const double* a, const double* b, double* out, long n, cudaStream_t s) {
+  ew_mul_kernel<<<gs_blocks(n), 256, 0, s>>>(a, b, out, n);
+  return cudaGetLastError();
+}
+cudaError_t launch_ew_sqrt(const double* a, double* out, long n, cudaStream_t s) {
+  ew_sqrt_kernel<<<gs_blocks(n), 256, 0, s>>>(a, out, n);
+  return cudaGetLastError();
+}
+cudaError_t launch_ew_div(const double* a, const double* b, double* out, long n, cudaStream_t s) {
+  ew_div_kernel<<<gs_blocks(n), 256, 0, s>>>(a, b, out, n);
+  return cudaGetLastError();
+}
+cudaError_t launch_lanczos_update(double* w, const double* q, const double* qprev, const double* alpha,
+                                  const double* beta_prev, long n, cudaStream_t s) {
+  lanczos_update_kernel<<<gs_blocks(n), 256, 0, s>>>(w, q, qprev, alpha, beta_prev, n);
+  return cudaGetLastError();
+}
+cudaError_t launch_scale_by_inv(const double* w, const double* s2, double* q, long n, cudaStream_t s) {
+  scale_by_inv_kernel<<<gs_blocks(n), 256, 0, s>>>(w, s2, q, n);
+  return cudaGetLastError();
+}
+cudaError_t launch_gather_cells(const double* src, const int* list, int ncells, int len, double* out,
+                                cudaStream_t s) {
+  if (ncells <= 0) return cudaSuccess;
+  gather_cells_kernel<<<nblk((long)ncells * len), 256, 0, s>>>(src, list, ncells, len, out);
+  return cudaGetLastError();
+}
+
+}  // namespace dgvv

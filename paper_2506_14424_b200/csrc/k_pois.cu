@@ -1,0 +1,44 @@
+// k_pois.cu — instantiations of the scalar SIPG Poisson apply (K4, with K6 epilogues).
+#include "tu_tables.cuh"
+#include "sipg_apply.cuh"
+#include "launch.h"
+
+namespace dgvv {
+
+cudaError_t launch_apply_visc(int n, int form, int geo, const ApplyArgs& a, cudaStream_t s);
+
+cudaError_t upload_tables_pois(const Tab1D* tabs) { return tu_upload_tables(tabs); }
+
+template <int n> constexpr int cpb_pois() { return (128 / (n * n)) > 0 ? (128 / (n * n)) : 1; }
+
+template <int n, int GEO>
+static cudaError_t run(const ApplyArgs& a, cudaStream_t s) {
+  constexpr int CPB = cpb_pois<n>();
+  const size_t smem = (size_t)CPB * 4 * n * n * n * sizeof(double);
+  auto k = sipg_apply_kernel<n, 1, 1, GEO, CPB>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  if (a.n_proc <= 0) return cudaSuccess;
+  const int grid = (a.n_proc + CPB - 1) / CPB;
+  k<<<grid, CPB * n * n, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_apply(int nc, int n, int form, int geo, const ApplyArgs& a, cudaStream_t s) {
+  if (nc == 3) return launch_apply_visc(n, form, geo, a, s);
+  switch (n) {
+    case 2: return geo ? run<2, 1>(a, s) : run<2, 0>(a, s);
+    case 3: return geo ? run<3, 1>(a, s) : run<3, 0>(a, s);
+    case 4: return geo ? run<4, 1>(a, s) : run<4, 0>(a, s);
+    case 5: return geo ? run<5, 1>(a, s) : run<5, 0>(a, s);
+    case 6: return geo ? run<6, 1>(a, s) : run<6, 0>(a, s);
+    case 7: return geo ? run<7, 1>(a, s) : run<7, 0>(a, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace dgvv

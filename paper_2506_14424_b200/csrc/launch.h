@@ -1,0 +1,55 @@
+// launch.h — host-side launchers exported by the kernel translation units.
+#pragma once
+#include "common.cuh"
+#include "tables.h"
+
+namespace dgvv {
+
+
+// each kernel TU owns a private __constant__ copy of the tables
+cudaError_t upload_tables_visc(const Tab1D* tabs);
+cudaError_t upload_tables_pois(const Tab1D* tabs);
+cudaError_t upload_tables_aux(const Tab1D* tabs);
+cudaError_t upload_tables_newton(const Tab1D* tabs);
+
+// K1 / K4 / K6: SIPG apply with epilogue (nc = 3 viscous, 1 Poisson)
+cudaError_t launch_apply(int nc, int n, int form, int geo, const ApplyArgs& a, cudaStream_t s);
+// K2: Newton-linearised viscous apply
+cudaError_t launch_newton(int n, int geo, const ApplyArgs& a, cudaStream_t s);
+// K3: Carreau viscosity at all points
+cudaError_t launch_carreau(int n, int geo, const NuArgs& a, cudaStream_t s);
+// K5: inverse diagonal
+cudaError_t launch_diag(int nc, int n, int form, int geo, const DiagArgs& a, cudaStream_t s);
+// K7: out = (M x M x M) in + beta out
+cudaError_t launch_tensor3(int nin, int nout, int nc, const double* M, const double* in, double* out,
+                           double beta, int ncells, cudaStream_t s);
+
+// setup kernels
+cudaError_t launch_cart_geom(const double* nodes, const int* nbr, int n_total, double* cart, cudaStream_t s);
+cudaError_t launch_cart_points(const double* cart, int n_owned, int n_total, int n, double* xq, double* xf,
+                               cudaStream_t s);
+cudaError_t launch_gen_geom(const GeoTab& g, const double* nodes, int n_total, double* vmet, double* fmet,
+                            double* xq, double* xf, int* bad, cudaStream_t s);
+cudaError_t launch_gen_H(const double* vmet, const double* fmet, const int* nbr, int n_total, int n, double* H,
+                         cudaStream_t s);
+cudaError_t launch_align_check(const double* xf, const int* nbr, int n_owned, int n, double tol, int* bad,
+                               cudaStream_t s);
+cudaError_t launch_law_points(int kind, const double* p, const double* x, long npts, double* out, cudaStream_t s);
+cudaError_t launch_range(const double* v, long n, double* bmin, double* bmax, int* bad, int nblocks,
+                         cudaStream_t s);
+
+// vector kernels
+cudaError_t launch_dot(const double* a, const double* b, long n, double* part, int nblocks, double* out,
+                       cudaStream_t s);
+cudaError_t launch_cheb_first(const double* b, const double* dinv, double c_r, double* d, double* x, long n,
+                              cudaStream_t s);
+cudaError_t launch_ew_mul(const double* a, const double* b, double* out, long n, cudaStream_t s);
+cudaError_t launch_ew_sqrt(const double* a, double* out, long n, cudaStream_t s);
+cudaError_t launch_ew_div(const double* a, const double* b, double* out, long n, cudaStream_t s);
+cudaError_t launch_lanczos_update(double* w, const double* q, const double* qprev, const double* alpha,
+                                  const double* beta_prev, long n, cudaStream_t s);
+cudaError_t launch_scale_by_inv(const double* w, const double* s2, double* q, long n, cudaStream_t s);
+cudaError_t launch_gather_cells(const double* src, const int* list, int ncells, int len, double* out,
+                                cudaStream_t s);
+
+}  // namespace dgvv

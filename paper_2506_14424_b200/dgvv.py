@@ -1,0 +1,191 @@
+"""Python binding of the dgvv C ABI (include/dgvv.h) — argument marshalling only.
+
+Vectors are torch CUDA float64 tensors (contiguous, canonical layout); every call forwards
+raw device pointers and the current torch CUDA stream to libdgvv.so, whose kernels do all
+of the work.  Laws are given as dicts and packed into dgvv_law.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _abi as A
+
+
+def pack_law(law):
+    """dict -> dgvv_law (marshalling: kind + parameter slots as documented in dgvv.h)."""
+    if law is None:
+        return None
+    L = A.DgvvLaw()
+    k = law["kind"]
+    if k == "const":
+        L.kind, vals = A.LAW_CONST, [law["value"]]
+    elif k == "sin3":
+        L.kind, vals = A.LAW_SIN3, [law.get("mean", 1.0), law.get("amp", 0.5)]
+    elif k == "exp":
+        L.kind, vals = A.LAW_EXP, [law["rate"]]
+    elif k == "carreau":
+        L.kind, vals = A.LAW_CARREAU, [law["eta0"], law["eta_inf"], law["lam"], law["n"]]
+    else:
+        raise ValueError(f"law kind {k!r} has no dgvv_law encoding")
+    for i, v in enumerate(vals):
+        L.p[i] = float(v)
+    return L
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t: torch.Tensor, n: int | None = None, name="vector"):
+    if not isinstance(t, torch.Tensor) or t.dtype != torch.float64 or not t.is_cuda or not t.is_contiguous():
+        raise TypeError(f"{name}: expected a contiguous CUDA float64 tensor")
+    if n is not None and t.numel() != n:
+        raise ValueError(f"{name}: expected {n} entries, got {t.numel()}")
+    return C.c_void_p(t.data_ptr())
+
+
+class Context:
+    """One dgvv context (one mesh partition, a hierarchy of degrees, up to two operators)."""
+
+    def __init__(self, mesh, degree: int, visc_law=None, poisson_law=None, degrees=None, ip=1.0,
+                 formulation="divergence", nccl_comm=None, n_ghost=0, ghost_global_id=None,
+                 ghost_owner=None, first_global_cell=0, n_owned=None):
+        L = A.lib()
+        self._L = L
+        n_owned = mesh.n_cells if n_owned is None else n_owned
+        self._nb = np.ascontiguousarray(mesh.neighbor, dtype=np.int64)
+        self._nodes = np.ascontiguousarray(mesh.nodes, dtype=np.float64)
+        m = A.DgvvMesh()
+        m.n_cells = n_owned
+        m.n_ghost = n_ghost
+        m.first_global_cell = first_global_cell
+        m.neighbor = self._nb.ctypes.data_as(C.POINTER(C.c_int64))
+        if n_ghost:
+            self._gid = np.ascontiguousarray(ghost_global_id, dtype=np.int64)
+            self._gown = np.ascontiguousarray(ghost_owner, dtype=np.int32)
+            m.ghost_global_id = self._gid.ctypes.data_as(C.POINTER(C.c_int64))
+            m.ghost_owner = self._gown.ctypes.data_as(C.POINTER(C.c_int32))
+        m.map_degree = mesh.map_degree
+        m.nodes = self._nodes.ctypes.data_as(C.POINTER(C.c_double))
+        degs = [degree] if degrees is None else list(degrees)
+        self.degrees = degs
+        self._degs = (C.c_int32 * len(degs))(*degs)
+        o = A.DgvvOptions()
+        o.n_levels = len(degs)
+        o.degrees = self._degs
+        o.ip_factor = ip
+        o.formulation = A.FORM_DIVERGENCE if formulation == "divergence" else A.FORM_LAPLACE
+        o.nccl_comm = nccl_comm
+        self._vl, self._pl = pack_law(visc_law), pack_law(poisson_law)
+        h = C.c_void_p()
+        A.check(L.dgvv_setup(C.byref(m), degree,
+                             C.byref(self._vl) if self._vl is not None else None,
+                             C.byref(self._pl) if self._pl is not None else None,
+                             C.byref(o), _stream(), C.byref(h)))
+        self.h = h
+        self.n_owned = n_owned
+
+    def close(self):
+        if getattr(self, "h", None):
+            self._L.dgvv_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------------ sizes
+    def n_dofs(self, level=0):
+        nl, ng = C.c_int64(), C.c_int64()
+        A.check(self._L.dgvv_sizes(self.h, level, C.byref(nl), C.byref(ng)))
+        return nl.value
+
+    def n_global_dofs(self, level=0):
+        nl, ng = C.c_int64(), C.c_int64()
+        A.check(self._L.dgvv_sizes(self.h, level, C.byref(nl), C.byref(ng)))
+        return ng.value
+
+    def _n(self, op, level):
+        return (3 if op == A.OP_VISCOUS else 1) * self.n_dofs(level)
+
+    # ------------------------------------------------------------------ calls
+    def update_viscosity(self, u_lin):
+        A.check(self._L.dgvv_update_viscosity(self.h, _ptr(u_lin, self._n(0, 0), "u_lin"), _stream()))
+        self._ulin = u_lin          # the library borrows u_lin until the next update
+
+    def apply_viscous(self, src, dst, level=0):
+        n = self._n(A.OP_VISCOUS, level)
+        A.check(self._L.dgvv_apply_viscous(self.h, level, _ptr(src, n, "src"), _ptr(dst, n, "dst"), _stream()))
+        return dst
+
+    def apply_linearized_viscous(self, src, dst):
+        n = self._n(A.OP_VISCOUS, 0)
+        A.check(self._L.dgvv_apply_linearized_viscous(self.h, _ptr(src, n, "src"), _ptr(dst, n, "dst"), _stream()))
+        return dst
+
+    def apply_poisson(self, src, dst, level=0):
+        n = self._n(A.OP_POISSON, level)
+        A.check(self._L.dgvv_apply_poisson(self.h, level, _ptr(src, n, "src"), _ptr(dst, n, "dst"), _stream()))
+        return dst
+
+    def inverse_diagonal(self, op, dst, level=0):
+        A.check(self._L.dgvv_inverse_diagonal(self.h, op, level, _ptr(dst, self._n(op, level), "dst"), _stream()))
+        return dst
+
+    def estimate_lambda_max(self, op, v0, level=0, steps=20):
+        out = C.c_double()
+        A.check(self._L.dgvv_estimate_lambda_max(self.h, op, level, steps, _ptr(v0, self._n(op, level), "v0"),
+                                                 C.byref(out), _stream()))
+        return out.value
+
+    def chebyshev_smooth(self, op, x, b, lam_lo, lam_hi, degree=5, x_is_zero=False, work=None, level=0):
+        n = self._n(op, level)
+        if work is None:
+            work = torch.empty(2 * n, dtype=torch.float64, device=x.device)
+        A.check(self._L.dgvv_chebyshev_smooth(self.h, op, level, _ptr(x, n, "x"), _ptr(b, n, "b"), degree,
+                                              lam_lo, lam_hi, int(x_is_zero), _ptr(work, 2 * n, "work"), _stream()))
+        return x
+
+    def prolongate(self, op, fine_level, coarse, fine, beta=0.0):
+        A.check(self._L.dgvv_prolongate(self.h, op, fine_level, _ptr(coarse, self._n(op, fine_level + 1), "coarse"),
+                                        _ptr(fine, self._n(op, fine_level), "fine"), beta, _stream()))
+        return fine
+
+    def restrict(self, op, fine_level, fine, coarse, beta=0.0):
+        A.check(self._L.dgvv_restrict(self.h, op, fine_level, _ptr(fine, self._n(op, fine_level), "fine"),
+                                      _ptr(coarse, self._n(op, fine_level + 1), "coarse"), beta, _stream()))
+        return coarse
+
+    def vcycle(self, op, b, x, lam_hi_per_level):
+        n = self._n(op, 0)
+        arr = (C.c_double * len(self.degrees))(*[float(v) for v in lam_hi_per_level])
+        A.check(self._L.dgvv_vcycle(self.h, op, _ptr(b, n, "b"), _ptr(x, n, "x"), arr, _stream()))
+        return x
+
+    def dot(self, a, b, ncomp=1, level=0):
+        out = C.c_double()
+        n = ncomp * self.n_dofs(level)
+        A.check(self._L.dgvv_dot(self.h, level, ncomp, _ptr(a, n, "a"), _ptr(b, n, "b"), C.byref(out), _stream()))
+        return out.value
+
+    def coefficient_range(self, op, level=0):
+        lo, hi = C.c_double(), C.c_double()
+        A.check(self._L.dgvv_coefficient_range(self.h, op, level, C.byref(lo), C.byref(hi)))
+        return lo.value, hi.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    A.check(A.lib().dgvv_nccl_get_unique_id(buf))
+    return buf.raw
+
+
+def nccl_comm_init(uid: bytes, nranks: int, rank: int):
+    comm = C.c_void_p()
+    A.check(A.lib().dgvv_nccl_comm_init(uid, nranks, rank, C.byref(comm)))
+    return comm
