@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libdgvv.so")
+LIB_PATH = os.environ.get("DGVV_LIB_PATH") or os.path.join(HERE, "lib", "libdgvv.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "dgvv.h")
 
 STATUS = {0: "DGVV_OK", 1: "DGVV_EINVAL", 2: "DGVV_EDOMAIN", 3: "DGVV_ENOMEM", 4: "DGVV_ECUDA",

@@ -107,13 +107,19 @@ dgvv_status upload_tables() {
 // ------------------------------------------------------------------ context
 struct Level {
   int k = 0, n = 0;
-  double* vmet = nullptr;     // general geometry
-  double* fmet = nullptr;
+  double* vJi = nullptr;      // general geometry: J^-1 at cell points [n_total][9][n^3]
+  double* fJi = nullptr;      //                   J^-1 at own face points [n_total][6][9][n^2]
+  double* jxw = nullptr;      //                   JxW [n_total][n^3]
+  double* fdA = nullptr;      //                   dA  [n_total][6][n^2]
   double* Hc = nullptr;
-  double* nu_cell = nullptr;  // viscous coefficient
+  double* nu_cell = nullptr;  // viscous coefficient at points (raw nu)
   double* nu_face = nullptr;
-  double* c_cell = nullptr;   // Poisson coefficient
+  double* wv_cell = nullptr;  // general geometry: nu*JxW, nu*dA
+  double* wv_face = nullptr;
+  double* c_cell = nullptr;   // Poisson coefficient (raw c)
   double* c_face = nullptr;
+  double* wc_cell = nullptr;  // general geometry: c*JxW, c*dA
+  double* wc_face = nullptr;
   double* dinv[2] = {nullptr, nullptr};
   double* ulin = nullptr;     // u_lin interpolated to this level (levels >= 1), owned
   double* ghost[2] = {nullptr, nullptr};   // ghost src buffers (NC = 3 / 1)
@@ -233,11 +239,18 @@ ApplyArgs base_args(dgvv_ctx* c, int l, int op) {
   a.cell_list = nullptr;
   a.n_proc = c->n_owned;
   a.n_owned = c->n_owned;
-  a.nu_cell = op == DGVV_OP_VISCOUS ? L.nu_cell : L.c_cell;
-  a.nu_face = op == DGVV_OP_VISCOUS ? L.nu_face : L.c_face;
+  if (c->geo == 0) {
+    a.nu_cell = op == DGVV_OP_VISCOUS ? L.nu_cell : L.c_cell;
+    a.nu_face = op == DGVV_OP_VISCOUS ? L.nu_face : L.c_face;
+  } else {
+    a.nu_cell = op == DGVV_OP_VISCOUS ? L.wv_cell : L.wc_cell;
+    a.nu_face = op == DGVV_OP_VISCOUS ? L.wv_face : L.wc_face;
+  }
   a.cart = c->d_cart;
-  a.vmet = L.vmet;
-  a.fmet = L.fmet;
+  a.vJi = L.vJi;
+  a.fJi = L.fJi;
+  a.jxw = L.jxw;
+  a.fdA = L.fdA;
   a.Hcell = L.Hc;
   a.pen = c->ip * (double)(L.k + 1) * (double)(L.k + 1);
   a.ghost = L.ghost[op == DGVV_OP_VISCOUS ? 0 : 1];
@@ -276,11 +289,16 @@ dgvv_status ensure_dinv(dgvv_ctx* c, int op, int l, cudaStream_t s) {
   DiagArgs d;
   d.nbr = c->d_nbr;
   d.n_owned = c->n_owned;
-  d.nu_cell = oi == 0 ? L.nu_cell : L.c_cell;
-  d.nu_face = oi == 0 ? L.nu_face : L.c_face;
+  if (c->geo == 0) {
+    d.nu_cell = oi == 0 ? L.nu_cell : L.c_cell;
+    d.nu_face = oi == 0 ? L.nu_face : L.c_face;
+  } else {
+    d.nu_cell = oi == 0 ? L.wv_cell : L.wc_cell;
+    d.nu_face = oi == 0 ? L.wv_face : L.wc_face;
+  }
   d.cart = c->d_cart;
-  d.vmet = L.vmet;
-  d.fmet = L.fmet;
+  d.vJi = L.vJi;
+  d.fJi = L.fJi;
   d.Hcell = L.Hc;
   d.pen = c->ip * (double)(L.k + 1) * (double)(L.k + 1);
   d.out = L.dinv[oi];
@@ -304,6 +322,18 @@ dgvv_status eval_analytic(dgvv_ctx* c, const dgvv_law* law, int l, double* xq, d
   double p[2] = {law->p[0], law->p[1]};
   DGVV_CUDA_TRY(launch_law_points(law->kind, p, xq, (long)c->n_owned * n * n * n, cell_out, s));
   DGVV_CUDA_TRY(launch_law_points(law->kind, p, xf, (long)c->n_total * 6 * n * n, face_out, s));
+  return DGVV_OK;
+}
+
+// general geometry: w_cell = nu * JxW, w_face = nu * dA (the apply and diagonal kernels read
+// these; the normal and dA are otherwise recomputed from J^-1)
+dgvv_status premultiply(dgvv_ctx* c, int l, const double* nc, const double* nf, double* wc, double* wf,
+                        cudaStream_t s) {
+  if (c->geo != 1) return DGVV_OK;
+  Level& L = c->L[l];
+  const long n3 = (long)L.n * L.n * L.n, n2 = (long)L.n * L.n;
+  DGVV_CUDA_TRY(launch_ew_mul(nc, L.jxw, wc, (long)c->n_owned * n3, s));
+  DGVV_CUDA_TRY(launch_ew_mul(nf, L.fdA, wf, (long)c->n_total * 6 * n2, s));
   return DGVV_OK;
 }
 
@@ -511,18 +541,20 @@ static dgvv_status setup_impl(const dgvv_mesh* m, int32_t degree, const dgvv_law
     if (c->geo == 0) {
       DGVV_CUDA_TRY(launch_cart_points(c->d_cart, c->n_total, c->n_total, n, xq, xf, s));
     } else {
-      TRY(dalloc(c, &L.vmet, (size_t)c->n_total * VMET_NV * n3));
-      TRY(dalloc(c, &L.fmet, (size_t)c->n_total * 6 * FMET_NV * n2));
+      TRY(dalloc(c, &L.vJi, (size_t)c->n_total * 9 * n3));
+      TRY(dalloc(c, &L.fJi, (size_t)c->n_total * 6 * 9 * n2));
+      TRY(dalloc(c, &L.jxw, (size_t)c->n_total * n3));
+      TRY(dalloc(c, &L.fdA, (size_t)c->n_total * 6 * n2));
       TRY(dalloc(c, &L.Hc, (size_t)c->n_total));
       GeoTab g;
       make_geotab(m->map_degree, n, &g);
       DGVV_CUDA_TRY(cudaMemsetAsync(c->d_flag, 0, sizeof(int), s));
-      DGVV_CUDA_TRY(launch_gen_geom(g, c->d_nodes, c->n_total, L.vmet, L.fmet, xq, xf, c->d_flag, s));
+      DGVV_CUDA_TRY(launch_gen_geom(g, c->d_nodes, c->n_total, L.vJi, L.jxw, L.fJi, L.fdA, xq, xf, c->d_flag, s));
       int bad = 0;
       DGVV_CUDA_TRY(cudaMemcpyAsync(&bad, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
       DGVV_CUDA_TRY(cudaStreamSynchronize(s));
       if (bad) return dgvv_fail(DGVV_EDOMAIN, "level %zu: %d points with non-positive Jacobian", l, bad);
-      DGVV_CUDA_TRY(launch_gen_H(L.vmet, L.fmet, c->d_nbr, c->n_total, n, L.Hc, s));
+      DGVV_CUDA_TRY(launch_gen_H(L.jxw, L.fdA, c->d_nbr, c->n_total, n, L.Hc, s));
     }
     if (l == 0) {   // structured alignment of face quadrature points (needed by the kernels)
       double sc = 0.0;
@@ -537,10 +569,15 @@ static dgvv_status setup_impl(const dgvv_mesh* m, int32_t degree, const dgvv_law
     if (c->has_visc) {
       TRY(dalloc(c, &L.nu_cell, (size_t)c->n_owned * n3));
       TRY(dalloc(c, &L.nu_face, (size_t)c->n_total * 6 * n2));
+      if (c->geo == 1) {
+        TRY(dalloc(c, &L.wv_cell, (size_t)c->n_owned * n3));
+        TRY(dalloc(c, &L.wv_face, (size_t)c->n_total * 6 * n2));
+      }
       if (!c->carreau) {
         TRY(eval_analytic(c, &c->visc, (int)l, xq, xf, L.nu_cell, L.nu_face, s));
         TRY(check_positive(c, L.nu_cell, (long)c->n_owned * n3, s, "viscosity (cells)"));
         TRY(check_positive(c, L.nu_face, (long)c->n_total * 6 * n2, s, "viscosity (faces)"));
+        TRY(premultiply(c, (int)l, L.nu_cell, L.nu_face, L.wv_cell, L.wv_face, s));
       }
       if (c->n_ghost) {
         TRY(dalloc(c, &L.ghost[0], (size_t)c->n_ghost * 3 * n3));
@@ -554,6 +591,11 @@ static dgvv_status setup_impl(const dgvv_mesh* m, int32_t degree, const dgvv_law
       TRY(eval_analytic(c, &c->pois, (int)l, xq, xf, L.c_cell, L.c_face, s));
       TRY(check_positive(c, L.c_cell, (long)c->n_owned * n3, s, "Poisson coefficient (cells)"));
       TRY(check_positive(c, L.c_face, (long)c->n_total * 6 * n2, s, "Poisson coefficient (faces)"));
+      if (c->geo == 1) {
+        TRY(dalloc(c, &L.wc_cell, (size_t)c->n_owned * n3));
+        TRY(dalloc(c, &L.wc_face, (size_t)c->n_total * 6 * n2));
+        TRY(premultiply(c, (int)l, L.c_cell, L.c_face, L.wc_cell, L.wc_face, s));
+      }
       if (c->n_ghost) TRY(dalloc(c, &L.ghost[1], (size_t)c->n_ghost * n3));
     }
     DGVV_CUDA_TRY(cudaStreamSynchronize(s));
@@ -679,14 +721,15 @@ dgvv_status dgvv_update_viscosity(dgvv_ctx* c, const double* u_lin, dgvv_stream 
     a.n_owned = c->n_owned;
     a.n_total = c->n_total;
     a.cart = c->d_cart;
-    a.vmet = L.vmet;
-    a.fmet = L.fmet;
+    a.vJi = L.vJi;
+    a.fJi = L.fJi;
     for (int i = 0; i < 4; ++i) a.law[i] = c->visc.p[i];
     a.nu_cell = L.nu_cell;
     a.nu_face = L.nu_face;
     DGVV_CUDA_TRY(launch_carreau(n, c->geo, a, s));
     TRY(check_positive(c, L.nu_cell, (long)c->n_owned * n3, s, "Carreau viscosity (cells)"));
     TRY(check_positive(c, L.nu_face, (long)c->n_total * 6 * n * n, s, "Carreau viscosity (faces)"));
+    TRY(premultiply(c, (int)l, L.nu_cell, L.nu_face, L.wv_cell, L.wv_face, s));
     for (int o = 0; o < 2; ++o)
       if (L.dinv[o] && o == 0) { /* diagonal depends on nu: recompute lazily */
         cudaFree(L.dinv[0]);

@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(CPB * n * n) carreau_nu_kernel(const NuArgs A)
       }
       double Ji[9];
       if (GEO == 1) {
-        const double* vm = A.vmet + (size_t)cell * VMET_NV * n3 + q;
+        const double* vm = A.vJi + (size_t)cell * 9 * n3 + q;
 #pragma unroll
         for (int r = 0; r < 9; ++r) Ji[r] = vm[r * n3];
       }
@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(CPB * n * n) carreau_nu_kernel(const NuArgs A)
       }
       double Ji[9];
       if (GEO == 1) {
-        const double* fm = A.fmet + ((size_t)cell * 6 + f) * FMET_NV * n2 + p;
+        const double* fm = A.fJi + ((size_t)cell * 6 + f) * 9 * n2 + p;
 #pragma unroll
         for (int r = 0; r < 9; ++r) Ji[r] = fm[r * n2];
       }
@@ -164,9 +164,9 @@ __global__ void diag_kernel(const DiagArgs A) {
       for (int j = 0; j < 3; ++j) g[j] = gxi[j] * ih[j];
       w = T.w[qv[0]] * T.w[qv[1]] * T.w[qv[2]] * vol;
     } else {
-      const double* vm = A.vmet + (size_t)cell * VMET_NV * n3 + q;
+      const double* vm = A.vJi + (size_t)cell * 9 * n3 + q;
       for (int j = 0; j < 3; ++j) g[j] = gxi[0] * vm[j * n3] + gxi[1] * vm[(3 + j) * n3] + gxi[2] * vm[(6 + j) * n3];
-      w = vm[9 * n3];
+      w = 1.0;                                   // nu_cell holds nu*JxW
     }
     double gg = g[0] * g[0] + g[1] * g[1] + g[2] * g[2];
     if (FORM == 0) gg += g[comp] * g[comp];
@@ -205,11 +205,14 @@ __global__ void diag_kernel(const DiagArgs A) {
       for (int j = 0; j < 3; ++j) g[j] = gxi[j] * ih[j];
       nrm[d] = s ? 1.0 : -1.0;
       dA = T.w[pa] * T.w[pb] * vol * ih[d];
-    } else {
-      const double* fm = A.fmet + ((size_t)cell * 6 + f) * FMET_NV * n2 + pidx;
+    } else {                                     // nu_face holds nu*dA: dA folded in below
+      const double* fm = A.fJi + ((size_t)cell * 6 + f) * 9 * n2 + pidx;
       for (int j = 0; j < 3; ++j) g[j] = gxi[0] * fm[j * n2] + gxi[1] * fm[(3 + j) * n2] + gxi[2] * fm[(6 + j) * n2];
-      nrm[0] = fm[9 * n2]; nrm[1] = fm[10 * n2]; nrm[2] = fm[11 * n2];
-      dA = fm[12 * n2];
+      const double sg = s ? 1.0 : -1.0;
+      const double v0 = fm[(3 * d) * n2], v1 = fm[(3 * d + 1) * n2], v2 = fm[(3 * d + 2) * n2];
+      const double il = sg / sqrt(v0 * v0 + v1 * v1 + v2 * v2);
+      nrm[0] = v0 * il; nrm[1] = v1 * il; nrm[2] = v2 * il;
+      dA = 1.0;
     }
     const double num = A.nu_face[((size_t)cell * 6 + f) * n2 + pidx];
     double nup = num, Hp = Hm;

@@ -6,6 +6,9 @@
 #include <stdint.h>
 
 #define DGVV_NMAX 8        // max points per direction (degree <= 7)
+#ifndef DGVV_MINB
+#define DGVV_MINB 1        // min resident CTAs per SM requested from ptxas for the apply kernel
+#endif
 
 // 1D tables of the degree-(n-1) Lagrange basis on the n Gauss-Legendre points of [0,1]
 // (readings G1/G2).  Computed on the host by tables.cpp (Newton iteration on P_n and the
@@ -28,10 +31,10 @@ struct Tab1D {
 #define CART_STRIDE 8
 
 // Streamed metric terms of the general (iso-parametric) path, per level:
-//   vmet[cell][10][n^3] : Ji[k][j] = d xi_k / d x_j (9, row-major k,j), JxW (1)
-//   fmet[cell][6][13][n^2]: Ji (9), outward unit normal (3), dA (1)
-#define VMET_NV 10
-#define FMET_NV 13
+//   vJi[cell][9][n^3]     : Ji[k][j] = d xi_k / d x_j at cell points (row-major k,j)
+//   fJi[cell][6][9][n^2]  : own-side Ji at face points; the outward unit normal is
+//                           n = s J^-T e_d / |J^-T e_d| (recomputed), dA = JxW-like weight
+//   jxw[cell][n^3], fdA[cell][6][n^2]: JxW and dA (setup; premultiplied by nu for the apply)
 
 enum { MODE_APPLY = 0, MODE_RESID = 1, MODE_CHEB = 2 };
 
@@ -43,11 +46,13 @@ struct ApplyArgs {
   const int* cell_list;     // cells to process (null: 0..n_proc-1)
   int n_proc;
   int n_owned;
+  // coefficient at quadrature points.  Cartesian: nu itself; general geometry:
+  // premultiplied weights nu*JxW (cells) and nu*dA (own face points).
   const double* nu_cell;    // [n_owned][n^3]
-  const double* nu_face;    // [n_total][6][n^2] own-side values
+  const double* nu_face;    // [n_total][6][n^2]
   const double* cart;       // [n_total][CART_STRIDE]      (Cartesian)
-  const double* vmet;       // [n_owned][10][n^3]          (general)
-  const double* fmet;       // [n_total][6][13][n^2]       (general)
+  const double* vJi;        // [n_total][9][n^3]  J^-1 at cell points        (general)
+  const double* fJi;        // [n_total][6][9][n^2] own J^-1 at face points  (general)
   const double* Hcell;      // [n_total]                   (general)
   double pen;               // IP (k+1)^2
   // epilogue
@@ -60,6 +65,8 @@ struct ApplyArgs {
   // Newton (linearised) extras
   const double* ulin;       // owned u_lin
   const double* ulin_ghost; // ghost u_lin
+  const double* jxw;        // general geometry: JxW [n_owned][n^3]
+  const double* fdA;        // general geometry: dA  [n_total][6][n^2]
   double law[4];            // eta0, eta_inf, lambda, n
 };
 
@@ -68,8 +75,8 @@ struct NuArgs {
   const double* ughost;     // ghost [n_ghost][3][n^3]
   int n_owned, n_total;
   const double* cart;
-  const double* vmet;
-  const double* fmet;
+  const double* vJi;        // general: [n_total][9][n^3]
+  const double* fJi;        // general: [n_total][6][9][n^2]
   double law[4];
   double* nu_cell;          // [n_owned][n^3]
   double* nu_face;          // [n_total][6][n^2]
@@ -78,11 +85,11 @@ struct NuArgs {
 struct DiagArgs {
   const int* nbr;
   int n_owned;
-  const double* nu_cell;
-  const double* nu_face;
+  const double* nu_cell;    // Cartesian: nu; general: nu*JxW
+  const double* nu_face;    // Cartesian: nu; general: nu*dA
   const double* cart;
-  const double* vmet;
-  const double* fmet;
+  const double* vJi;
+  const double* fJi;
   const double* Hcell;
   double pen;
   double* out;              // 1 / D

@@ -129,17 +129,17 @@ cudaError_t launch_cart_points(const double* cart, int n_owned, int n_total, int
   return cudaGetLastError();
 }
 
-cudaError_t launch_gen_geom(const GeoTab& g, const double* nodes, int n_total, double* vmet, double* fmet,
-                            double* xq, double* xf, int* bad, cudaStream_t s) {
+cudaError_t launch_gen_geom(const GeoTab& g, const double* nodes, int n_total, double* vJi, double* jxw,
+                            double* fJi, double* fdA, double* xq, double* xf, int* bad, cudaStream_t s) {
   const int n = g.n;
   const long tot = (long)n_total * (n * n * n + 6 * n * n);
-  gen_geom_kernel<<<nblk(tot, 128), 128, 0, s>>>(g, nodes, n_total, vmet, fmet, xq, xf, bad);
+  gen_geom_kernel<<<nblk(tot, 128), 128, 0, s>>>(g, nodes, n_total, vJi, jxw, fJi, fdA, xq, xf, bad);
   return cudaGetLastError();
 }
 
-cudaError_t launch_gen_H(const double* vmet, const double* fmet, const int* nbr, int n_total, int n, double* H,
+cudaError_t launch_gen_H(const double* jxw, const double* fdA, const int* nbr, int n_total, int n, double* H,
                          cudaStream_t s) {
-  gen_H_kernel<<<nblk(n_total), 256, 0, s>>>(vmet, fmet, nbr, n_total, n, H);
+  gen_H_kernel<<<nblk(n_total), 256, 0, s>>>(jxw, fdA, nbr, n_total, n, H);
   return cudaGetLastError();
 }
 

@@ -9,13 +9,14 @@ cudaError_t launch_apply_visc(int n, int form, int geo, const ApplyArgs& a, cuda
 
 cudaError_t upload_tables_pois(const Tab1D* tabs) { return tu_upload_tables(tabs); }
 
-template <int n> constexpr int cpb_pois() { return (128 / (n * n)) > 0 ? (128 / (n * n)) : 1; }
+template <int n> constexpr int cpb_pois() { return n == 2 ? 32 : n == 3 ? 14 : n == 4 ? 8 : n == 5 ? 5 : n == 6 ? 4 : 3; }
+template <int n> constexpr int minb_pois() { return n <= 3 ? 3 : 4; }
 
 template <int n, int GEO>
 static cudaError_t run(const ApplyArgs& a, cudaStream_t s) {
   constexpr int CPB = cpb_pois<n>();
-  const size_t smem = (size_t)CPB * 4 * n * n * n * sizeof(double);
-  auto k = sipg_apply_kernel<n, 1, 1, GEO, CPB>;
+  const size_t smem = (size_t)CPB * ApplyCfg<n, 1, 1, GEO>::CS * sizeof(double);
+  auto k = sipg_apply_kernel<n, 1, 1, GEO, CPB, minb_pois<n>()>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

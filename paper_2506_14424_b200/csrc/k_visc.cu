@@ -7,14 +7,16 @@ namespace dgvv {
 
 cudaError_t upload_tables_visc(const Tab1D* tabs) { return tu_upload_tables(tabs); }
 
-template <int n> constexpr int cpb_visc() { return (128 / (n * n)) > 0 ? (128 / (n * n)) : 1; }
+// cells per CTA and min resident CTAs per SM (register cap), chosen by measurement
+template <int n> constexpr int cpb_visc() { return n == 2 ? 32 : n == 3 ? 14 : n == 4 ? 8 : n == 5 ? 5 : 3; }
+template <int n> constexpr int minb_visc() { return n == 2 ? 2 : n == 3 ? 3 : n == 4 ? 4 : n == 5 ? 3 : 2; }
 
 template <int n, int FORM, int GEO>
 static cudaError_t run(const ApplyArgs& a, cudaStream_t s) {
   constexpr int CPB = cpb_visc<n>();
   constexpr int NC = 3;
-  const size_t smem = (size_t)CPB * 4 * NC * n * n * n * sizeof(double);
-  auto k = sipg_apply_kernel<n, NC, FORM, GEO, CPB>;
+  const size_t smem = (size_t)CPB * ApplyCfg<n, NC, FORM, GEO>::CS * sizeof(double);
+  auto k = sipg_apply_kernel<n, NC, FORM, GEO, CPB, minb_visc<n>()>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

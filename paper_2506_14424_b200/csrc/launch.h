@@ -28,9 +28,9 @@ cudaError_t launch_tensor3(int nin, int nout, int nc, const double* M, const dou
 cudaError_t launch_cart_geom(const double* nodes, const int* nbr, int n_total, double* cart, cudaStream_t s);
 cudaError_t launch_cart_points(const double* cart, int n_owned, int n_total, int n, double* xq, double* xf,
                                cudaStream_t s);
-cudaError_t launch_gen_geom(const GeoTab& g, const double* nodes, int n_total, double* vmet, double* fmet,
-                            double* xq, double* xf, int* bad, cudaStream_t s);
-cudaError_t launch_gen_H(const double* vmet, const double* fmet, const int* nbr, int n_total, int n, double* H,
+cudaError_t launch_gen_geom(const GeoTab& g, const double* nodes, int n_total, double* vJi, double* jxw,
+                            double* fJi, double* fdA, double* xq, double* xf, int* bad, cudaStream_t s);
+cudaError_t launch_gen_H(const double* jxw, const double* fdA, const int* nbr, int n_total, int n, double* H,
                          cudaStream_t s);
 cudaError_t launch_align_check(const double* xf, const int* nbr, int n_owned, int n, double tol, int* bad,
                                cudaStream_t s);

@@ -74,10 +74,10 @@ __global__ void cart_points_kernel(const double* cart, int n_owned, int n_total,
 
 // ----------------------------------------------------------------- general geometry
 // x(xi) = sum_a X_a L_a(xi) over the (m+1)^3 GLL nodes; J_{i,k} = d x_i / d xi_k.
-// vmet[cell][10][n^3] (J^-1 row-major k,j; JxW), fmet[cell][6][13][n^2] (J^-1, outward unit
-// normal n = J^-T N / |J^-T N|, dA = det J |J^-T N| w_a w_b  — Nanson), xq, xf points.
-__global__ void gen_geom_kernel(GeoTab G, const double* nodes, int n_total, double* vmet,
-                                double* fmet, double* xq, double* xf, int* bad) {
+// vJi[cell][9][n^3] (J^-1 row-major k,j), jxw; fJi[cell][6][9][n^2] (own J^-1 at face points),
+// fdA = det J |J^-T N| w_a w_b (Nanson; the unit normal is recomputed from J^-1), xq, xf points.
+__global__ void gen_geom_kernel(GeoTab G, const double* nodes, int n_total, double* vJi, double* jxw,
+                                double* fJi, double* fdA, double* xq, double* xf, int* bad) {
   const int n = G.n, m1 = G.m + 1, n2 = n * n, n3 = n2 * n, P = n3 + 6 * n2;
   const long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (long)n_total * P) return;
@@ -134,34 +134,32 @@ __global__ void gen_geom_kernel(GeoTab G, const double* nodes, int n_total, doub
   Ji[7] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * id;
   Ji[8] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * id;
   if (f < 0) {
-    double* o = vmet + (size_t)c * VMET_NV * n3 + r;
+    double* o = vJi + (size_t)c * 9 * n3 + r;
     for (int k = 0; k < 9; ++k) o[k * n3] = Ji[k];
-    o[9 * n3] = det * w;
+    jxw[(size_t)c * n3 + r] = det * w;
     for (int i = 0; i < 3; ++i) xq[((size_t)c * n3 + r) * 3 + i] = x[i];
   } else {
-    const double sg = s ? 1.0 : -1.0;
-    const double v0 = sg * Ji[3 * d], v1 = sg * Ji[3 * d + 1], v2 = sg * Ji[3 * d + 2];
+    const double v0 = Ji[3 * d], v1 = Ji[3 * d + 1], v2 = Ji[3 * d + 2];
     const double ln = sqrt(v0 * v0 + v1 * v1 + v2 * v2);
-    double* o = fmet + ((size_t)c * 6 + f) * FMET_NV * n2 + p;
+    double* o = fJi + ((size_t)c * 6 + f) * 9 * n2 + p;
     for (int k = 0; k < 9; ++k) o[k * n2] = Ji[k];
-    o[9 * n2] = v0 / ln; o[10 * n2] = v1 / ln; o[11 * n2] = v2 / ln;
-    o[12 * n2] = det * ln * w;
+    fdA[((size_t)c * 6 + f) * n2 + p] = det * ln * w;
     for (int i = 0; i < 3; ++i) xf[(((size_t)c * 6 + f) * n2 + p) * 3 + i] = x[i];
   }
 }
 
 // H_K from the streamed metric: V = sum JxW, A_f = sum dA  (G3)
-__global__ void gen_H_kernel(const double* vmet, const double* fmet, const int* nbr, int n_total,
+__global__ void gen_H_kernel(const double* jxw, const double* fdA, const int* nbr, int n_total,
                              int n, double* H) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= n_total) return;
   const int n2 = n * n, n3 = n2 * n;
   double V = 0.0;
-  for (int q = 0; q < n3; ++q) V += vmet[((size_t)c * VMET_NV + 9) * n3 + q];
+  for (int q = 0; q < n3; ++q) V += jxw[(size_t)c * n3 + q];
   double num = 0.0;
   for (int f = 0; f < 6; ++f) {
     double A = 0.0;
-    for (int p = 0; p < n2; ++p) A += fmet[(((size_t)c * 6 + f) * FMET_NV + 12) * n2 + p];
+    for (int p = 0; p < n2; ++p) A += fdA[((size_t)c * 6 + f) * n2 + p];
     const int nb = nbr[c * 6 + f];
     num += (nb == NB_DIRICHLET || nb == NB_NEUMANN) ? A : 0.5 * A;
   }
