@@ -1,8 +1,39 @@
-// k_newton.cu — Newton-linearised viscous apply (K2).  Placeholder until the kernel lands.
+// k_newton.cu — instantiations of the Newton-linearised viscous apply (K2).
 #include "tu_tables.cuh"
+#include "newton_apply.cuh"
 #include "launch.h"
 
 namespace dgvv {
+
 cudaError_t upload_tables_newton(const Tab1D* tabs) { return tu_upload_tables(tabs); }
-cudaError_t launch_newton(int, int, const ApplyArgs&, cudaStream_t) { return cudaErrorNotSupported; }
+
+template <int n> constexpr int cpb_newton() { return n == 2 ? 16 : n == 3 ? 8 : n == 4 ? 4 : n == 5 ? 3 : 2; }
+
+template <int n, int GEO>
+static cudaError_t run(const ApplyArgs& a, cudaStream_t s) {
+  constexpr int CPB = cpb_newton<n>();
+  const size_t smem = (size_t)CPB * NewtonCfg<n, GEO>::CS * sizeof(double);
+  auto k = newton_apply_kernel<n, GEO, CPB, 1>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  if (a.n_proc <= 0) return cudaSuccess;
+  k<<<(a.n_proc + CPB - 1) / CPB, CPB * n * n, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_newton(int n, int geo, const ApplyArgs& a, cudaStream_t s) {
+  switch (n) {
+    case 2: return geo ? run<2, 1>(a, s) : run<2, 0>(a, s);
+    case 3: return geo ? run<3, 1>(a, s) : run<3, 0>(a, s);
+    case 4: return geo ? run<4, 1>(a, s) : run<4, 0>(a, s);
+    case 5: return geo ? run<5, 1>(a, s) : run<5, 0>(a, s);
+    case 6: return geo ? run<6, 1>(a, s) : run<6, 0>(a, s);
+    default: return cudaErrorNotSupported;
+  }
+}
+
 }  // namespace dgvv

@@ -8,8 +8,20 @@ namespace dgvv {
 cudaError_t upload_tables_visc(const Tab1D* tabs) { return tu_upload_tables(tabs); }
 
 // cells per CTA and min resident CTAs per SM (register cap), chosen by measurement
-template <int n> constexpr int cpb_visc() { return n == 2 ? 32 : n == 3 ? 14 : n == 4 ? 8 : n == 5 ? 5 : 3; }
-template <int n> constexpr int minb_visc() { return n == 2 ? 2 : n == 3 ? 3 : n == 4 ? 4 : n == 5 ? 3 : 2; }
+#ifndef CPB4
+#define CPB4 8
+#endif
+#ifndef CPB5
+#define CPB5 5
+#endif
+#ifndef MINB4
+#define MINB4 4
+#endif
+#ifndef MINB5
+#define MINB5 3
+#endif
+template <int n> constexpr int cpb_visc() { return n == 2 ? 32 : n == 3 ? 14 : n == 4 ? CPB4 : n == 5 ? CPB5 : 3; }
+template <int n> constexpr int minb_visc() { return n == 2 ? 2 : n == 3 ? 3 : n == 4 ? MINB4 : n == 5 ? MINB5 : 2; }
 
 template <int n, int FORM, int GEO>
 static cudaError_t run(const ApplyArgs& a, cudaStream_t s) {

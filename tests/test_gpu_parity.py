@@ -291,3 +291,45 @@ def test_c3_full_size_sampled_carreau():
     cells = _sample_cells(m, 48)
     ref = dg.viscous_apply(d, u, dg.CarreauNu(d, ulin, laws.C3_CARREAU), cells=cells)
     assert rel(y[cells], ref) < TOL
+
+
+# ------------------------------------------------------------------ Newton (K2)
+@pytest.mark.parametrize("mk,k", [(lambda: cube(3), 4), (lambda: deformed_cube(3, 2), 2),
+                                  (lambda: bfs(nx_in=2, ny_in=1, nx_out=4, nz=3), 3), (lambda: cube(2), 1)])
+def test_newton_apply_parity(mk, k):
+    """J(u0) w on the GPU == oracle newton_apply (reading G10; FD-pinned in the oracle tests)."""
+    m = mk()
+    d = dg.Disc(m, k)
+    law = laws.C3_CARREAU
+    if m.map_degree == 1 and m.periods == (0.0, 0.0, 0.0):
+        u0 = c3_linearization(m, k)
+    else:
+        u0 = 2.0 * uniform(7, m.n_cells * 3 * d.N)
+    w = uniform(0, len(u0))
+    ref = dg.newton_apply(d, u0, w, law)
+    ctx = Ctx(m, k, visc_law=law)
+    from paper_2506_14424_b200 import DgvvError
+    with pytest.raises(DgvvError):
+        ctx.apply_linearized_viscous(dev(w), dev(w * 0))
+    ul = dev(u0)
+    ctx.update_viscosity(ul)
+    y = torch.empty_like(ul)
+    ctx.apply_linearized_viscous(dev(w), y)
+    assert rel(host(y), ref) < TOL
+
+
+def test_newton_full_size_sampled_c3():
+    m = cube(64)
+    k = 4
+    d = dg.Disc(m, k)
+    u0 = c3_linearization(m, k)
+    w = uniform(0, len(u0))
+    ctx = Ctx(m, k, visc_law=laws.C3_CARREAU)
+    ul = dev(u0)
+    ctx.update_viscosity(ul)
+    y = torch.empty_like(ul)
+    ctx.apply_linearized_viscous(dev(w), y)
+    y = host(y).reshape(m.n_cells, 3, 125)
+    cells = _sample_cells(m, 32)
+    ref = dg.newton_apply(d, u0, w, laws.C3_CARREAU, cells=cells)
+    assert rel(y[cells], ref) < TOL
