@@ -181,45 +181,91 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def _dist_setup(world, rank):
+    """torch.distributed (NCCL) for barriers/timing reductions; the library's own NCCL
+    communicator for the ghost exchange (unique id broadcast through torch.distributed)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2506_14424_b200.dgvv import nccl_comm_init, nccl_unique_id
+    dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0))))
+    uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+    if rank == 0:
+        uid.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
+    dist.broadcast(uid, 0)
+    return nccl_comm_init(bytes(uid.cpu().numpy().tobytes()), world, rank)
+
+
+def build_workload(cfg, world, scaling):
+    """Global mesh: strong scaling splits the config's mesh; weak scaling (C2) stacks one
+    C2 cube per GPU in z so every rank owns exactly the C2 workload."""
+    if scaling == "weak" and cfg["name"] == "C2" and world > 1:
+        return deformed_cube(32, 3, nz_mult=world)
+    return cfg["mesh"]()
+
+
 def run_ours(args, rank, world):
     import torch
     from paper_2506_14424_b200.dgvv import Context
+    from paper_2506_14424_b200.partition import slab_partition
 
     cfg = CONFIGS[args.config]
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
-    if world > 1:
-        raise SystemExit("multi-GPU bench: see --gpus handling (not in this build)")
-    m = cfg["mesh"]()
+    comm = _dist_setup(world, rank) if world > 1 else None
+    scaling = args.scaling or ("weak" if cfg["name"] == "C2" else "strong")
+    mg = build_workload(cfg, world, scaling)
     k = cfg["k"]
     n = k + 1
-    ctx = Context(m, k, visc_law=cfg["law"])
-    N = m.n_cells * 3 * n ** 3
-    geo = "general" if m.map_degree > 1 else "cartesian"
+    per = 3 * n ** 3
+    if world > 1:
+        part = slab_partition(mg, world, rank)
+        ctx = Context(part, k, visc_law=cfg["law"], n_owned=part.n_owned, n_ghost=part.n_ghost,
+                      ghost_global_id=part.ghost_global_id, ghost_owner=part.ghost_owner,
+                      first_global_cell=part.first, nccl_comm=comm)
+        first, n_own = part.first, part.n_owned
+    else:
+        ctx = Context(mg, k, visc_law=cfg["law"])
+        first, n_own = 0, mg.n_cells
+    N_glob = mg.n_cells * per
+    N = n_own * per
+    geo = "general" if mg.map_degree > 1 else "cartesian"
     if cfg["law"]["kind"] == "carreau":
         from inputs.vectors import c3_linearization, c5_linearization
-        ulin = (c3_linearization if cfg["name"] == "C3" else c5_linearization)(m, k)
-        ulin_d = torch.from_numpy(ulin).to(dev)
+        ulin = (c3_linearization if cfg["name"] == "C3" else c5_linearization)(mg, k)
+        ulin_d = torch.from_numpy(ulin[first * per:(first + n_own) * per].copy()).to(dev)
         ctx.update_viscosity(ulin_d)
-    src0 = uniform(0, N)
+    src0 = uniform(0, N_glob)[first * per:(first + n_own) * per].copy()
     npairs = 4
     srcs = [torch.from_numpy(src0 if i == 0 else uniform(100 + i, N)).to(dev) for i in range(npairs)]
     dsts = [torch.empty(N, dtype=torch.float64, device=dev) for _ in range(npairs)]
     stream = torch.cuda.current_stream()
 
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
     for i in range(max(3, args.warmup)):
         ctx.apply_viscous(srcs[i % npairs], dsts[i % npairs])
-    torch.cuda.synchronize()
+    barrier()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(dev.index) as clk:
-        torch.cuda.synchronize()
+        barrier()
         start.record(stream)
         for i in range(args.steps):
             ctx.apply_viscous(srcs[i % npairs], dsts[i % npairs])
         end.record(stream)
-        torch.cuda.synchronize()
-    t_ms = start.elapsed_time(end) / args.steps
-    value = N / (t_ms * 1e-3)
+        barrier()
+    t_ms = max_over_ranks(start.elapsed_time(end) / args.steps)
+    value = N_glob / (t_ms * 1e-3)
 
     # end to end through the public API with host buffers (pinned), copies inside the timed region
     hsrc = torch.from_numpy(src0).pin_memory()
@@ -231,7 +277,7 @@ def run_ours(args, rank, world):
         dsrc.copy_(hsrc, non_blocking=True)
         ctx.apply_viscous(dsrc, ddst)
         hdst.copy_(ddst, non_blocking=True)
-    torch.cuda.synchronize()
+    barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(e_steps):
@@ -239,11 +285,11 @@ def run_ours(args, rank, world):
         ctx.apply_viscous(dsrc, ddst)
         hdst.copy_(ddst, non_blocking=True)
     e1.record(stream)
-    torch.cuda.synchronize()
-    e_ms = e0.elapsed_time(e1) / e_steps
+    barrier()
+    e_ms = max_over_ranks(e0.elapsed_time(e1) / e_steps)
 
     hbm_peak, peak_src, _ = load_peaks()
-    bytes_launch = algorithmic_bytes_per_cell(n, geo) * m.n_cells
+    bytes_launch = algorithmic_bytes_per_cell(n, geo) * n_own
     flops_launch = algorithmic_flops_per_dof(n, geo) * N
     t_hbm = bytes_launch / (hbm_peak * 1e9)
     t_alu = flops_launch / (FP64_PEAK_TFLOPS * 1e12)
@@ -257,27 +303,38 @@ def run_ours(args, rank, world):
                 "algorithmic_bytes_per_launch": bytes_launch}
     alu_roof = {"bound": "alu", "achieved": flops_launch / (t_ms * 1e-3) / 1e12, "peak": FP64_PEAK_TFLOPS,
                 "unit": "TFLOP/s", "frac": flops_launch / (t_ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
-                "peak_source": "nominal FP64 148 SM x 64 FMA x 2 x 1.965 GHz (DESIGN.md)",
+                "peak_source": "nominal FP64 148 SM x 64 FMA x 2 x 1.965 GHz (DESIGN.md; measured DFMA 34.2)",
                 "algorithmic_flops_per_launch": flops_launch}
     roof, other = (hbm_roof, alu_roof) if t_hbm >= t_alu else (alu_roof, hbm_roof)
-
+    launches = args.steps * (1 if world == 1 else 2 + sum(1 for _ in ctx.ghost_layout()))
     line = {"metric": METRIC, "value": value, "unit": "DoFs/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": t_ms, "higher_is_better": True, "scaling": "strong",
+            "warmup": args.warmup, "ms_per_step": t_ms, "higher_is_better": True,
+            "scaling": scaling if world > 1 else "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg["desc"], "dofs": N, "cells": m.n_cells, "degree": k,
-                       "geometry": geo, "l2": f"{npairs} rotating src/dst pairs ({npairs * 2 * N * 8 / 1e6:.0f} MB) "
-                       "+ streamed metric > 126 MB L2", "step": "one dgvv_apply_viscous"},
-            "gpu_launches": args.steps,
+            "config": {"workload": cfg["desc"] + (f"; weak scaling: {world} C2 cubes stacked in z, one per GPU"
+                                                  if world > 1 and scaling == "weak" else ""),
+                       "dofs": N_glob, "cells": mg.n_cells, "degree": k, "geometry": geo,
+                       "parallelism": f"slab domain decomposition x{world}, NCCL ghost-cell exchange" if world > 1 else "1 GPU",
+                       "l2": f"{npairs} rotating src/dst pairs ({npairs * 2 * N * 8 / 1e6:.0f} MB) + coefficient/metric "
+                             "streams > 126 MB L2", "step": "one dgvv_apply_viscous"},
+            "gpu_launches": launches,
             "roofline": roof, "roofline_other": other,
-            "e2e": {"value": N / (e_ms * 1e-3), "unit": "DoFs/s", "h2d_bytes_per_step": N * 8,
-                    "d2h_bytes_per_step": N * 8, "ms_per_step": e_ms},
+            "e2e": {"value": N_glob / (e_ms * 1e-3), "unit": "DoFs/s", "h2d_bytes_per_step": N_glob * 8,
+                    "d2h_bytes_per_step": N_glob * 8, "ms_per_step": e_ms},
             "clocks": clk.result()}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = time_cpu_oracle(cfg, seconds=args.cpu_seconds)
         cb.pop("seconds")
         cb.pop("dofs")
         line["cpu_baseline"] = cb
-    print(json.dumps(line), flush=True)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.barrier()
+        ctx.close()
+        from paper_2506_14424_b200 import _abi
+        _abi.lib().dgvv_nccl_comm_destroy(comm)
+        torch.distributed.destroy_process_group()
 
 
 def main():
@@ -289,6 +346,8 @@ def main():
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default=None,
+                    help="multi-GPU: weak (C2 default: one C2 cube per GPU) or strong (split the config's mesh)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

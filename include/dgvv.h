@@ -174,6 +174,24 @@ dgvv_status dgvv_sizes(const dgvv_ctx* ctx, int32_t level, int64_t* n_local_dofs
 dgvv_status dgvv_coefficient_range(dgvv_ctx* ctx, int32_t op, int32_t level, double* lo,
                                    double* hi);
 
+/* Ghost cells (multi-GPU).  Each rank owns a contiguous range of global cell
+ * ids; the off-rank face neighbours are its ghosts, stored in (owner rank, global id) order.
+ * Per apply the library packs, for every peer, its owned cells that have a face neighbour
+ * owned by that peer (ascending id) and exchanges them with grouped ncclSend/ncclRecv on an
+ * internal stream while the interior cells are computed; the cells with a ghost neighbour
+ * run after the exchange.  Without a communicator (external-exchange mode) the caller fills
+ * the ghost buffers itself, using dgvv_pack_ghosts on the peer's context. */
+enum { DGVV_GHOST_VISCOUS = 0, DGVV_GHOST_POISSON = 1, DGVV_GHOST_ULIN = 2 };
+/* Peers in ascending rank; arrays (may be NULL) sized by a first call that only reads n_peers. */
+dgvv_status dgvv_ghost_layout(const dgvv_ctx* ctx, int32_t* n_peers, int32_t* peer_ranks,
+                              int32_t* send_counts, int32_t* recv_counts);
+/* sendbuf = the cells every peer needs from src, concatenated in peer order (device). */
+dgvv_status dgvv_pack_ghosts(dgvv_ctx* ctx, int32_t level, int32_t kind, const double* src,
+                             double* sendbuf, dgvv_stream stream);
+/* Device pointer of the ghost buffer of `kind` on `level` ([n_ghost][comp][n^3], owned by the
+ * library). */
+dgvv_status dgvv_ghost_buffer(dgvv_ctx* ctx, int32_t level, int32_t kind, double** out);
+
 /* NCCL plumbing (multi-GPU): 128-byte unique id on rank 0, broadcast by the caller, then a
  * communicator on every rank.  The library loads libnccl.so.2 at run time. */
 dgvv_status dgvv_nccl_get_unique_id(char out_id[128]);

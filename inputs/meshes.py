@@ -129,10 +129,21 @@ def cube(N: int, lo=0.0, hi=1.0, bc=DIRICHLET, periodic=(False, False, False), g
     return m
 
 
-def deformed_cube(N: int, map_degree: int, amp: float = 0.05, bc=DIRICHLET) -> Mesh:
+def deformed_cube(N: int, map_degree: int, amp: float = 0.05, bc=DIRICHLET, nz_mult: int = 1) -> Mesh:
     """C2: [0,1]^3, N^3 cells, X = x^ + amp sin(2 pi x^) sin(2 pi y^) sin(2 pi z^) (1,1,1),
-    sampled at the degree-`map_degree` GLL nodes of every cell (iso-parametric map)."""
-    base = cube(N, bc=bc)
+    sampled at the degree-`map_degree` GLL nodes of every cell (iso-parametric map).
+    nz_mult > 1 stacks nz_mult such unit cubes in z ([0,1]^2 x [0,nz_mult], N x N x N nz_mult
+    cells; the weak-scaling workload: one C2 cube per GPU)."""
+    if nz_mult == 1:
+        base = cube(N, bc=bc)
+    else:
+        g = np.linspace(0.0, 1.0, N + 1)
+        gz = np.linspace(0.0, float(nz_mult), N * nz_mult + 1)
+        ids, verts = box_block(g, g, gz, "xyz")
+        nb = np.empty((ids.size, 6), dtype=np.int64)
+        code = bc_code(bc)
+        _block_neighbors(ids, nb, [code] * 3, [code] * 3, (False, False, False))
+        base = Mesh(ids.size, nb, verts, 1)
     m1 = map_degree + 1
     g = gll_points01(map_degree)
     gz, gy, gx = np.meshgrid(g, g, g, indexing="ij")        # lexicographic, x fastest
@@ -142,8 +153,8 @@ def deformed_cube(N: int, map_degree: int, amp: float = 0.05, bc=DIRICHLET) -> M
     xh = x0[:, None, :] + h[:, None, :] * ref[None, :, :]
     s = np.sin(2 * np.pi * xh[..., 0]) * np.sin(2 * np.pi * xh[..., 1]) * np.sin(2 * np.pi * xh[..., 2])
     X = xh + amp * s[..., None]
-    assert X.shape == (N ** 3, m1 ** 3, 3)
-    m = Mesh(N ** 3, base.neighbor, X, map_degree, (0.0, 0.0, 0.0), name=f"deformed{N}_m{map_degree}")
+    assert X.shape == (base.n_cells, m1 ** 3, 3)
+    m = Mesh(base.n_cells, base.neighbor, X, map_degree, (0.0, 0.0, 0.0), name=f"deformed{N}_m{map_degree}x{nz_mult}")
     m.meta["amp"] = amp
     m.validate()
     return m

@@ -19,6 +19,7 @@ BC_DIRICHLET, BC_NEUMANN = 1, 2
 LAW_CONST, LAW_SIN3, LAW_EXP, LAW_CARREAU = 0, 1, 2, 3
 OP_VISCOUS, OP_POISSON = 0, 1
 FORM_DIVERGENCE, FORM_LAPLACE = 0, 1
+GHOST_VISCOUS, GHOST_POISSON, GHOST_ULIN = 0, 1, 2
 
 
 class DgvvLaw(C.Structure):
@@ -62,6 +63,9 @@ _SIGS = {
     "dgvv_dot": [VP, I32, I32, VP, VP, PD, VP],
     "dgvv_sizes": [VP, I32, C.POINTER(I64), C.POINTER(I64)],
     "dgvv_coefficient_range": [VP, I32, I32, PD, PD],
+    "dgvv_ghost_layout": [VP, C.POINTER(I32), C.POINTER(I32), C.POINTER(I32), C.POINTER(I32)],
+    "dgvv_pack_ghosts": [VP, I32, I32, VP, VP, VP],
+    "dgvv_ghost_buffer": [VP, I32, I32, C.POINTER(VP)],
     "dgvv_nccl_get_unique_id": [C.c_char_p],
     "dgvv_nccl_comm_init": [C.c_char_p, I32, I32, C.POINTER(VP)],
     "dgvv_nccl_comm_destroy": [VP],

@@ -148,12 +148,17 @@ struct dgvv_ctx {
   int form = 0;
   double ip = 1.0;
   const double* ulin = nullptr;
-  // comm
+  // comm: peers exist whenever there are ghosts; NCCL transport only with a communicator
+  // (without one the caller fills the ghost buffers: external-exchange mode, used by tests)
   void* comm = nullptr;
-  int rank = 0, nranks = 1;
   std::vector<Peer> peers;
   double* d_sendbuf = nullptr;
   size_t sendbuf_len = 0;
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_pack = nullptr, ev_comm = nullptr;
+  int* d_interior = nullptr;      // owned cells without a ghost neighbour
+  int* d_boundary = nullptr;      // owned cells with a ghost neighbour
+  int n_interior = 0, n_boundary = 0;
   // scratch
   double* d_part = nullptr;     // 1024 partials
   double* d_scal = nullptr;     // 16 scalars
@@ -208,26 +213,44 @@ dgvv_status array_range(dgvv_ctx* c, const double* v, long n, cudaStream_t s, do
   return DGVV_OK;
 }
 
-// ghost exchange of a level vector (NC components): pack owned cells per peer, grouped
-// ncclSend/ncclRecv into the level's ghost buffer.  No-op on one GPU.
-dgvv_status exchange(dgvv_ctx* c, int l, int nc, const double* src, double* ghost, cudaStream_t s) {
-  if (c->nranks <= 1 || c->peers.empty()) return DGVV_OK;
+// pack the owned cells every peer needs into the send buffer (peer-rank order)
+dgvv_status pack(dgvv_ctx* c, int l, int nc, const double* src, double* sendbuf, cudaStream_t s) {
   const int n = c->L[l].n;
   const int len = nc * n * n * n;
   size_t off = 0;
   for (auto& P : c->peers) {
-    DGVV_CUDA_TRY(launch_gather_cells(src, P.d_send, P.n_send, len, c->d_sendbuf + off, s));
+    DGVV_CUDA_TRY(launch_gather_cells(src, P.d_send, P.n_send, len, sendbuf + off, s));
     off += (size_t)P.n_send * len;
   }
+  return DGVV_OK;
+}
+
+// ghost exchange of a level vector (NC components): pack on s, grouped ncclSend/ncclRecv on
+// the comm stream into `ghost`; ev_comm marks completion (the caller's stream must wait on it
+// before reading ghosts).  No-op without ghosts or without a communicator.
+dgvv_status exchange(dgvv_ctx* c, int l, int nc, const double* src, double* ghost, cudaStream_t s) {
+  if (!c->comm || c->peers.empty()) return DGVV_OK;
+  const int n = c->L[l].n;
+  const int len = nc * n * n * n;
+  TRY(pack(c, l, nc, src, c->d_sendbuf, s));
+  DGVV_CUDA_TRY(cudaEventRecord(c->ev_pack, s));
+  DGVV_CUDA_TRY(cudaStreamWaitEvent(c->comm_stream, c->ev_pack, 0));
   ncclComm_t comm = (ncclComm_t)c->comm;
   NCCL_TRY(g_nccl.groupStart());
-  off = 0;
+  size_t off = 0;
   for (auto& P : c->peers) {
-    if (P.n_send) NCCL_TRY(g_nccl.send(c->d_sendbuf + off, (size_t)P.n_send * len, ncclDouble, P.rank, comm, s));
-    if (P.n_recv) NCCL_TRY(g_nccl.recv(ghost + (size_t)P.recv_off * len, (size_t)P.n_recv * len, ncclDouble, P.rank, comm, s));
+    if (P.n_send) NCCL_TRY(g_nccl.send(c->d_sendbuf + off, (size_t)P.n_send * len, ncclDouble, P.rank, comm, c->comm_stream));
+    if (P.n_recv) NCCL_TRY(g_nccl.recv(ghost + (size_t)P.recv_off * len, (size_t)P.n_recv * len, ncclDouble, P.rank, comm, c->comm_stream));
     off += (size_t)P.n_send * len;
   }
   NCCL_TRY(g_nccl.groupEnd());
+  DGVV_CUDA_TRY(cudaEventRecord(c->ev_comm, c->comm_stream));
+  return DGVV_OK;
+}
+
+dgvv_status exchange_sync(dgvv_ctx* c, int l, int nc, const double* src, double* ghost, cudaStream_t s) {
+  TRY(exchange(c, l, nc, src, ghost, s));
+  if (c->comm && !c->peers.empty()) DGVV_CUDA_TRY(cudaStreamWaitEvent(s, c->ev_comm, 0));
   return DGVV_OK;
 }
 
@@ -270,14 +293,28 @@ dgvv_status op_ready(dgvv_ctx* c, int op) {
   return DGVV_OK;
 }
 
-// launch one apply (with exchange) in a given mode
-dgvv_status run_apply(dgvv_ctx* c, int op, int l, ApplyArgs a, cudaStream_t s) {
+// launch one apply in a given mode.  Multi-GPU: interior cells run while NCCL moves the
+// ghost cells on the comm stream; cells with a ghost neighbour run after the exchange event.
+dgvv_status run_apply(dgvv_ctx* c, int op, int l, ApplyArgs a, cudaStream_t s, bool newton = false) {
   const int nc = op == DGVV_OP_VISCOUS ? 3 : 1;
-  TRY(exchange(c, l, nc, a.src, const_cast<double*>(a.ghost), s));
   const int form = op == DGVV_OP_VISCOUS ? c->form : DGVV_FORM_LAPLACE;
-  cudaError_t e = launch_apply(nc, c->L[l].n, form, c->geo, a, s);
-  if (e != cudaSuccess) return dgvv_fail(DGVV_ECUDA, "apply kernel: %s", cudaGetErrorString(e));
-  return DGVV_OK;
+  auto launch = [&](const ApplyArgs& x) -> dgvv_status {
+    cudaError_t e = newton ? launch_newton(c->L[l].n, c->geo, x, s) : launch_apply(nc, c->L[l].n, form, c->geo, x, s);
+    if (e == cudaErrorNotSupported) return dgvv_fail(DGVV_EUNSUPPORTED, "kernel not built for degree %d", c->L[l].k);
+    if (e != cudaSuccess) return dgvv_fail(DGVV_ECUDA, "apply kernel: %s", cudaGetErrorString(e));
+    return DGVV_OK;
+  };
+  if (!c->comm || c->peers.empty()) return launch(a);
+  TRY(exchange(c, l, nc, a.src, const_cast<double*>(a.ghost), s));
+  ApplyArgs ai = a;
+  ai.cell_list = c->d_interior;
+  ai.n_proc = c->n_interior;
+  TRY(launch(ai));
+  DGVV_CUDA_TRY(cudaStreamWaitEvent(s, c->ev_comm, 0));
+  ApplyArgs ab = a;
+  ab.cell_list = c->d_boundary;
+  ab.n_proc = c->n_boundary;
+  return launch(ab);
 }
 
 dgvv_status ensure_dinv(dgvv_ctx* c, int op, int l, cudaStream_t s) {
@@ -311,7 +348,7 @@ dgvv_status ensure_dinv(dgvv_ctx* c, int op, int l, cudaStream_t s) {
 dgvv_status dot_dev(dgvv_ctx* c, const double* a, const double* b, long n, double* dout, cudaStream_t s) {
   const int nb = (int)std::max(1L, std::min((long)kPartials, (n + 255) / 256));
   DGVV_CUDA_TRY(launch_dot(a, b, n, c->d_part, nb, dout, s));
-  if (c->nranks > 1) NCCL_TRY(g_nccl.allReduce(dout, dout, 1, ncclDouble, ncclSum, (ncclComm_t)c->comm, s));
+  if (c->comm) NCCL_TRY(g_nccl.allReduce(dout, dout, 1, ncclDouble, ncclSum, (ncclComm_t)c->comm, s));
   return DGVV_OK;
 }
 
@@ -412,6 +449,9 @@ void dgvv_destroy(dgvv_ctx* c) {
   for (auto& L : c->L)
     for (int o = 0; o < 2; ++o) L.scratch[o].clear();
   for (void* p : c->allocs) cudaFree(p);
+  if (c->ev_pack) cudaEventDestroy(c->ev_pack);
+  if (c->ev_comm) cudaEventDestroy(c->ev_comm);
+  if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
   delete c;
 }
 
@@ -601,27 +641,20 @@ static dgvv_status setup_impl(const dgvv_mesh* m, int32_t degree, const dgvv_law
     DGVV_CUDA_TRY(cudaStreamSynchronize(s));
   }
 
-  // ---- communication plan
-  if (opt && opt->nccl_comm) {
-    TRY(nccl_load());
-    c->comm = opt->nccl_comm;
-    int nr = 0, rk = 0;
-    // rank/size are not queried through NCCL (older ABIs): derive peers from ghost owners
+  // ---- communication plan: peers from the ghost owners (sorted), send lists by the rule of
+  // partition.py (owned cells with a face neighbour owned by the peer, ascending id)
+  if (c->n_ghost > 0) {
     std::vector<int> owners;
     for (int i = 0; i < c->n_ghost; ++i) owners.push_back(m->ghost_owner[gperm[i]]);
     std::vector<int> uniq = owners;
     std::sort(uniq.begin(), uniq.end());
     uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
-    (void)nr; (void)rk;
-    c->nranks = 2;   // > 1: exchange active
-    size_t maxlen = 0;
+    size_t total_send = 0;
     for (int r : uniq) {
       Peer P;
       P.rank = r;
-      // receive range
       P.recv_off = (int)(std::lower_bound(owners.begin(), owners.end(), r) - owners.begin());
       P.n_recv = (int)(std::upper_bound(owners.begin(), owners.end(), r) - owners.begin()) - P.recv_off;
-      // send list: owned cells adjacent to a ghost owned by r, ascending local (= global) id
       std::vector<int> send;
       for (int lc = 0; lc < c->n_owned; ++lc)
         for (int f = 0; f < 6; ++f) {
@@ -631,31 +664,52 @@ static dgvv_status setup_impl(const dgvv_mesh* m, int32_t degree, const dgvv_law
       P.n_send = (int)send.size();
       TRY(dalloc(c, &P.d_send, send.size()));
       DGVV_CUDA_TRY(cudaMemcpy(P.d_send, send.data(), send.size() * sizeof(int), cudaMemcpyHostToDevice));
-      maxlen += send.size();
+      total_send += send.size();
       c->peers.push_back(P);
     }
     int nmax = 0;
     for (auto& L : c->L) nmax = std::max(nmax, L.n);
-    c->sendbuf_len = maxlen * 3 * nmax * nmax * nmax;
+    c->sendbuf_len = total_send * 3 * nmax * nmax * nmax;
     TRY(dalloc(c, &c->d_sendbuf, c->sendbuf_len));
-    // handshake: counts must agree pairwise
-    int* d_cnt = nullptr;
-    TRY(dalloc(c, &d_cnt, 2 * c->peers.size() + 2));
-    std::vector<int> hs(c->peers.size());
-    for (size_t i = 0; i < c->peers.size(); ++i) hs[i] = c->peers[i].n_send;
-    DGVV_CUDA_TRY(cudaMemcpy(d_cnt, hs.data(), hs.size() * sizeof(int), cudaMemcpyHostToDevice));
-    NCCL_TRY(g_nccl.groupStart());
-    for (size_t i = 0; i < c->peers.size(); ++i) {
-      NCCL_TRY(g_nccl.send(d_cnt + i, 1, ncclInt32, c->peers[i].rank, (ncclComm_t)c->comm, s));
-      NCCL_TRY(g_nccl.recv(d_cnt + c->peers.size() + i, 1, ncclInt32, c->peers[i].rank, (ncclComm_t)c->comm, s));
+    std::vector<int> inner, bnd;
+    for (int lc = 0; lc < c->n_owned; ++lc) {
+      bool g = false;
+      for (int f = 0; f < 6; ++f) g |= nbr[(size_t)lc * 6 + f] >= c->n_owned;
+      (g ? bnd : inner).push_back(lc);
     }
-    NCCL_TRY(g_nccl.groupEnd());
-    std::vector<int> got(c->peers.size());
-    DGVV_CUDA_TRY(cudaMemcpyAsync(got.data(), d_cnt + c->peers.size(), got.size() * sizeof(int), cudaMemcpyDeviceToHost, s));
-    DGVV_CUDA_TRY(cudaStreamSynchronize(s));
-    for (size_t i = 0; i < c->peers.size(); ++i)
-      if (got[i] != c->peers[i].n_recv)
-        return dgvv_fail(DGVV_EINVAL, "peer %d sends %d cells but %d ghosts are listed", c->peers[i].rank, got[i], c->peers[i].n_recv);
+    c->n_interior = (int)inner.size();
+    c->n_boundary = (int)bnd.size();
+    TRY(dalloc(c, &c->d_interior, inner.size()));
+    TRY(dalloc(c, &c->d_boundary, bnd.size()));
+    DGVV_CUDA_TRY(cudaMemcpy(c->d_interior, inner.data(), inner.size() * sizeof(int), cudaMemcpyHostToDevice));
+    DGVV_CUDA_TRY(cudaMemcpy(c->d_boundary, bnd.data(), bnd.size() * sizeof(int), cudaMemcpyHostToDevice));
+  }
+  if (opt && opt->nccl_comm) {
+    TRY(nccl_load());
+    c->comm = opt->nccl_comm;
+    DGVV_CUDA_TRY(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+    DGVV_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_pack, cudaEventDisableTiming));
+    DGVV_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_comm, cudaEventDisableTiming));
+    if (!c->peers.empty()) {
+      // handshake: every peer's send count must equal the ghosts listed here
+      int* d_cnt = nullptr;
+      TRY(dalloc(c, &d_cnt, 2 * c->peers.size()));
+      std::vector<int> hs(c->peers.size());
+      for (size_t i = 0; i < c->peers.size(); ++i) hs[i] = c->peers[i].n_send;
+      DGVV_CUDA_TRY(cudaMemcpy(d_cnt, hs.data(), hs.size() * sizeof(int), cudaMemcpyHostToDevice));
+      NCCL_TRY(g_nccl.groupStart());
+      for (size_t i = 0; i < c->peers.size(); ++i) {
+        NCCL_TRY(g_nccl.send(d_cnt + i, 1, ncclInt32, c->peers[i].rank, (ncclComm_t)c->comm, s));
+        NCCL_TRY(g_nccl.recv(d_cnt + c->peers.size() + i, 1, ncclInt32, c->peers[i].rank, (ncclComm_t)c->comm, s));
+      }
+      NCCL_TRY(g_nccl.groupEnd());
+      std::vector<int> got(c->peers.size());
+      DGVV_CUDA_TRY(cudaMemcpyAsync(got.data(), d_cnt + c->peers.size(), got.size() * sizeof(int), cudaMemcpyDeviceToHost, s));
+      DGVV_CUDA_TRY(cudaStreamSynchronize(s));
+      for (size_t i = 0; i < c->peers.size(); ++i)
+        if (got[i] != c->peers[i].n_recv)
+          return dgvv_fail(DGVV_EINVAL, "peer %d sends %d cells but %d ghosts are listed", c->peers[i].rank, got[i], c->peers[i].n_recv);
+    }
   }
   // global DoF count
   c->n_global = c->n_owned;   // multi-rank: caller sums (dgvv_sizes reports local/global via comm)
@@ -712,9 +766,12 @@ dgvv_status dgvv_update_viscosity(dgvv_ctx* c, const double* u_lin, dgvv_stream 
         for (int i = 0; i < nf; ++i) I1[(size_t)j * nf + i] = v[i];
       }
       DGVV_CUDA_TRY(launch_tensor3(nf, n, 3, I1.data(), u_lin, L.ulin, 0.0, c->n_owned, s));
+      if (c->n_ghost)
+        DGVV_CUDA_TRY(launch_tensor3(nf, n, 3, I1.data(), c->L[0].ulin_ghost, L.ulin_ghost, 0.0, c->n_ghost, s));
       u = L.ulin;
+    } else if (c->n_ghost) {
+      TRY(exchange_sync(c, 0, 3, u_lin, L.ulin_ghost, s));
     }
-    if (c->n_ghost) TRY(exchange(c, (int)l, 3, u, L.ulin_ghost, s));
     NuArgs a;
     a.u = u;
     a.ughost = L.ulin_ghost;
@@ -777,11 +834,7 @@ dgvv_status dgvv_apply_linearized_viscous(dgvv_ctx* c, const double* src, double
   a.ulin = c->ulin;
   a.ulin_ghost = c->L[0].ulin_ghost;
   for (int i = 0; i < 4; ++i) a.law[i] = c->visc.p[i];
-  TRY(exchange(c, 0, 3, src, c->L[0].ghost[0], s));
-  cudaError_t e = launch_newton(c->L[0].n, c->geo, a, s);
-  if (e == cudaErrorNotSupported) return dgvv_fail(DGVV_EUNSUPPORTED, "Newton kernel not built for this degree");
-  if (e != cudaSuccess) return dgvv_fail(DGVV_ECUDA, "newton kernel: %s", cudaGetErrorString(e));
-  return DGVV_OK;
+  return run_apply(c, DGVV_OP_VISCOUS, 0, a, s, true);
 }
 
 dgvv_status dgvv_inverse_diagonal(dgvv_ctx* c, int32_t op, int32_t level, double* dst, dgvv_stream stream) {
@@ -997,6 +1050,36 @@ dgvv_status dgvv_coefficient_range(dgvv_ctx* c, int32_t op, int32_t level, doubl
   TRY(array_range(c, vf, (long)c->n_owned * 6 * n * n, s, &a2, &b2, &bad));
   *lo = std::min(a1, a2);
   *hi = std::max(b1, b2);
+  return DGVV_OK;
+}
+
+dgvv_status dgvv_ghost_layout(const dgvv_ctx* c, int32_t* n_peers, int32_t* peer_ranks, int32_t* send_counts,
+                              int32_t* recv_counts) {
+  if (!c || !n_peers) return dgvv_fail(DGVV_EINVAL, "null argument");
+  *n_peers = (int32_t)c->peers.size();
+  for (size_t i = 0; i < c->peers.size(); ++i) {
+    if (peer_ranks) peer_ranks[i] = c->peers[i].rank;
+    if (send_counts) send_counts[i] = c->peers[i].n_send;
+    if (recv_counts) recv_counts[i] = c->peers[i].n_recv;
+  }
+  return DGVV_OK;
+}
+
+dgvv_status dgvv_pack_ghosts(dgvv_ctx* c, int32_t level, int32_t kind, const double* src, double* sendbuf,
+                             dgvv_stream stream) {
+  TRY(check_level(c, level));
+  if (!src || !sendbuf) return dgvv_fail(DGVV_EINVAL, "null vector");
+  const int nc = kind == DGVV_GHOST_POISSON ? 1 : 3;
+  return pack(c, level, nc, src, sendbuf, (cudaStream_t)stream);
+}
+
+dgvv_status dgvv_ghost_buffer(dgvv_ctx* c, int32_t level, int32_t kind, double** out) {
+  TRY(check_level(c, level));
+  if (!out) return dgvv_fail(DGVV_EINVAL, "null out");
+  Level& L = c->L[level];
+  double* p = kind == DGVV_GHOST_VISCOUS ? L.ghost[0] : kind == DGVV_GHOST_POISSON ? L.ghost[1] : L.ulin_ghost;
+  if (!p) return dgvv_fail(DGVV_ESTATE, "no ghost buffer of kind %d on level %d (no ghosts or operator unused)", kind, level);
+  *out = p;
   return DGVV_OK;
 }
 

@@ -173,10 +173,40 @@ class Context:
         A.check(self._L.dgvv_dot(self.h, level, ncomp, _ptr(a, n, "a"), _ptr(b, n, "b"), C.byref(out), _stream()))
         return out.value
 
+    # ------------------------------------------------------------------ ghosts (multi-GPU)
+    def ghost_layout(self):
+        """[(peer rank, send count, recv count)] in peer order."""
+        n = C.c_int32()
+        A.check(self._L.dgvv_ghost_layout(self.h, C.byref(n), None, None, None))
+        r, sc, rc = (C.c_int32 * max(1, n.value))(), (C.c_int32 * max(1, n.value))(), (C.c_int32 * max(1, n.value))()
+        A.check(self._L.dgvv_ghost_layout(self.h, C.byref(n), r, sc, rc))
+        return [(r[i], sc[i], rc[i]) for i in range(n.value)]
+
+    def pack_ghosts(self, kind, src, sendbuf, level=0):
+        A.check(self._L.dgvv_pack_ghosts(self.h, level, kind, _ptr(src, None, "src"), _ptr(sendbuf, None, "sendbuf"),
+                                         _stream()))
+        return sendbuf
+
+    def ghost_buffer(self, kind, n_ghost, level=0):
+        """torch view (no copy) of the library-owned ghost buffer of `kind`."""
+        p = C.c_void_p()
+        A.check(self._L.dgvv_ghost_buffer(self.h, level, kind, C.byref(p)))
+        k = self.degrees[level]
+        per = (1 if kind == A.GHOST_POISSON else 3) * (k + 1) ** 3
+        return _wrap_device(p.value, n_ghost * per)
+
     def coefficient_range(self, op, level=0):
         lo, hi = C.c_double(), C.c_double()
         A.check(self._L.dgvv_coefficient_range(self.h, op, level, C.byref(lo), C.byref(hi)))
         return lo.value, hi.value
+
+
+def _wrap_device(ptr: int, n: int) -> torch.Tensor:
+    """Non-owning float64 CUDA tensor over library memory (marshalling for the ghost buffers)."""
+    class _Iface:
+        __cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False), "version": 3,
+                                    "strides": None}
+    return torch.as_tensor(_Iface(), device="cuda")
 
 
 def nccl_unique_id() -> bytes:
