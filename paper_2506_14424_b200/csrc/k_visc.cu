@@ -12,13 +12,13 @@ cudaError_t upload_tables_visc(const Tab1D* tabs) { return tu_upload_tables(tabs
 #define CPB4 8
 #endif
 #ifndef CPB5
-#define CPB5 5
+#define CPB5 1
 #endif
 #ifndef MINB4
 #define MINB4 4
 #endif
 #ifndef MINB5
-#define MINB5 3
+#define MINB5 12
 #endif
 template <int n> constexpr int cpb_visc() { return n == 2 ? 32 : n == 3 ? 14 : n == 4 ? CPB4 : n == 5 ? CPB5 : 3; }
 template <int n> constexpr int minb_visc() { return n == 2 ? 2 : n == 3 ? 3 : n == 4 ? MINB4 : n == 5 ? MINB5 : 2; }
