@@ -1,6 +1,6 @@
 // k_pois.cu — instantiations of the scalar SIPG Poisson apply (K4, with K6 epilogues).
 #include "tu_tables.cuh"
-#include "sipg_apply.cuh"
+#include "sipg_apply2.cuh"
 #include "launch.h"
 
 namespace dgvv {
@@ -15,8 +15,8 @@ template <int n> constexpr int minb_pois() { return n <= 3 ? 3 : 4; }
 template <int n, int GEO>
 static cudaError_t run(const ApplyArgs& a, cudaStream_t s) {
   constexpr int CPB = cpb_pois<n>();
-  const size_t smem = (size_t)CPB * ApplyCfg<n, 1, 1, GEO>::CS * sizeof(double);
-  auto k = sipg_apply_kernel<n, 1, 1, GEO, CPB, minb_pois<n>()>;
+  const size_t smem = (size_t)CPB * Apply2Cfg<n, 1, 1, GEO>::CS * sizeof(double);
+  auto k = sipg_apply2_kernel<n, 1, 1, GEO, CPB, minb_pois<n>()>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

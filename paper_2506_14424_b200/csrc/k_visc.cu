@@ -1,34 +1,46 @@
 // k_visc.cu — instantiations of the vector SIPG viscous apply (K1, with K6 epilogues).
 #include "tu_tables.cuh"
-#include "sipg_apply.cuh"
+#include "sipg_apply2.cuh"
 #include "launch.h"
 
 namespace dgvv {
 
 cudaError_t upload_tables_visc(const Tab1D* tabs) { return tu_upload_tables(tabs); }
 
-// cells per CTA and min resident CTAs per SM (register cap), chosen by measurement
+// cells per CTA and min resident CTAs per SM (register cap), chosen by measurement (DESIGN.md
+// §11): n = 4 general geometry (C2) 4 cells x 4 CTAs (smem-bound by the TMA face stage);
+// n = 4 Cartesian (C5) 8 x 4; n = 5 Cartesian (C3) 1 x 12.
+#ifndef CPB4G
+#define CPB4G 4
+#endif
+#ifndef MINB4G
+#define MINB4G 4
+#endif
 #ifndef CPB4
 #define CPB4 8
-#endif
-#ifndef CPB5
-#define CPB5 1
 #endif
 #ifndef MINB4
 #define MINB4 4
 #endif
+#ifndef CPB5
+#define CPB5 1
+#endif
 #ifndef MINB5
 #define MINB5 12
 #endif
-template <int n> constexpr int cpb_visc() { return n == 2 ? 32 : n == 3 ? 14 : n == 4 ? CPB4 : n == 5 ? CPB5 : 3; }
-template <int n> constexpr int minb_visc() { return n == 2 ? 2 : n == 3 ? 3 : n == 4 ? MINB4 : n == 5 ? MINB5 : 2; }
+template <int n, int GEO> constexpr int cpb_visc() {
+  return n == 2 ? 32 : n == 3 ? 14 : n == 4 ? (GEO ? CPB4G : CPB4) : n == 5 ? CPB5 : 3;
+}
+template <int n, int GEO> constexpr int minb_visc() {
+  return n == 2 ? 2 : n == 3 ? 3 : n == 4 ? (GEO ? MINB4G : MINB4) : n == 5 ? MINB5 : 2;
+}
 
 template <int n, int FORM, int GEO>
 static cudaError_t run(const ApplyArgs& a, cudaStream_t s) {
-  constexpr int CPB = cpb_visc<n>();
+  constexpr int CPB = cpb_visc<n, GEO>();
   constexpr int NC = 3;
-  const size_t smem = (size_t)CPB * ApplyCfg<n, NC, FORM, GEO>::CS * sizeof(double);
-  auto k = sipg_apply_kernel<n, NC, FORM, GEO, CPB, minb_visc<n>()>;
+  const size_t smem = (size_t)CPB * Apply2Cfg<n, NC, FORM, GEO>::CS * sizeof(double);
+  auto k = sipg_apply2_kernel<n, NC, FORM, GEO, CPB, minb_visc<n, GEO>()>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

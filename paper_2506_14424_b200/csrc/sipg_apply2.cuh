@@ -1,0 +1,644 @@
+// sipg_apply2.cuh — K1/K4/K6 v3: the hot kernel, matrix-free sum-factorised SIPG operator
+// apply (vector viscous operator, PAPER.md:1055-1111 eqn:viscous_term_weak; scalar Poisson,
+// PAPER.md:713-758 eqn:pressure_step_weak) with fused epilogues (plain apply, residual
+// b - A x, Chebyshev-Jacobi update of SURVEY §8(c) c1.6).
+//
+// Same cell-centric algorithm as v2 (team of n^2 threads per cell, thread (a,b) owns the
+// z-column x=a, y=b in registers, faces evaluated from the cell's own side, no atomics), with
+// the shared-memory traffic redesigned after the v2 ncu source profile (L1
+// wavefronts 80 % of peak, 4-way bank conflicts on the face accumulator, per-thread
+// uncoalesced neighbour x-lines as the top stall):
+//  * every volume array is kept twice, [c][z][y][x] and transposed [c][z][x][y], with rows
+//    padded to an even length RS and planes to PS (PS/2 odd): every contraction reads whole
+//    rows with 16-byte loads (broadcast across the team), and rows read by 16 different lanes
+//    are bank-conflict free;
+//  * x- and y-face contributions are written once per direction (no read-modify-write, no
+//    zeroing) into a row-major buffer and folded into the column registers by the owners;
+//  * a neighbour that sits in the same CTA (consecutive cells: the x-neighbours of structured
+//    meshes) is read from shared memory; other neighbour x-lines are read as 16-byte rows;
+//  * faces one at a time (traces + tangential coefficients of one face in shared memory), the
+//    general-geometry flux computed neighbour side first so J^-1 of both sides is never live
+//    together with both physical gradients.
+#pragma once
+#include "common.cuh"
+
+#ifndef DGVV_FACE_TMA
+#define DGVV_FACE_TMA 1   // stage the general-geometry face metric with TMA bulk copies
+#endif
+#ifndef USE_ST
+#define USE_ST 0          // keep a transposed [c][z][x][y] copy of the cell (16-byte y-lines)
+#endif
+
+namespace dgvv {
+
+template <int n>
+struct Lay {
+  static constexpr int n2 = n * n, n3 = n * n * n;
+  static constexpr int RS = (n + 1) & ~1;                          // row stride (even)
+  static constexpr int PS0 = n * RS;
+  static constexpr int PS = ((PS0 / 2) % 2 == 1) ? PS0 : PS0 + 2;  // plane stride, PS/2 odd
+  static constexpr int CST = n * PS;                               // component stride
+  static constexpr int FA = n * RS;                                // one face array [n][RS]
+};
+
+template <int n, int NC, int FORM, int GEO>
+struct Apply2Cfg {
+  using L = Lay<n>;
+  static constexpr int NT = (GEO == 1) ? NC : (FORM == 0 ? 1 : 0);
+  static constexpr int VOL = NC * L::CST;
+  static constexpr int FB = 8 * NT * L::FA;                        // [2 faces][Tm Tp G1 G2T]
+  static constexpr int RW = (2 * VOL > VOL + FB) ? 2 * VOL : VOL + FB;
+  // general geometry, n even: the face metric of one direction (own J^-1 and nu*dA of both
+  // faces, the two neighbours' of their opposite faces) is staged by TMA bulk copies
+  static constexpr bool TMA = (GEO == 1) && (n % 2 == 0) && (DGVV_FACE_TMA != 0);
+  static constexpr int STG = TMA ? 40 * L::n2 : 0;
+  static constexpr int CS = (1 + USE_ST) * VOL + RW + STG;         // doubles of smem per cell
+};
+
+// --- TMA (cp.async.bulk) + mbarrier helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* m, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* m, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* m) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(m)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* m, uint32_t parity) {
+  asm volatile("{\n .reg .pred P;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+               " @!P bra WAIT_%=;\n}" ::"r"(smem_u32(m)), "r"(parity) : "memory");
+}
+
+// row of n doubles (16-byte aligned) into registers
+template <int n>
+__device__ __forceinline__ void ld_row(const double* __restrict__ r, double (&x)[n]) {
+#pragma unroll
+  for (int k = 0; k + 1 < n; k += 2) {
+    const double2 v = *reinterpret_cast<const double2*>(r + k);
+    x[k] = v.x;
+    x[k + 1] = v.y;
+  }
+  if constexpr (n & 1) x[n - 1] = r[n - 1];
+}
+template <int n>
+__device__ __forceinline__ void ldg_row(const double* __restrict__ r, double (&x)[n]) {
+#pragma unroll
+  for (int k = 0; k + 1 < n; k += 2) {
+    const double2 v = __ldg(reinterpret_cast<const double2*>(r + k));
+    x[k] = v.x;
+    x[k + 1] = v.y;
+  }
+  if constexpr (n & 1) x[n - 1] = __ldg(r + n - 1);
+}
+template <int n>
+__device__ __forceinline__ void st_row(double* __restrict__ r, const double (&x)[n]) {
+#pragma unroll
+  for (int k = 0; k + 1 < n; k += 2) *reinterpret_cast<double2*>(r + k) = make_double2(x[k], x[k + 1]);
+  if constexpr (n & 1) r[n - 1] = x[n - 1];
+}
+template <int n>
+__device__ __forceinline__ double rowdot(const double* __restrict__ r, const double (&w)[n]) {
+  double x[n];
+  ld_row<n>(r, x);
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < n; ++k) s = fma(w[k], x[k], s);
+  return s;
+}
+
+template <int n, int NC, int FORM, int GEO, int CPB, int MINB>
+__global__ void __launch_bounds__(CPB * n * n, MINB)
+sipg_apply2_kernel(const ApplyArgs A) {
+  static_assert(FORM == 1 || NC == 3, "divergence form needs 3 components");
+  using L = Lay<n>;
+  using Cf = Apply2Cfg<n, NC, FORM, GEO>;
+  constexpr int n2 = L::n2, n3 = L::n3, RS = L::RS, PS = L::PS, CST = L::CST, FA = L::FA;
+  constexpr int NT = Cf::NT, VOL = Cf::VOL;
+  extern __shared__ __align__(16) double smem[];
+  __shared__ __align__(16) double sD[n * RS];    // sD[i][k]  = l_k'(x_i)
+  __shared__ __align__(16) double sDT[n * RS];   // sDT[i][k] = l_i'(x_k)
+  __shared__ int sid[CPB];
+  const Tab1D& T = c_tab[n];
+
+  const int lc = threadIdx.x / n2;
+  const int p = threadIdx.x - lc * n2;
+  const int a = p % n, b = p / n;
+  const int slot_raw = blockIdx.x * CPB + lc;
+  const bool active = slot_raw < A.n_proc;
+  const int slot = active ? slot_raw : (A.n_proc - 1);
+  const int cell = A.cell_list ? A.cell_list[slot] : slot;
+
+  for (int i = threadIdx.x; i < n * RS; i += blockDim.x) {
+    const int r = i / RS, k = i - r * RS;
+    sD[i] = k < n ? T.D[r * DGVV_NMAX + k] : 0.0;
+    sDT[i] = k < n ? T.D[k * DGVV_NMAX + r] : 0.0;
+  }
+  if (p == 0) sid[lc] = active ? cell : -1;
+  __shared__ __align__(8) uint64_t mbar[CPB];
+  double* stg = smem + lc * Cf::CS + (Cf::CS - Cf::STG);   // face-metric stage (TMA)
+  // issue the TMA bulk copies of direction d's face metric for this cell (thread p == 0)
+  auto stage_issue = [&](int d, const int (&nb)[6]) {
+    if constexpr (Cf::TMA) {
+      constexpr uint32_t BJ = 9 * n2 * 8, BN = n2 * 8;
+      uint32_t bytes = 2 * (BJ + BN);
+#pragma unroll
+      for (int s = 0; s < 2; ++s) bytes += nb[2 * d + s] >= 0 ? BJ + BN : 0;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(&mbar[lc], bytes);
+      tma_load_1d(stg, A.fJi + ((size_t)cell * 6 + 2 * d) * 9 * n2, 2 * BJ, &mbar[lc]);
+      tma_load_1d(stg + 18 * n2, A.nu_face + ((size_t)cell * 6 + 2 * d) * n2, 2 * BN, &mbar[lc]);
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const int nb_ = nb[2 * d + s];
+        if (nb_ >= 0) {
+          const int fo = (2 * d + s) ^ 1;
+          tma_load_1d(stg + 20 * n2 + s * 9 * n2, A.fJi + ((size_t)nb_ * 6 + fo) * 9 * n2, BJ, &mbar[lc]);
+          tma_load_1d(stg + 38 * n2 + s * n2, A.nu_face + ((size_t)nb_ * 6 + fo) * n2, BN, &mbar[lc]);
+        }
+      }
+    }
+  };
+
+  double* su = smem + lc * Cf::CS;      // values     [NC][z][y][x]
+  double* sT = su + VOL;                // transposed [NC][z][x][y] (USE_ST)
+  double* R = su + (1 + USE_ST) * VOL;  // work: W1 | W2T (volume); Y | face buffers (faces)
+
+  double ucol[NC][n], y[NC][n];
+  {
+    const double* gsrc = A.src + (size_t)cell * NC * n3;
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+#pragma unroll
+      for (int z = 0; z < n; ++z) {
+        const double v = __ldg(gsrc + c * n3 + z * n2 + p);
+        ucol[c][z] = v;
+        y[c][z] = 0.0;
+        su[c * CST + z * PS + b * RS + a] = v;
+        if (USE_ST) sT[c * CST + z * PS + a * RS + b] = v;
+      }
+  }
+  double ih[3] = {0, 0, 0}, vol = 0.0, Hm;
+  if constexpr (GEO == 0) {
+    const double* cg = A.cart + (size_t)cell * CART_STRIDE;
+    ih[0] = cg[0]; ih[1] = cg[1]; ih[2] = cg[2]; Hm = cg[3]; vol = cg[4];
+  } else {
+    Hm = A.Hcell[cell];
+  }
+  int nbf[6];
+#pragma unroll
+  for (int f = 0; f < 6; ++f) nbf[f] = __ldg(A.nbr + cell * 6 + f);
+  if constexpr (Cf::TMA) {
+    if (p == 0) {
+      mbar_init(&mbar[lc], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      stage_issue(2, nbf);      // z faces first: latency hidden by the volume term
+    }
+  }
+  __syncthreads();
+
+  // =============================================================== volume term
+  {
+    double Da[n], Db[n];
+    ld_row<n>(sD + a * RS, Da);
+    ld_row<n>(sD + b * RS, Db);
+    const double wab = T.w[a] * T.w[b];
+#pragma unroll
+    for (int z = 0; z < n; ++z) {
+      const int q = z * n2 + p;
+      double gxi[NC][3];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        gxi[c][0] = rowdot<n>(su + c * CST + z * PS + b * RS, Da);
+        if (USE_ST) {
+          gxi[c][1] = rowdot<n>(sT + c * CST + z * PS + a * RS, Db);
+        } else {
+          double sy = 0.0;
+#pragma unroll
+          for (int k = 0; k < n; ++k) sy = fma(Db[k], su[c * CST + z * PS + k * RS + a], sy);
+          gxi[c][1] = sy;
+        }
+        double sz = 0.0;
+#pragma unroll
+        for (int k = 0; k < n; ++k) sz = fma(T.D[z * DGVV_NMAX + k], ucol[c][k], sz);
+        gxi[c][2] = sz;
+      }
+      double Ji[9], w;
+      if constexpr (GEO == 0) {
+        w = A.nu_cell[(size_t)cell * n3 + q] * wab * T.w[z] * vol;
+      } else {
+        const double* vm = A.vJi + (size_t)cell * 9 * n3 + q;
+#pragma unroll
+        for (int r = 0; r < 9; ++r) Ji[r] = __ldg(vm + r * n3);
+        w = A.nu_cell[(size_t)cell * n3 + q];                  // nu * JxW
+      }
+      double G[NC][3];
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          if constexpr (GEO == 0) G[c][j] = gxi[c][j] * ih[j];
+          else G[c][j] = gxi[c][0] * Ji[j] + gxi[c][1] * Ji[3 + j] + gxi[c][2] * Ji[6 + j];
+        }
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        double Tc[3];
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          if constexpr (FORM == 0) Tc[j] = w * (G[c][j] + G[j][c]);
+          else Tc[j] = w * G[c][j];
+        }
+        double F[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          if constexpr (GEO == 0) F[k] = Tc[k] * ih[k];
+          else F[k] = Tc[0] * Ji[3 * k] + Tc[1] * Ji[3 * k + 1] + Tc[2] * Ji[3 * k + 2];
+        }
+        R[c * CST + z * PS + b * RS + a] = F[0];               // W1  [c][z][y][x]
+        R[VOL + c * CST + z * PS + a * RS + b] = F[1];         // W2T [c][z][x][y]
+#pragma unroll
+        for (int z2 = 0; z2 < n; ++z2) y[c][z2] = fma(T.D[z * DGVV_NMAX + z2], F[2], y[c][z2]);
+      }
+    }
+    __syncthreads();
+    double DTa[n], DTb[n];
+    ld_row<n>(sDT + a * RS, DTa);
+    ld_row<n>(sDT + b * RS, DTb);
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+#pragma unroll
+      for (int z = 0; z < n; ++z)
+        y[c][z] += rowdot<n>(R + c * CST + z * PS + b * RS, DTa) + rowdot<n>(R + VOL + c * CST + z * PS + a * RS, DTb);
+    __syncthreads();
+  }
+
+  // =============================================================== face terms
+  // Faces in opposite pairs (-d,+d): one pass over each normal line gives the own traces of
+  // both faces; the traces of both faces go to smem together (one barrier), then the
+  // tangential coefficients of both (second barrier).  Order z, x, y: the z pair works on the
+  // column registers (ucol dies after it).  buffers: [s][Tm | Tp | G1 | G2T][NT][FA]
+#pragma unroll
+  for (int dd = 0; dd < 3; ++dd) {
+    const int d = (dd == 0) ? 2 : dd - 1;
+    const int t1 = face_t1(d), t2 = face_t2(d);
+
+    double um[2][NC], dm[2][NC], up[2][NC], dp[2][NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      double x[n];
+      if (d == 2) {
+#pragma unroll
+        for (int i = 0; i < n; ++i) x[i] = ucol[c][i];
+      } else if (d == 0 || USE_ST) {
+        ld_row<n>((d == 0 ? su : sT) + c * CST + b * PS + a * RS, x);
+      } else {
+#pragma unroll
+        for (int i = 0; i < n; ++i) x[i] = su[c * CST + b * PS + i * RS + a];
+      }
+      double v0 = 0.0, g0 = 0.0, v1 = 0.0, g1 = 0.0;
+#pragma unroll
+      for (int i = 0; i < n; ++i) {
+        v0 = fma(T.l0[i], x[i], v0); g0 = fma(T.d0[i], x[i], g0);
+        v1 = fma(T.l1[i], x[i], v1); g1 = fma(T.d1[i], x[i], g1);
+      }
+      um[0][c] = v0; dm[0][c] = g0; um[1][c] = v1; dm[1][c] = g1;
+    }
+    // neighbour traces: from the neighbour's smem copy when it sits in this CTA, else global
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const int nbv = nbf[2 * d + s];
+      if (nbv >= 0) {
+        const double* lO = s ? T.l0 : T.l1;
+        const double* dO = s ? T.d0 : T.d1;
+        const int sl = lc + (nbv - cell);
+        const bool in_cta = sl >= 0 && sl < CPB && sid[sl] == nbv;
+        const double* pn = nbv < A.n_owned ? A.src + (size_t)nbv * NC * n3
+                                           : A.ghost + (size_t)(nbv - A.n_owned) * NC * n3;
+        const double* ns = smem + (in_cta ? sl : 0) * Cf::CS;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          double x[n];
+          if (in_cta) {
+            if (d == 2) {
+#pragma unroll
+              for (int i = 0; i < n; ++i) x[i] = ns[c * CST + i * PS + b * RS + a];
+            } else if (d == 0 || USE_ST) {
+              ld_row<n>(ns + (d == 0 ? 0 : VOL) + c * CST + b * PS + a * RS, x);
+            } else {
+#pragma unroll
+              for (int i = 0; i < n; ++i) x[i] = ns[c * CST + b * PS + i * RS + a];
+            }
+          } else {
+            if (d == 0) {
+              if constexpr ((n & 1) == 0) ldg_row<n>(pn + c * n3 + b * n2 + a * n, x);
+              else {
+#pragma unroll
+                for (int i = 0; i < n; ++i) x[i] = __ldg(pn + c * n3 + b * n2 + a * n + i);
+              }
+            } else if (d == 1) {
+#pragma unroll
+              for (int i = 0; i < n; ++i) x[i] = __ldg(pn + c * n3 + b * n2 + i * n + a);
+            } else {
+#pragma unroll
+              for (int i = 0; i < n; ++i) x[i] = __ldg(pn + c * n3 + i * n2 + p);
+            }
+          }
+          double v = 0.0, g = 0.0;
+#pragma unroll
+          for (int i = 0; i < n; ++i) { v = fma(lO[i], x[i], v); g = fma(dO[i], x[i], g); }
+          up[s][c] = v; dp[s][c] = g;
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) { up[s][c] = -um[s][c]; dp[s][c] = dm[s][c]; }
+      }
+    }
+    if constexpr (NT > 0) {
+#pragma unroll
+      for (int s = 0; s < 2; ++s)
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          const int c = (GEO == 1) ? t : d;
+          R[VOL + ((s * 4 + 0) * NT + t) * FA + b * RS + a] = um[s][c];
+          R[VOL + ((s * 4 + 1) * NT + t) * FA + b * RS + a] = up[s][c];
+        }
+      __syncthreads();
+    }
+
+    double fv[2][NC], gn[2][NC];
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const int f = 2 * d + s;
+      const int nbv = nbf[f];
+      const bool inter = nbv >= 0;
+      const bool act = inter || (nbv == NB_DIRICHLET);
+      const double* Tm = R + VOL + (s * 4 + 0) * NT * FA;
+      const double* Tp = R + VOL + (s * 4 + 1) * NT * FA;
+      // general geometry: every global load of this face issued up front (one round trip)
+      double Jim[9], Jip[9], wm = 0.0, wp = 0.0, Hp = Hm;
+      if constexpr (Cf::TMA) {
+        if (s == 0) mbar_wait(&mbar[lc], dd & 1);
+#pragma unroll
+        for (int r = 0; r < 9; ++r) Jim[r] = stg[(s * 9 + r) * n2 + p];
+        wm = stg[(18 + s) * n2 + p];
+        wp = wm;
+        if (inter) {
+#pragma unroll
+          for (int r = 0; r < 9; ++r) Jip[r] = stg[(20 + s * 9 + r) * n2 + p];
+          wp = stg[(38 + s) * n2 + p];
+          Hp = A.Hcell[nbv];
+        }
+      } else if constexpr (GEO == 1) {
+        const double* fm = A.fJi + ((size_t)cell * 6 + f) * 9 * n2 + p;
+#pragma unroll
+        for (int r = 0; r < 9; ++r) Jim[r] = __ldg(fm + r * n2);
+        wm = A.nu_face[((size_t)cell * 6 + f) * n2 + p];      // nu * dA
+        wp = wm;
+        if (inter) {
+          const double* fp = A.fJi + ((size_t)nbv * 6 + (f ^ 1)) * 9 * n2 + p;
+#pragma unroll
+          for (int r = 0; r < 9; ++r) Jip[r] = __ldg(fp + r * n2);
+          wp = A.nu_face[((size_t)nbv * 6 + (f ^ 1)) * n2 + p];
+          Hp = A.Hcell[nbv];
+        }
+      }
+      // tangential reference derivatives of the traces (NT components)
+      double tm1[NT > 0 ? NT : 1], tm2[NT > 0 ? NT : 1], tp1[NT > 0 ? NT : 1], tp2[NT > 0 ? NT : 1];
+      if constexpr (NT > 0) {
+        double Da[n], Db[n];
+        ld_row<n>(sD + a * RS, Da);
+        ld_row<n>(sD + b * RS, Db);
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          tm1[t] = rowdot<n>(Tm + t * FA + b * RS, Da);
+          double m2 = 0.0, p2 = 0.0;
+#pragma unroll
+          for (int k = 0; k < n; ++k) m2 = fma(Db[k], Tm[t * FA + k * RS + a], m2);
+          tm2[t] = m2;
+          if (inter) {
+            tp1[t] = rowdot<n>(Tp + t * FA + b * RS, Da);
+#pragma unroll
+            for (int k = 0; k < n; ++k) p2 = fma(Db[k], Tp[t * FA + k * RS + a], p2);
+            tp2[t] = p2;
+          } else {
+            tp1[t] = tm1[t];
+            tp2[t] = m2;
+          }
+        }
+      }
+
+      double gt1[NT > 0 ? NT : 1], gt2[NT > 0 ? NT : 1];
+      if constexpr (GEO == 0) {
+        // ---------------- Cartesian: n = sgn e_d, J^-1 = diag(1/h)
+        const double sgn = s ? 1.0 : -1.0;
+        const double num = A.nu_face[((size_t)cell * 6 + f) * n2 + p];
+        double nup = num, Hp = Hm;
+        double ihp[3] = {ih[0], ih[1], ih[2]};
+        if (inter) {
+          const double* cg = A.cart + (size_t)nbv * CART_STRIDE;
+          ihp[0] = cg[0]; ihp[1] = cg[1]; ihp[2] = cg[2]; Hp = cg[3];
+          nup = A.nu_face[((size_t)nbv * 6 + (f ^ 1)) * n2 + p];
+        }
+        const double dA = T.w[a] * T.w[b] * vol * ih[d];
+        const double tau = A.pen * fmax(Hm, Hp) * 0.5 * (num + nup);
+        double Sm[NC], Sp[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          const double gnm = dm[s][c] * ih[d], gnp = dp[s][c] * ihp[d];
+          if constexpr (FORM == 0) {
+            if (c == d) { Sm[c] = gnm; Sp[c] = gnp; }
+            else {
+              const bool c_is_t1 = (c == t1);
+              const double gtm = (c_is_t1 ? tm1[0] : tm2[0]) * ih[c];
+              const double gtp = (c_is_t1 ? tp1[0] : tp2[0]) * ihp[c];
+              Sm[c] = 0.5 * (gnm + gtm);
+              Sp[c] = 0.5 * (gnp + gtp);
+            }
+          } else {
+            Sm[c] = 0.5 * gnm;
+            Sp[c] = 0.5 * gnp;
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          const double jmp = um[s][c] - up[s][c];
+          const double sbn = sgn * (num * Sm[c] + nup * Sp[c]);
+          const double pv = (FORM == 0 && c == d) ? 2.0 * jmp : jmp;
+          fv[s][c] = dA * (-sbn + tau * pv);
+          const double Gcd = (FORM == 0 && c == d) ? -num * jmp * sgn : -0.5 * num * jmp * sgn;
+          gn[s][c] = dA * Gcd * ih[d];
+        }
+        if constexpr (NT > 0) {
+          gt1[0] = dA * (-0.5 * num * (um[s][t1] - up[s][t1]) * sgn) * ih[t1];
+          gt2[0] = dA * (-0.5 * num * (um[s][t2] - up[s][t2]) * sgn) * ih[t2];
+        }
+      } else {
+        // ---------------- general geometry: own / neighbour J^-1 at the face point
+        const double sgn = s ? 1.0 : -1.0;
+        double nrm[3];
+        {
+          const double v0 = Jim[3 * d], v1 = Jim[3 * d + 1], v2 = Jim[3 * d + 2];
+          const double il = sgn / sqrt(v0 * v0 + v1 * v1 + v2 * v2);
+          nrm[0] = v0 * il; nrm[1] = v1 * il; nrm[2] = v2 * il;
+        }
+        double spn[NC];
+        if (inter) {
+          // neighbour side first: sigma+ n = 1/2 (G+ + G+^T) n  (FORM 0) or 1/2 G+ n
+          double Gp[NC][3];
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            double gx[3];
+            gx[d] = dp[s][c]; gx[t1] = tp1[c]; gx[t2] = tp2[c];
+#pragma unroll
+            for (int j = 0; j < 3; ++j) Gp[c][j] = gx[0] * Jip[j] + gx[1] * Jip[3 + j] + gx[2] * Jip[6 + j];
+          }
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            double acc = 0.0;
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+              const double sp = (FORM == 0) ? 0.5 * (Gp[c][j] + Gp[j][c]) : 0.5 * Gp[c][j];
+              acc += sp * nrm[j];
+            }
+            spn[c] = acc;
+          }
+        }
+        double smn[NC];
+        {
+          double Gm[NC][3];
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            double gx[3];
+            gx[d] = dm[s][c]; gx[t1] = tm1[c]; gx[t2] = tm2[c];
+#pragma unroll
+            for (int j = 0; j < 3; ++j) Gm[c][j] = gx[0] * Jim[j] + gx[1] * Jim[3 + j] + gx[2] * Jim[6 + j];
+          }
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            double acc = 0.0;
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+              const double sm = (FORM == 0) ? 0.5 * (Gm[c][j] + Gm[j][c]) : 0.5 * Gm[c][j];
+              acc += sm * nrm[j];
+            }
+            smn[c] = acc;
+          }
+        }
+        if (!inter) {
+#pragma unroll
+          for (int c = 0; c < NC; ++c) spn[c] = smn[c];
+        }
+        const double tau = A.pen * fmax(Hm, Hp) * 0.5 * (wm + wp);
+        double jmp[NC], jn = 0.0;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) jmp[c] = um[s][c] - up[s][c];
+        if constexpr (FORM == 0) {
+#pragma unroll
+          for (int c = 0; c < NC; ++c) jn += jmp[c] * nrm[c];
+        }
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          const double pv = (FORM == 0) ? (jmp[c] + nrm[c] * jn) : jmp[c];
+          fv[s][c] = -(wm * smn[c] + wp * spn[c]) + tau * pv;
+          double Gc[3];
+#pragma unroll
+          for (int j = 0; j < 3; ++j) {
+            if constexpr (FORM == 0) Gc[j] = -wm * 0.5 * (jmp[c] * nrm[j] + jmp[j] * nrm[c]);
+            else Gc[j] = -wm * 0.5 * jmp[c] * nrm[j];
+          }
+          double gk[3];
+#pragma unroll
+          for (int k = 0; k < 3; ++k) gk[k] = Gc[0] * Jim[3 * k] + Gc[1] * Jim[3 * k + 1] + Gc[2] * Jim[3 * k + 2];
+          gn[s][c] = gk[d];
+          gt1[c] = gk[t1];
+          gt2[c] = gk[t2];
+        }
+      }
+      if (!act) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) { fv[s][c] = 0.0; gn[s][c] = 0.0; }
+        if constexpr (NT > 0) {
+#pragma unroll
+          for (int t = 0; t < NT; ++t) { gt1[t] = 0.0; gt2[t] = 0.0; }
+        }
+      }
+      if constexpr (NT > 0) {
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          R[VOL + ((s * 4 + 2) * NT + t) * FA + b * RS + a] = gt1[t];
+          R[VOL + ((s * 4 + 3) * NT + t) * FA + a * RS + b] = gt2[t];
+        }
+      }
+    }
+    // value coefficient at each face node = fv + transposed tangential contributions
+    if constexpr (NT > 0) {
+      __syncthreads();
+      if constexpr (Cf::TMA) {
+        if (dd < 2 && p == 0) stage_issue(dd == 0 ? 0 : 1, nbf);   // stage is free: next direction
+      }
+      double DTa[n], DTb[n];
+      ld_row<n>(sDT + a * RS, DTa);
+      ld_row<n>(sDT + b * RS, DTb);
+#pragma unroll
+      for (int s = 0; s < 2; ++s)
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          const int c = (GEO == 1) ? t : d;
+          fv[s][c] += rowdot<n>(R + VOL + ((s * 4 + 2) * NT + t) * FA + b * RS, DTa) +
+                      rowdot<n>(R + VOL + ((s * 4 + 3) * NT + t) * FA + a * RS, DTb);
+        }
+    }
+
+    // extrapolate both faces' coefficients along the normal line into the cell
+    if (NT == 0 && d == 1) __syncthreads();   // x-fold reads of Y are complete
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      double add[n];
+#pragma unroll
+      for (int i = 0; i < n; ++i)
+        add[i] = T.l0[i] * fv[0][c] + T.d0[i] * gn[0][c] + T.l1[i] * fv[1][c] + T.d1[i] * gn[1][c];
+      if (d == 2) {
+#pragma unroll
+        for (int i = 0; i < n; ++i) y[c][i] += add[i];
+      } else {
+        st_row<n>(R + c * CST + b * PS + a * RS, add);
+      }
+    }
+    if (d != 2) {
+      __syncthreads();
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+#pragma unroll
+        for (int z = 0; z < n; ++z)
+          y[c][z] += (d == 0) ? R[c * CST + z * PS + b * RS + a] : R[c * CST + z * PS + a * RS + b];
+    }
+  }
+
+  // =============================================================== epilogue
+  if (active) {
+    const size_t off = (size_t)cell * NC * n3;
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+#pragma unroll
+      for (int z = 0; z < n; ++z) {
+        const size_t i = off + c * n3 + z * n2 + p;
+        if (A.mode == MODE_APPLY) {
+          A.dst[i] = y[c][z];
+        } else if (A.mode == MODE_RESID) {
+          A.dst[i] = __ldg(A.b + i) - y[c][z];
+        } else {
+          const double r = __ldg(A.b + i) - y[c][z];
+          double dn = A.c_r * __ldg(A.dinv + i) * r;
+          if (A.c_rho != 0.0) dn += A.c_rho * A.dvec[i];
+          A.dvec[i] = dn;
+          A.xout[i] = su[c * CST + z * PS + b * RS + a] + dn;
+        }
+      }
+  }
+}
+
+}  // namespace dgvv

@@ -1,0 +1,178 @@
+#!/usr/bin/env python
+"""Per-operation B200 timings for every SURVEY §8(a) row on the BASELINE configs (C2-C5).
+
+    python scripts/bench_ops.py [--configs 2,3,4,5] [--reps 5] > profiles/rNN_ops.json
+
+One JSON object per (config, op): median over `reps` loops of N calls (SURVEY §8(d) protocol:
+3 warm-up calls, CUDA events on the launching stream), ms per call, DoFs/s, and the
+algorithmic-byte / algorithmic-flop fractions of the measured peaks (HBM from
+MEASURED_PEAKS.json, FP64 from scripts/fp64_peak.cu, 34.2 TFLOP/s).  Inputs are the seeded
+synthetic inputs of DESIGN.md §4.  Not a bench.py line: the driver's metric is bench.py's.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from inputs import bfs, cube, deformed_cube, uniform  # noqa: E402
+from inputs.vectors import c3_linearization, c5_linearization  # noqa: E402
+from paper_2506_14424_b200 import _abi as A  # noqa: E402
+from paper_2506_14424_b200.dgvv import Context  # noqa: E402
+
+FP64_MEASURED = 34.2e12
+C2_LAW = {"kind": "exp", "rate": np.log(100.0) / 3.0}
+C4_LAW = {"kind": "exp", "rate": -np.log(1.0e4) / 3.0}
+C3_LAW = {"kind": "carreau", "eta0": 1.0, "eta_inf": 1.0e-3, "lam": 1.0, "n": 0.5}
+C5_LAW = {"kind": "carreau", "eta0": 1.0, "eta_inf": 1.0e-4, "lam": 10.0, "n": 0.5}
+
+
+def hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    return json.load(open(p))["hbm_gbs"] * 1e9 if os.path.exists(p) else 6.65e12
+
+
+def timeit(fn, n_calls, reps):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    s = torch.cuda.current_stream()
+    ts = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for _ in range(n_calls):
+            fn()
+        e1.record(s)
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1) / n_calls)
+    return statistics.median(ts)
+
+
+def report(cfg, op, ms, dofs, bytes_=None, flops=None, note=""):
+    d = {"config": cfg, "op": op, "ms": round(ms, 5), "dofs": dofs, "gdofs_per_s": round(dofs / ms / 1e6, 3)}
+    if bytes_ is not None:
+        d["alg_bytes"] = bytes_
+        d["hbm_frac"] = round(bytes_ / (ms * 1e-3) / hbm_peak(), 4)
+    if flops is not None:
+        d["alg_flops"] = flops
+        d["fp64_frac_measured"] = round(flops / (ms * 1e-3) / FP64_MEASURED, 4)
+    if note:
+        d["note"] = note
+    print(json.dumps(d), flush=True)
+
+
+def visc_bytes(cells, n, general):
+    b = 8 * 2 * 3 * n ** 3 + 24
+    b += 8 * (10 * n ** 3 + 60 * n * n + 1) if general else 8 * (n ** 3 + 6 * n * n + 8)
+    return b * cells
+
+
+def visc_flops(dofs, n, general):
+    return dofs * ((12 * n + 96 + 40 + 315 / n) if general else (12 * n + 96 + 10 + 135 / n))
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def run_c2(reps):
+    m = deformed_cube(32, 3)
+    ctx = Context(m, 3, visc_law=C2_LAW)
+    N = ctx.n_dofs() * 3
+    src = [dev(uniform(100 + i, N)) for i in range(4)]
+    dst = [torch.empty_like(src[0]) for _ in range(4)]
+    it = iter(range(10 ** 9))
+    ms = timeit(lambda: ctx.apply_viscous(src[next(it) % 4], dst[0]), 100, reps)
+    report("C2", "apply_viscous", ms, N, visc_bytes(m.n_cells, 4, True), visc_flops(N, 4, True))
+
+
+def run_c3(reps):
+    m = cube(64)
+    ctx = Context(m, 4, visc_law=C3_LAW)
+    N = ctx.n_dofs() * 3
+    ulin = dev(c3_linearization(m, 4))
+    ms = timeit(lambda: ctx.update_viscosity(ulin), 10, reps)
+    cells = m.n_cells
+    report("C3", "update_viscosity", ms, N, 8 * cells * (3 * 125 + 125 + 6 * 25), None,
+           "K3 Carreau nu at cell + own face points")
+    src = dev(uniform(0, N))
+    dst = torch.empty_like(src)
+    ms = timeit(lambda: ctx.apply_viscous(src, dst), 20, reps)
+    report("C3", "apply_viscous", ms, N, visc_bytes(cells, 5, False), visc_flops(N, 5, False))
+    ms = timeit(lambda: ctx.apply_linearized_viscous(src, dst), 20, reps)
+    report("C3", "apply_linearized_viscous", ms, N, 8 * 3 * N + 8 * 8 * cells, 360.0 * N)
+
+
+def run_c4(reps):
+    m = cube(64)
+    degs = [5, 3, 2, 1]
+    ctx = Context(m, 5, poisson_law=C4_LAW, degrees=degs)
+    N = ctx.n_dofs(0)
+    n = 6
+    b = dev(uniform(0, N))
+    x = torch.empty_like(b)
+    cells = m.n_cells
+    pb = 8 * cells * (2 * n ** 3 + n ** 3 + 6 * n * n + 8) + 24 * cells
+    ms = timeit(lambda: ctx.apply_poisson(b, x), 20, reps)
+    report("C4", "apply_poisson_k5", ms, N, pb, N * (12 * n + 96 + 10 + 120 / n))
+    dinv = torch.empty_like(b)
+    ctx.inverse_diagonal(A.OP_POISSON, dinv)
+    ms = timeit(lambda: ctx.inverse_diagonal(A.OP_POISSON, dinv), 10, reps)
+    report("C4", "inverse_diagonal_k5", ms, N, 8 * cells * (2 * n ** 3 + 6 * n * n) + 24 * cells)
+    lam = []
+    for lvl in range(len(degs)):
+        v0 = dev(uniform(2, ctx.n_dofs(lvl)))
+        lam.append(1.2 * ctx.estimate_lambda_max(A.OP_POISSON, v0, level=lvl, steps=20))
+    work = torch.empty(2 * N, dtype=torch.float64, device="cuda")
+    ms = timeit(lambda: ctx.chebyshev_smooth(A.OP_POISSON, x, b, lam[0] / 20, lam[0], 5, True, work), 10, reps)
+    report("C4", "chebyshev5_from_zero_k5", ms, N, 4 * pb + 8 * N * (2 + 6 * 4), None,
+           "4 applies with fused Chebyshev epilogue (x0 = 0)")
+    x0 = dev(uniform(3, N))
+    xs = x0.clone()
+    ms = timeit(lambda: (xs.copy_(x0), ctx.chebyshev_smooth(A.OP_POISSON, xs, b, lam[0] / 20, lam[0], 5, False, work)),
+                10, reps)
+    report("C4", "chebyshev5_from_x0_k5", ms, N, 5 * pb + 8 * N * (2 + 6 * 5), None, "includes one vector copy")
+    ms = timeit(lambda: ctx.vcycle(A.OP_POISSON, b, x, lam), 10, reps)
+    report("C4", "vcycle_5_3_2_1", ms, N, None, None, "fine-level DoFs per V-cycle second")
+    c = torch.empty(ctx.n_dofs(1), dtype=torch.float64, device="cuda")
+    ms = timeit(lambda: ctx.restrict(A.OP_POISSON, 0, b, c), 20, reps)
+    report("C4", "restrict_5_to_3", ms, N, 8 * cells * (216 + 64))
+    ms = timeit(lambda: ctx.prolongate(A.OP_POISSON, 0, c, x, 1.0), 20, reps)
+    report("C4", "prolongate_add_3_to_5", ms, N, 8 * cells * (64 + 2 * 216))
+
+
+def run_c5(reps):
+    m = bfs()
+    ctx = Context(m, 3, visc_law=C5_LAW)
+    N = ctx.n_dofs() * 3
+    ulin = dev(c5_linearization(m, 3))
+    ms = timeit(lambda: ctx.update_viscosity(ulin), 5, reps)
+    report("C5", "update_viscosity", ms, N, 8 * m.n_cells * (3 * 64 + 64 + 6 * 16))
+    src = dev(uniform(0, N))
+    dst = torch.empty_like(src)
+    ms = timeit(lambda: ctx.apply_viscous(src, dst), 20, reps)
+    report("C5", "apply_viscous", ms, N, visc_bytes(m.n_cells, 4, False), visc_flops(N, 4, False))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="2,3,4,5")
+    ap.add_argument("--reps", type=int, default=5)
+    a = ap.parse_args()
+    torch.cuda.set_device(0)
+    for c in a.configs.split(","):
+        {"2": run_c2, "3": run_c3, "4": run_c4, "5": run_c5}[c](a.reps)
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
