@@ -1,6 +1,7 @@
 // k_newton.cu — instantiations of the Newton-linearised viscous apply (K2).
 #include "tu_tables.cuh"
 #include "newton_apply.cuh"
+#include "newton_apply2.cuh"
 #include "launch.h"
 
 namespace dgvv {
@@ -9,8 +10,35 @@ cudaError_t upload_tables_newton(const Tab1D* tabs) { return tu_upload_tables(ta
 
 template <int n> constexpr int cpb_newton() { return n == 2 ? 16 : n == 3 ? 8 : n == 4 ? 4 : n == 5 ? 3 : 2; }
 
+#ifndef NCPB5
+#define NCPB5 1
+#endif
+#ifndef NMINB5
+#define NMINB5 8
+#endif
+// Cartesian cells: newton_apply2_kernel (no power evaluations, merged stresses)
+template <int n> constexpr int cpb_newton2() { return n == 2 ? 16 : n == 3 ? 6 : n == 4 ? 2 : n == 5 ? NCPB5 : 1; }
+template <int n> constexpr int minb_newton2() { return n == 5 ? NMINB5 : n == 4 ? 4 : 2; }
+
+template <int n>
+static cudaError_t run2(const ApplyArgs& a, cudaStream_t s) {
+  constexpr int CPB = cpb_newton2<n>();
+  const size_t smem = (size_t)CPB * Newton2Cfg<n>::CS * sizeof(double);
+  auto k = newton_apply2_kernel<n, CPB, minb_newton2<n>()>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  if (a.n_proc <= 0) return cudaSuccess;
+  k<<<(a.n_proc + CPB - 1) / CPB, CPB * n * n, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
 template <int n, int GEO>
 static cudaError_t run(const ApplyArgs& a, cudaStream_t s) {
+  if constexpr (GEO == 0) return run2<n>(a, s);
   constexpr int CPB = cpb_newton<n>();
   const size_t smem = (size_t)CPB * NewtonCfg<n, GEO>::CS * sizeof(double);
   auto k = newton_apply_kernel<n, GEO, CPB, 1>;
