@@ -115,6 +115,18 @@ dgvv_status dgvv_update_viscosity(dgvv_ctx* ctx, const double* u_lin, dgvv_strea
 dgvv_status dgvv_apply_viscous(dgvv_ctx* ctx, int32_t level, const double* src, double* dst,
                                dgvv_stream stream);
 
+/* End-to-end variant of dgvv_apply_viscous with HOST buffers (src_host, dst_host: n_local
+ * doubles, canonical layout; page-locked memory gives overlapped copies, pageable memory is
+ * accepted but the copies then serialise).  The library stages them through its own device
+ * vectors: on one GPU the owned cells are split into contiguous slabs; slab i is copied in on
+ * a copy stream, applied on `stream` as soon as every slab holding one of its neighbours has
+ * arrived, and copied out on a second copy stream, so host->device, compute and device->host
+ * overlap (PCIe is full duplex).  With ghosts (multi-GPU) the whole vector is copied in, the
+ * normal exchange + apply runs, and the result is copied out.  Asynchronous on `stream`: the
+ * host buffers must stay valid (and src unchanged) until `stream` reaches this point. */
+dgvv_status dgvv_apply_viscous_host(dgvv_ctx* ctx, int32_t level, const double* src_host,
+                                    double* dst_host, dgvv_stream stream);
+
 /* dst = J(u_lin) src = A(nu0) src + A(delta nu[src]) u_lin on level 0 (Newton derivative,
  * reading G10; delta nu = 2 eta'(gd)/gd eps(u_lin):eps(src) at every point, both sides).
  * DGVV_ESTATE before dgvv_update_viscosity; DGVV_EUNSUPPORTED for analytic laws. */

@@ -52,6 +52,7 @@ _SIGS = {
     "dgvv_setup": [C.POINTER(DgvvMesh), I32, C.POINTER(DgvvLaw), C.POINTER(DgvvLaw), C.POINTER(DgvvOptions), VP, C.POINTER(VP)],
     "dgvv_update_viscosity": [VP, VP, VP],
     "dgvv_apply_viscous": [VP, I32, VP, VP, VP],
+    "dgvv_apply_viscous_host": [VP, I32, VP, VP, VP],
     "dgvv_apply_linearized_viscous": [VP, VP, VP, VP],
     "dgvv_apply_poisson": [VP, I32, VP, VP, VP],
     "dgvv_inverse_diagonal": [VP, I32, I32, VP, VP],

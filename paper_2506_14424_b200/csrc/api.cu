@@ -5,6 +5,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -164,6 +165,17 @@ struct dgvv_ctx {
   double* d_scal = nullptr;     // 16 scalars
   int* d_flag = nullptr;
   std::vector<void*> allocs;
+  // host-buffer pipelined apply (dgvv_apply_viscous_host)
+  std::vector<int> h_nbr;           // local neighbour table [n_total][6] (host copy)
+  struct HostPipe {
+    int level = -1, nslab = 0;
+    double* d_src = nullptr;
+    double* d_dst = nullptr;
+    std::vector<int> first, count, need;
+    cudaStream_t cs[2] = {nullptr, nullptr};
+    std::vector<cudaEvent_t> ev_in, ev_out;
+    cudaEvent_t ev_start = nullptr, ev_done = nullptr;
+  } hp;
 };
 
 namespace {
@@ -449,6 +461,12 @@ void dgvv_destroy(dgvv_ctx* c) {
   for (auto& L : c->L)
     for (int o = 0; o < 2; ++o) L.scratch[o].clear();
   for (void* p : c->allocs) cudaFree(p);
+  for (cudaEvent_t e : c->hp.ev_in) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->hp.ev_out) cudaEventDestroy(e);
+  if (c->hp.ev_start) cudaEventDestroy(c->hp.ev_start);
+  if (c->hp.ev_done) cudaEventDestroy(c->hp.ev_done);
+  for (int i = 0; i < 2; ++i)
+    if (c->hp.cs[i]) cudaStreamDestroy(c->hp.cs[i]);
   if (c->ev_pack) cudaEventDestroy(c->ev_pack);
   if (c->ev_comm) cudaEventDestroy(c->ev_comm);
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
@@ -562,7 +580,8 @@ static dgvv_status setup_impl(const dgvv_mesh* m, int32_t degree, const dgvv_law
   TRY(dalloc(c, &c->d_scal, 16));
   TRY(dalloc(c, &c->d_flag, 4));
   TRY(dalloc(c, &c->d_nbr, nbr.size()));
-  DGVV_CUDA_TRY(cudaMemcpyAsync(c->d_nbr, nbr.data(), nbr.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+  c->h_nbr = nbr;
+  DGVV_CUDA_TRY(cudaMemcpyAsync(c->d_nbr, c->h_nbr.data(), nbr.size() * sizeof(int), cudaMemcpyHostToDevice, s));
   TRY(dalloc(c, &c->d_nodes, nodes.size()));
   DGVV_CUDA_TRY(cudaMemcpyAsync(c->d_nodes, nodes.data(), nodes.size() * sizeof(double), cudaMemcpyHostToDevice, s));
   if (c->geo == 0) {
@@ -808,6 +827,104 @@ dgvv_status dgvv_apply_viscous(dgvv_ctx* c, int32_t level, const double* src, do
   a.src = src;
   a.dst = dst;
   return run_apply(c, DGVV_OP_VISCOUS, level, a, (cudaStream_t)stream);
+}
+
+// Host-buffer apply: slab pipeline H2D (copy stream 0) -> apply (caller stream) -> D2H (copy
+// stream 1).  Slab i is applied once every slab holding one of its neighbours has arrived.
+static dgvv_status host_pipe_setup(dgvv_ctx* c, int level) {
+  auto& P = c->hp;
+  const size_t N = (size_t)3 * level_dofs(c, level);
+  if (P.level == level) return DGVV_OK;
+  if (P.level >= 0) return dgvv_fail(DGVV_EUNSUPPORTED, "host apply is set up for level %d only", P.level);
+  TRY(dalloc(c, &P.d_src, N));
+  TRY(dalloc(c, &P.d_dst, N));
+  for (int i = 0; i < 2; ++i) DGVV_CUDA_TRY(cudaStreamCreateWithFlags(&P.cs[i], cudaStreamNonBlocking));
+  DGVV_CUDA_TRY(cudaEventCreateWithFlags(&P.ev_start, cudaEventDisableTiming));
+  DGVV_CUDA_TRY(cudaEventCreateWithFlags(&P.ev_done, cudaEventDisableTiming));
+  const int n = c->n_owned;
+  // slab sizes: small first/last slabs shorten the pipeline fill (compute of slab 0 waits for
+  // its neighbours' slab) and drain (copy-out of the last slab); large middle slabs keep the
+  // per-slab launch/event overhead low.  Weights 1 1 6 6 6 6 6 6 1 1 (DGVV_HOST_SLABS = uniform k).
+  std::vector<int> wts = {1, 1, 6, 6, 6, 6, 6, 6, 1, 1};
+  if (const char* e = std::getenv("DGVV_HOST_SLABS")) wts.assign(std::max(1, std::atoi(e)), 1);
+  if (n < 64 * (int)wts.size()) wts.assign(1, 1);
+  P.nslab = (int)wts.size();
+  long long wsum = 0, acc = 0;
+  for (int w : wts) wsum += w;
+  std::vector<int> slab_of(n);
+  for (int i = 0; i < P.nslab; ++i) {
+    const int a = (int)((long long)n * acc / wsum);
+    acc += wts[i];
+    const int b = (int)((long long)n * acc / wsum);
+    P.first.push_back(a);
+    P.count.push_back(b - a);
+    for (int k = a; k < b; ++k) slab_of[k] = i;
+  }
+  P.need.assign(P.nslab, 0);
+  for (int k = 0; k < n; ++k) {
+    int nd = slab_of[k];
+    for (int f = 0; f < 6; ++f) {
+      const int v = c->h_nbr[(size_t)k * 6 + f];
+      if (v >= 0 && v < n) nd = std::max(nd, slab_of[v]);
+    }
+    P.need[slab_of[k]] = std::max(P.need[slab_of[k]], nd);
+  }
+  P.ev_in.resize(P.nslab);
+  P.ev_out.resize(P.nslab);
+  for (int i = 0; i < P.nslab; ++i) {
+    DGVV_CUDA_TRY(cudaEventCreateWithFlags(&P.ev_in[i], cudaEventDisableTiming));
+    DGVV_CUDA_TRY(cudaEventCreateWithFlags(&P.ev_out[i], cudaEventDisableTiming));
+  }
+  P.level = level;
+  return DGVV_OK;
+}
+
+dgvv_status dgvv_apply_viscous_host(dgvv_ctx* c, int32_t level, const double* src_host, double* dst_host,
+                                    dgvv_stream stream) {
+  TRY(check_level(c, level));
+  TRY(op_ready(c, DGVV_OP_VISCOUS));
+  if (!src_host || !dst_host) return dgvv_fail(DGVV_EINVAL, "null vector");
+  if (src_host == dst_host) return dgvv_fail(DGVV_EINVAL, "src and dst alias");
+  TRY(host_pipe_setup(c, level));
+  auto& P = c->hp;
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t per = (size_t)3 * level_dofs(c, level) / std::max(1, c->n_owned);   // doubles per cell
+  if (!c->peers.empty()) {   // ghosts: whole vector in, exchange + apply, whole vector out
+    const size_t N = per * c->n_owned;
+    DGVV_CUDA_TRY(cudaMemcpyAsync(P.d_src, src_host, N * sizeof(double), cudaMemcpyHostToDevice, s));
+    TRY(dgvv_apply_viscous(c, level, P.d_src, P.d_dst, stream));
+    DGVV_CUDA_TRY(cudaMemcpyAsync(dst_host, P.d_dst, N * sizeof(double), cudaMemcpyDeviceToHost, s));
+    return DGVV_OK;
+  }
+  // the copy streams start after everything already queued on the caller's stream
+  DGVV_CUDA_TRY(cudaEventRecord(P.ev_start, s));
+  for (int i = 0; i < 2; ++i) DGVV_CUDA_TRY(cudaStreamWaitEvent(P.cs[i], P.ev_start, 0));
+  for (int i = 0; i < P.nslab; ++i) {
+    DGVV_CUDA_TRY(cudaMemcpyAsync(P.d_src + per * P.first[i], src_host + per * P.first[i],
+                                  per * P.count[i] * sizeof(double), cudaMemcpyHostToDevice, P.cs[0]));
+    DGVV_CUDA_TRY(cudaEventRecord(P.ev_in[i], P.cs[0]));
+  }
+  ApplyArgs a = base_args(c, level, DGVV_OP_VISCOUS);
+  a.src = P.d_src;
+  a.dst = P.d_dst;
+  int waited = -1;
+  for (int i = 0; i < P.nslab; ++i) {
+    if (P.need[i] > waited) {
+      DGVV_CUDA_TRY(cudaStreamWaitEvent(s, P.ev_in[P.need[i]], 0));
+      waited = P.need[i];
+    }
+    a.cell_base = P.first[i];
+    a.n_proc = P.count[i];
+    cudaError_t e = launch_apply(3, c->L[level].n, c->form, c->geo, a, s);
+    if (e != cudaSuccess) return dgvv_fail(DGVV_ECUDA, "apply kernel: %s", cudaGetErrorString(e));
+    DGVV_CUDA_TRY(cudaEventRecord(P.ev_out[i], s));
+    DGVV_CUDA_TRY(cudaStreamWaitEvent(P.cs[1], P.ev_out[i], 0));
+    DGVV_CUDA_TRY(cudaMemcpyAsync(dst_host + per * P.first[i], P.d_dst + per * P.first[i],
+                                  per * P.count[i] * sizeof(double), cudaMemcpyDeviceToHost, P.cs[1]));
+  }
+  DGVV_CUDA_TRY(cudaEventRecord(P.ev_done, P.cs[1]));
+  DGVV_CUDA_TRY(cudaStreamWaitEvent(s, P.ev_done, 0));
+  return DGVV_OK;
 }
 
 dgvv_status dgvv_apply_poisson(dgvv_ctx* c, int32_t level, const double* src, double* dst, dgvv_stream stream) {

@@ -43,8 +43,9 @@ struct ApplyArgs {
   const double* ghost;      // ghost cells [n_ghost][NC][n^3] (may be null)
   double* dst;
   const int* nbr;           // [n_total][6]
-  const int* cell_list;     // cells to process (null: 0..n_proc-1)
+  const int* cell_list;     // cells to process (null: cell_base .. cell_base+n_proc-1)
   int n_proc;
+  int cell_base;
   int n_owned;
   // coefficient at quadrature points.  Cartesian: nu itself; general geometry:
   // premultiplied weights nu*JxW (cells) and nu*dA (own face points).

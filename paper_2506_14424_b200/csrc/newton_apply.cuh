@@ -34,7 +34,7 @@ __global__ void __launch_bounds__(CPB * n * n, MINB) newton_apply_kernel(const A
   const int slot_raw = blockIdx.x * CPB + lc;
   const bool active = slot_raw < A.n_proc;
   const int slot = active ? slot_raw : (A.n_proc - 1);
-  const int cell = A.cell_list ? A.cell_list[slot] : slot;
+  const int cell = A.cell_list ? A.cell_list[slot] : A.cell_base + slot;
 
   double* sw = smem + lc * Cf::CS;      // w  [3][n3]
   double* s0 = sw + 3 * n3;             // u0 [3][n3]

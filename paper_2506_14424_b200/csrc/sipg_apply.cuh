@@ -94,7 +94,7 @@ sipg_apply_kernel(const ApplyArgs A) {
   const int slot_raw = blockIdx.x * CPB + lc;
   const bool active = slot_raw < A.n_proc;
   const int slot = active ? slot_raw : (A.n_proc - 1);
-  const int cell = A.cell_list ? A.cell_list[slot] : slot;
+  const int cell = A.cell_list ? A.cell_list[slot] : A.cell_base + slot;
 
   double* su = smem + lc * Cf::CS;      // own cell values [NC][n3]
   double* W = su + NC * n3;             // work region

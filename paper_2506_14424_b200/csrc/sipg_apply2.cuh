@@ -131,7 +131,7 @@ sipg_apply2_kernel(const ApplyArgs A) {
   const int slot_raw = blockIdx.x * CPB + lc;
   const bool active = slot_raw < A.n_proc;
   const int slot = active ? slot_raw : (A.n_proc - 1);
-  const int cell = A.cell_list ? A.cell_list[slot] : slot;
+  const int cell = A.cell_list ? A.cell_list[slot] : A.cell_base + slot;
 
   for (int i = threadIdx.x; i < n * RS; i += blockDim.x) {
     const int r = i / RS, k = i - r * RS;

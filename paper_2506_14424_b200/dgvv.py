@@ -123,6 +123,17 @@ class Context:
         A.check(self._L.dgvv_apply_viscous(self.h, level, _ptr(src, n, "src"), _ptr(dst, n, "dst"), _stream()))
         return dst
 
+    def apply_viscous_host(self, src_host, dst_host, level=0):
+        """dst_host = A_visc src_host with host (CPU, preferably pinned) tensors; the copies are
+        pipelined with the apply inside the library (dgvv_apply_viscous_host)."""
+        n = self._n(A.OP_VISCOUS, level)
+        for t, nm in ((src_host, "src_host"), (dst_host, "dst_host")):
+            if t.device.type != "cpu" or t.dtype != torch.float64 or not t.is_contiguous() or t.numel() != n:
+                raise ValueError(f"{nm}: contiguous float64 CPU tensor of {n} entries required")
+        A.check(self._L.dgvv_apply_viscous_host(self.h, level, C.c_void_p(src_host.data_ptr()),
+                                                C.c_void_p(dst_host.data_ptr()), _stream()))
+        return dst_host
+
     def apply_linearized_viscous(self, src, dst):
         n = self._n(A.OP_VISCOUS, 0)
         A.check(self._L.dgvv_apply_linearized_viscous(self.h, _ptr(src, n, "src"), _ptr(dst, n, "dst"), _stream()))
