@@ -9,7 +9,7 @@ cudaError_t upload_tables_visc(const Tab1D* tabs) { return tu_upload_tables(tabs
 
 // cells per CTA and min resident CTAs per SM (register cap), chosen by measurement (DESIGN.md
 // §11): n = 4 general geometry (C2) 4 cells x 4 CTAs (smem-bound by the TMA face stage);
-// n = 4 Cartesian (C5) 8 x 4; n = 5 Cartesian (C3) 1 x 12.
+// n = 4 Cartesian (C5) 8 x 4; n = 5 Cartesian (C3) 5 x 3 (125 threads: 98 % lane use).
 #ifndef CPB4G
 #define CPB4G 4
 #endif
@@ -23,10 +23,10 @@ cudaError_t upload_tables_visc(const Tab1D* tabs) { return tu_upload_tables(tabs
 #define MINB4 4
 #endif
 #ifndef CPB5
-#define CPB5 1
+#define CPB5 5
 #endif
 #ifndef MINB5
-#define MINB5 12
+#define MINB5 3
 #endif
 template <int n, int GEO> constexpr int cpb_visc() {
   return n == 2 ? 32 : n == 3 ? 14 : n == 4 ? (GEO ? CPB4G : CPB4) : n == 5 ? CPB5 : 3;
