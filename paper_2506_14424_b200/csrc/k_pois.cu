@@ -9,8 +9,20 @@ cudaError_t launch_apply_visc(int n, int form, int geo, const ApplyArgs& a, cuda
 
 cudaError_t upload_tables_pois(const Tab1D* tabs) { return tu_upload_tables(tabs); }
 
-template <int n> constexpr int cpb_pois() { return n == 2 ? 32 : n == 3 ? 14 : n == 4 ? 8 : n == 5 ? 5 : n == 6 ? 4 : 3; }
-template <int n> constexpr int minb_pois() { return n <= 3 ? 3 : 4; }
+#ifndef PCPB6
+#define PCPB6 6
+#endif
+#ifndef PMINB6
+#define PMINB6 4
+#endif
+#ifndef PCPB4
+#define PCPB4 8
+#endif
+#ifndef PCPB3
+#define PCPB3 14
+#endif
+template <int n> constexpr int cpb_pois() { return n == 2 ? 32 : n == 3 ? PCPB3 : n == 4 ? PCPB4 : n == 5 ? 5 : n == 6 ? PCPB6 : 3; }
+template <int n> constexpr int minb_pois() { return n <= 3 ? 3 : n == 6 ? PMINB6 : 4; }
 
 template <int n, int GEO>
 static cudaError_t run(const ApplyArgs& a, cudaStream_t s) {

@@ -478,56 +478,43 @@ sipg_apply2_kernel(const ApplyArgs A) {
         }
       } else {
         // ---------------- general geometry: own / neighbour J^-1 at the face point
+        // With v = J^-1 n (v_k = sum_j Ji[k][j] n_j) the physical gradient G = gx J^-1 never has
+        // to be formed:  (G n)_c = gx[c].v,  (G^T n)_c = sum_k (n.gx[.][k]) Ji[k][c],  and the
+        // test-side coefficients of d v_c / d xi_k are -1/2 w (jmp_c v_k + n_c (J^-1 jmp)_k)
+        // (divergence form) or -1/2 w jmp_c v_k (Laplace form).
         const double sgn = s ? 1.0 : -1.0;
         double nrm[3];
         {
           const double v0 = Jim[3 * d], v1 = Jim[3 * d + 1], v2 = Jim[3 * d + 2];
-          const double il = sgn / sqrt(v0 * v0 + v1 * v1 + v2 * v2);
+          const double il = sgn * rsqrt(v0 * v0 + v1 * v1 + v2 * v2);
           nrm[0] = v0 * il; nrm[1] = v1 * il; nrm[2] = v2 * il;
         }
-        double spn[NC];
+        auto sigma_n = [&](const double (&Ji)[9], const double* gd, const double* g1, const double* g2,
+                           double (&v)[3], double (&out)[NC]) {
+#pragma unroll
+          for (int k = 0; k < 3; ++k) v[k] = Ji[3 * k] * nrm[0] + Ji[3 * k + 1] * nrm[1] + Ji[3 * k + 2] * nrm[2];
+          double gx[NC][3];
+#pragma unroll
+          for (int c = 0; c < NC; ++c) { gx[c][d] = gd[c]; gx[c][t1] = g1[c]; gx[c][t2] = g2[c]; }
+#pragma unroll
+          for (int c = 0; c < NC; ++c) out[c] = gx[c][0] * v[0] + gx[c][1] * v[1] + gx[c][2] * v[2];
+          if constexpr (FORM == 0) {
+            double w[3];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) w[k] = nrm[0] * gx[0][k] + nrm[1] * gx[1][k] + nrm[2] * gx[2][k];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) out[c] = 0.5 * (out[c] + w[0] * Ji[c] + w[1] * Ji[3 + c] + w[2] * Ji[6 + c]);
+          } else {
+#pragma unroll
+            for (int c = 0; c < NC; ++c) out[c] *= 0.5;
+          }
+        };
+        double spn[NC], smn[NC], vm[3];
         if (inter) {
-          // neighbour side first: sigma+ n = 1/2 (G+ + G+^T) n  (FORM 0) or 1/2 G+ n
-          double Gp[NC][3];
-#pragma unroll
-          for (int c = 0; c < NC; ++c) {
-            double gx[3];
-            gx[d] = dp[s][c]; gx[t1] = tp1[c]; gx[t2] = tp2[c];
-#pragma unroll
-            for (int j = 0; j < 3; ++j) Gp[c][j] = gx[0] * Jip[j] + gx[1] * Jip[3 + j] + gx[2] * Jip[6 + j];
-          }
-#pragma unroll
-          for (int c = 0; c < NC; ++c) {
-            double acc = 0.0;
-#pragma unroll
-            for (int j = 0; j < 3; ++j) {
-              const double sp = (FORM == 0) ? 0.5 * (Gp[c][j] + Gp[j][c]) : 0.5 * Gp[c][j];
-              acc += sp * nrm[j];
-            }
-            spn[c] = acc;
-          }
+          double vp[3];
+          sigma_n(Jip, dp[s], tp1, tp2, vp, spn);
         }
-        double smn[NC];
-        {
-          double Gm[NC][3];
-#pragma unroll
-          for (int c = 0; c < NC; ++c) {
-            double gx[3];
-            gx[d] = dm[s][c]; gx[t1] = tm1[c]; gx[t2] = tm2[c];
-#pragma unroll
-            for (int j = 0; j < 3; ++j) Gm[c][j] = gx[0] * Jim[j] + gx[1] * Jim[3 + j] + gx[2] * Jim[6 + j];
-          }
-#pragma unroll
-          for (int c = 0; c < NC; ++c) {
-            double acc = 0.0;
-#pragma unroll
-            for (int j = 0; j < 3; ++j) {
-              const double sm = (FORM == 0) ? 0.5 * (Gm[c][j] + Gm[j][c]) : 0.5 * Gm[c][j];
-              acc += sm * nrm[j];
-            }
-            smn[c] = acc;
-          }
-        }
+        sigma_n(Jim, dm[s], tm1, tm2, vm, smn);
         if (!inter) {
 #pragma unroll
           for (int c = 0; c < NC; ++c) spn[c] = smn[c];
@@ -536,23 +523,21 @@ sipg_apply2_kernel(const ApplyArgs A) {
         double jmp[NC], jn = 0.0;
 #pragma unroll
         for (int c = 0; c < NC; ++c) jmp[c] = um[s][c] - up[s][c];
+        double q[3] = {0.0, 0.0, 0.0};
         if constexpr (FORM == 0) {
 #pragma unroll
           for (int c = 0; c < NC; ++c) jn += jmp[c] * nrm[c];
+#pragma unroll
+          for (int k = 0; k < 3; ++k) q[k] = Jim[3 * k] * jmp[0] + Jim[3 * k + 1] * jmp[1] + Jim[3 * k + 2] * jmp[2];
         }
+        const double hw = -0.5 * wm;
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
           const double pv = (FORM == 0) ? (jmp[c] + nrm[c] * jn) : jmp[c];
           fv[s][c] = -(wm * smn[c] + wp * spn[c]) + tau * pv;
-          double Gc[3];
-#pragma unroll
-          for (int j = 0; j < 3; ++j) {
-            if constexpr (FORM == 0) Gc[j] = -wm * 0.5 * (jmp[c] * nrm[j] + jmp[j] * nrm[c]);
-            else Gc[j] = -wm * 0.5 * jmp[c] * nrm[j];
-          }
           double gk[3];
 #pragma unroll
-          for (int k = 0; k < 3; ++k) gk[k] = Gc[0] * Jim[3 * k] + Gc[1] * Jim[3 * k + 1] + Gc[2] * Jim[3 * k + 2];
+          for (int k = 0; k < 3; ++k) gk[k] = (FORM == 0) ? hw * (jmp[c] * vm[k] + nrm[c] * q[k]) : hw * jmp[c] * vm[k];
           gn[s][c] = gk[d];
           gt1[c] = gk[t1];
           gt2[c] = gk[t2];
