@@ -333,3 +333,66 @@ def test_newton_full_size_sampled_c3():
     cells = _sample_cells(m, 32)
     ref = dg.newton_apply(d, u0, w, laws.C3_CARREAU, cells=cells)
     assert rel(y[cells], ref) < TOL
+
+
+def test_c4_full_size_sampled_poisson_and_chebyshev_step():
+    """C4 at full size (64^3, k=5, c = exp(-ln(1e4)(x+y+z)/3), 56.6M DoFs): the Poisson apply vs
+    the oracle on sampled cells; then the fused Chebyshev step (K6 epilogue, x0 != 0, m = 1) must
+    equal its unfused definition x1 = x0 + D^-1 (b - A x0)/theta built from
+    the library's own apply and diagonal — a fusion property at full size (the oracle pins A x0
+    here, D^-1 and Chebyshev on the dense oracle in the small-mesh tests above)."""
+    m = cube(64)
+    k = 5
+    d = dg.Disc(m, k)
+    n3 = (k + 1) ** 3
+    ctx = Ctx(m, k, poisson_law=laws.C4_LAW)
+    x0 = uniform(3, m.n_cells * n3)
+    b = uniform(0, m.n_cells * n3)
+    cells = _sample_cells(m, 32)
+    y = gpu_apply(ctx, x0, op="pois")
+    Ax = dg.poisson_apply(d, x0, dg.AnalyticNu(d, laws.C4_LAW), cells=cells)
+    assert rel(y.reshape(m.n_cells, n3)[cells], Ax) < TOL
+    dinv = torch.empty(m.n_cells * n3, dtype=torch.float64, device="cuda")
+    ctx.inverse_diagonal(1, dinv)
+    lo, hi = 0.05, 1.0
+    x = dev(x0)
+    ctx.chebyshev_smooth(1, x, dev(b), lo, hi, 1, x_is_zero=False)
+    theta = 0.5 * (hi + lo)
+    ref = x0 + host(dinv) * (b - y) / theta
+    assert rel(host(x), ref) < 1e-14
+
+
+def test_c4_full_size_vcycle_is_symmetric():
+    """V-cycle 5->3->2->1 at full C4 size is linear and symmetric (P11: pre- and post-Chebyshev
+    are adjoint): <V r1, r2> = <r1, V r2> and V(r1 + 2 r2) = V r1 + 2 V r2 to rounding."""
+    m = cube(64)
+    degs = [5, 3, 2, 1]
+    ctx = Ctx(m, 5, poisson_law=laws.C4_LAW, degrees=degs)
+    lams = [1.2 * ctx.estimate_lambda_max(1, dev(uniform(2, ctx.n_dofs(l))), level=l, steps=20)
+            for l in range(len(degs))]
+    n0 = ctx.n_dofs(0)
+    r1, r2 = dev(uniform(0, n0)), dev(uniform(1, n0))
+    v1, v2, v3 = (torch.zeros(n0, dtype=torch.float64, device="cuda") for _ in range(3))
+    ctx.vcycle(1, r1, v1, lams)
+    ctx.vcycle(1, r2, v2, lams)
+    ctx.vcycle(1, r1 + 2.0 * r2, v3, lams)
+    a, bb = ctx.dot(v1, r2), ctx.dot(r1, v2)
+    assert abs(a - bb) < 1e-10 * abs(a)
+    assert rel(host(v3), host(v1) + 2.0 * host(v2)) < 1e-12
+
+
+def test_c5_full_size_sampled_carreau():
+    """C5 at full size (BFS, 999,424 graded cells, k=3, Carreau contrast 1e4, periodic z,
+    Neumann outlet): GPU apply vs oracle on sampled cells (boundary and interior)."""
+    from inputs.vectors import c5_linearization
+    m = bfs()
+    k = 3
+    d = dg.Disc(m, k)
+    ulin = c5_linearization(m, k)
+    u = uniform(0, len(ulin))
+    ctx = Ctx(m, k, visc_law=laws.C5_CARREAU)
+    ctx.update_viscosity(dev(ulin))
+    y = gpu_apply(ctx, u).reshape(m.n_cells, 3, 64)
+    cells = _sample_cells(m, 48)
+    ref = dg.viscous_apply(d, u, dg.CarreauNu(d, ulin, laws.C5_CARREAU), cells=cells)
+    assert rel(y[cells], ref) < TOL
