@@ -502,3 +502,29 @@ def newton_apply(disc: Disc, u0: np.ndarray, w: np.ndarray, law: dict, cells=Non
 def carreau_residual(disc: Disc, u: np.ndarray, law: dict, cells=None) -> np.ndarray:
     """R(u) = a(., u; eta(gamma_dot(u))) — the fully nonlinear viscous term."""
     return viscous_apply(disc, u, CarreauNu(disc, u, law), cells)
+
+
+def mass_apply(disc: Disc, u: np.ndarray, ncomp: int = 3, cells=None) -> np.ndarray:
+    """y = M u, the DG mass matrix m(v, u) = sum_K int_K v . u dx by Gauss quadrature (G1):
+    y[K,c,i] = sum_q JxW_q phi_i(x_q) u_c(x_q), u_c(x_q) = sum_j u[K,c,j] phi_j(x_q).
+    This is the time-derivative term (gamma_0/dt) M u of the viscous step of the projection
+    scheme (PAPER.md:867-910, BDF; SURVEY §8(f) f1).  Written as the full-tensor definition;
+    with the collocation basis (G2) Phi is the identity, so M is diagonal — pinned, not assumed."""
+    d = disc
+    nc = d.mesh.n_cells
+    U = u.reshape(nc, ncomp, d.N)
+    full = cells is None
+    cells = np.arange(nc) if full else np.asarray(cells)
+    _, JxW, _ = d.vol_geom(cells)
+    uq = np.einsum("qj,kcj->kcq", d.Phi, U[cells])
+    y = np.einsum("qi,kq,kcq->kci", d.Phi, JxW, uq)
+    return y.reshape(-1) if full else y
+
+
+def helmholtz_apply(disc: Disc, u: np.ndarray, nu, mass: float, cells=None) -> np.ndarray:
+    """y = (mass M + A(nu)) u: the Helmholtz-type operator of the viscous step
+    (gamma_0/dt) M + A(nu)."""
+    y = viscous_apply(disc, u, nu, cells=cells)
+    if mass != 0.0:
+        y = y + mass * mass_apply(disc, u, 3, cells=cells)
+    return y

@@ -120,3 +120,36 @@ def diagonal_entries(apply_cells, n_dofs_cell, idx, ncomp=1):
         e[int(i) % per_cell] = 1.0
         out[t] = apply_cells(c, e)[int(i) % per_cell]
     return out
+
+
+def pcg(apply, b, x0, precond, rtol, maxit):
+    """Preconditioned conjugate gradients (Hestenes-Stiefel), the Krylov solver the paper uses
+    for the symmetric viscous and pressure steps:
+      r = b - A x; z = P r; p = z; rz = (r, z)
+      repeat: q = A p; alpha = rz / (p, q); x += alpha p; r -= alpha q;
+              stop when ||r|| <= rtol ||b|| (or maxit); z = P r; beta = (r, z)_new / rz; p = z + beta p
+    `precond(r)` returns P r (identity for plain CG).  Returns (x, iterations, ||r||/||b||)."""
+    x = np.array(x0, dtype=np.float64, copy=True)
+    bn = np.sqrt(b @ b)
+    r = b - apply(x)
+    rn = np.sqrt(r @ r)
+    if bn == 0.0 or rn <= rtol * bn:
+        return x, 0, (rn / bn if bn else 0.0)
+    z = precond(r)
+    p = z.copy()
+    rz = r @ z
+    it = 0
+    while it < maxit:
+        it += 1
+        q = apply(p)
+        alpha = rz / (p @ q)
+        x += alpha * p
+        r -= alpha * q
+        rn = np.sqrt(r @ r)
+        if rn <= rtol * bn:
+            break
+        z = precond(r)
+        rz_new = r @ z
+        p = z + (rz_new / rz) * p
+        rz = rz_new
+    return x, it, rn / bn
