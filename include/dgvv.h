@@ -138,6 +138,27 @@ dgvv_status dgvv_apply_linearized_viscous(dgvv_ctx* ctx, const double* src, doub
 dgvv_status dgvv_apply_poisson(dgvv_ctx* ctx, int32_t level, const double* src, double* dst,
                                dgvv_stream stream);
 
+/* Helmholtz form of the operator: every later apply, diagonal, smoother,
+ * V-cycle and CG of `op` uses  mass * M + A  with M the DG mass matrix (diagonal with the
+ * collocation basis G2: M_ii = JxW_i, per component on every level) — the
+ * (gamma_0 / dt) M + A(nu) operator of the viscous step.  mass = 0 (the
+ * default) gives the plain operator.  DGVV_EDOMAIN for mass < 0 or non-finite. */
+dgvv_status dgvv_set_mass(dgvv_ctx* ctx, int32_t op, double mass);
+
+enum { DGVV_PRECOND_NONE = 0, DGVV_PRECOND_JACOBI = 1, DGVV_PRECOND_VCYCLE = 2 };
+
+/* Preconditioned conjugate gradients on (mass M +) A_op, level 0 (the Krylov solver of the
+ * symmetric viscous and pressure steps):
+ *   r = b - A x; z = P r; p = z;  repeat q = A p, alpha = (r,z)/(p,q), x += alpha p,
+ *   r -= alpha q, stop when ||r|| <= rtol ||b||, z = P r, p = z + beta p.
+ * x is the initial guess on entry, the solution on return.  P = identity, inverse diagonal
+ * (Jacobi) or one V-cycle (dgvv_vcycle, lambda_hi_per_level required).  Synchronous (one host
+ * read per dot product); *iters and *relres = ||r||/||b|| returned.  Work vectors are owned
+ * by the library.  Multi-GPU: every rank calls collectively; dots are allreduced. */
+dgvv_status dgvv_cg_solve(dgvv_ctx* ctx, int32_t op, const double* b, double* x, double rtol,
+                          int32_t maxit, int32_t precond, const double* lambda_hi_per_level,
+                          int32_t* iters, double* relres, dgvv_stream stream);
+
 /* dst = 1 / diag(A) for op = DGVV_OP_* on `level`. */
 dgvv_status dgvv_inverse_diagonal(dgvv_ctx* ctx, int32_t op, int32_t level, double* dst,
                                   dgvv_stream stream);

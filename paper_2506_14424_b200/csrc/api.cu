@@ -148,6 +148,8 @@ struct dgvv_ctx {
   bool has_visc = false, has_pois = false, carreau = false, nu_ready = false;
   int form = 0;
   double ip = 1.0;
+  double mass[2] = {0.0, 0.0};  // Helmholtz mass coefficient per op (dgvv_set_mass)
+  double* cg_work[2] = {nullptr, nullptr};   // CG vectors r, z, p, q per op (level 0)
   const double* ulin = nullptr;
   // comm: peers exist whenever there are ghosts; NCCL transport only with a communicator
   // (without one the caller fills the ghost buffers: external-exchange mode, used by tests)
@@ -288,6 +290,7 @@ ApplyArgs base_args(dgvv_ctx* c, int l, int op) {
   a.fdA = L.fdA;
   a.Hcell = L.Hc;
   a.pen = c->ip * (double)(L.k + 1) * (double)(L.k + 1);
+  a.mass = (op == DGVV_OP_VISCOUS || op == DGVV_OP_POISSON) ? c->mass[op] : 0.0;
   a.ghost = L.ghost[op == DGVV_OP_VISCOUS ? 0 : 1];
   a.mode = MODE_APPLY;
   return a;
@@ -350,6 +353,8 @@ dgvv_status ensure_dinv(dgvv_ctx* c, int op, int l, cudaStream_t s) {
   d.fJi = L.fJi;
   d.Hcell = L.Hc;
   d.pen = c->ip * (double)(L.k + 1) * (double)(L.k + 1);
+  d.mass = c->mass[oi];
+  d.jxw = L.jxw;
   d.out = L.dinv[oi];
   const int form = op == DGVV_OP_VISCOUS ? c->form : DGVV_FORM_LAPLACE;
   cudaError_t e = launch_diag(nc, L.n, form, c->geo, d, s);
@@ -954,6 +959,21 @@ dgvv_status dgvv_apply_linearized_viscous(dgvv_ctx* c, const double* src, double
   return run_apply(c, DGVV_OP_VISCOUS, 0, a, s, true);
 }
 
+dgvv_status dgvv_set_mass(dgvv_ctx* c, int32_t op, double mass) {
+  if (!c) return dgvv_fail(DGVV_EINVAL, "null context");
+  if (op != DGVV_OP_VISCOUS && op != DGVV_OP_POISSON) return dgvv_fail(DGVV_EINVAL, "unknown op %d", op);
+  if (!std::isfinite(mass) || mass < 0.0) return dgvv_fail(DGVV_EDOMAIN, "mass coefficient %g must be finite and >= 0", mass);
+  if (c->mass[op] == mass) return DGVV_OK;
+  c->mass[op] = mass;
+  for (auto& L : c->L)                 // the diagonal changes: recompute lazily
+    if (L.dinv[op]) {
+      cudaFree(L.dinv[op]);
+      c->allocs.erase(std::remove(c->allocs.begin(), c->allocs.end(), (void*)L.dinv[op]), c->allocs.end());
+      L.dinv[op] = nullptr;
+    }
+  return DGVV_OK;
+}
+
 dgvv_status dgvv_inverse_diagonal(dgvv_ctx* c, int32_t op, int32_t level, double* dst, dgvv_stream stream) {
   TRY(check_level(c, level));
   TRY(op_ready(c, op));
@@ -1079,6 +1099,93 @@ dgvv_status dgvv_vcycle(dgvv_ctx* c, int32_t op, const double* b, double* x, con
     }
   }
   return vcycle_rec(c, op, 0, b, x, his, (cudaStream_t)stream);
+}
+
+// ------------------------------------------------------------------ f1: preconditioned CG
+static dgvv_status dot_host(dgvv_ctx* c, const double* a, const double* b, long n, double* out, cudaStream_t s) {
+  TRY(dot_dev(c, a, b, n, c->d_scal + 5, s));
+  DGVV_CUDA_TRY(cudaMemcpyAsync(out, c->d_scal + 5, sizeof(double), cudaMemcpyDeviceToHost, s));
+  DGVV_CUDA_TRY(cudaStreamSynchronize(s));
+  return DGVV_OK;
+}
+
+dgvv_status dgvv_cg_solve(dgvv_ctx* c, int32_t op, const double* b, double* x, double rtol, int32_t maxit,
+                          int32_t precond, const double* lambda_hi_per_level, int32_t* iters, double* relres,
+                          dgvv_stream stream) {
+  if (!c || !b || !x) return dgvv_fail(DGVV_EINVAL, "null argument");
+  TRY(op_ready(c, op));
+  if (b == x) return dgvv_fail(DGVV_EINVAL, "b and x alias");
+  if (!(rtol >= 0.0) || maxit < 0) return dgvv_fail(DGVV_EINVAL, "rtol >= 0 and maxit >= 0 required");
+  if (precond < DGVV_PRECOND_NONE || precond > DGVV_PRECOND_VCYCLE)
+    return dgvv_fail(DGVV_EINVAL, "unknown preconditioner %d", precond);
+  if (precond == DGVV_PRECOND_VCYCLE && !lambda_hi_per_level)
+    return dgvv_fail(DGVV_EINVAL, "V-cycle preconditioner needs lambda_hi_per_level");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int oi = op == DGVV_OP_VISCOUS ? 0 : 1;
+  const int nc = op == DGVV_OP_VISCOUS ? 3 : 1;
+  const long N = (long)nc * level_dofs(c, 0);
+  auto& W = c->cg_work[oi];
+  if (!W) TRY(dalloc(c, &W, (size_t)4 * N));
+  double *r = W, *z = W + N, *pv = W + 2 * N, *q = W + 3 * N;
+  if (precond == DGVV_PRECOND_JACOBI) TRY(ensure_dinv(c, op, 0, s));
+  if (precond == DGVV_PRECOND_VCYCLE) {      // scratch of every level (as dgvv_vcycle)
+    for (size_t l = 0; l < c->L.size(); ++l) {
+      auto& S = c->L[l].scratch[oi];
+      if (S.empty()) {
+        const size_t Nl = (size_t)nc * level_dofs(c, (int)l);
+        S.resize(5, nullptr);
+        TRY(dalloc(c, &S[0], Nl));
+        TRY(dalloc(c, &S[1], 2 * Nl));
+        S[2] = S[1] + Nl;
+        if (l > 0) { TRY(dalloc(c, &S[3], Nl)); TRY(dalloc(c, &S[4], Nl)); }
+      }
+    }
+  }
+  auto apply_A = [&](const double* src, double* dst, const double* rhs) -> dgvv_status {
+    ApplyArgs a = base_args(c, 0, op);
+    a.src = src; a.dst = dst;
+    if (rhs) { a.b = rhs; a.mode = MODE_RESID; }
+    return run_apply(c, op, 0, a, s);
+  };
+  auto prec = [&](const double* rr, double* zz) -> dgvv_status {
+    if (precond == DGVV_PRECOND_JACOBI) {
+      DGVV_CUDA_TRY(launch_ew_mul(c->L[0].dinv[oi], rr, zz, N, s));
+    } else if (precond == DGVV_PRECOND_VCYCLE) {
+      TRY(vcycle_rec(c, op, 0, rr, zz, lambda_hi_per_level, s));
+    } else {
+      DGVV_CUDA_TRY(cudaMemcpyAsync(zz, rr, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    }
+    return DGVV_OK;
+  };
+  double bb, rr, rz, pq;
+  TRY(dot_host(c, b, b, N, &bb, s));
+  TRY(apply_A(x, r, b));                      // r = b - A x
+  TRY(dot_host(c, r, r, N, &rr, s));
+  const double bn = std::sqrt(bb);
+  int it = 0;
+  if (bn > 0.0 && std::sqrt(rr) > rtol * bn && maxit > 0) {
+    TRY(prec(r, z));
+    DGVV_CUDA_TRY(cudaMemcpyAsync(pv, z, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    TRY(dot_host(c, r, z, N, &rz, s));
+    while (it < maxit) {
+      ++it;
+      TRY(apply_A(pv, q, nullptr));           // q = A p
+      TRY(dot_host(c, pv, q, N, &pq, s));
+      const double alpha = rz / pq;
+      DGVV_CUDA_TRY(launch_axpby(alpha, pv, 1.0, x, N, s));
+      DGVV_CUDA_TRY(launch_axpby(-alpha, q, 1.0, r, N, s));
+      TRY(dot_host(c, r, r, N, &rr, s));
+      if (std::sqrt(rr) <= rtol * bn) break;
+      TRY(prec(r, z));
+      double rz_new;
+      TRY(dot_host(c, r, z, N, &rz_new, s));
+      DGVV_CUDA_TRY(launch_axpby(1.0, z, rz_new / rz, pv, N, s));
+      rz = rz_new;
+    }
+  }
+  if (iters) *iters = it;
+  if (relres) *relres = bn > 0.0 ? std::sqrt(rr) / bn : 0.0;
+  return DGVV_OK;
 }
 
 dgvv_status dgvv_estimate_lambda_max(dgvv_ctx* c, int32_t op, int32_t level, int32_t steps, const double* v0,

@@ -226,6 +226,8 @@ __global__ void diag_kernel(const DiagArgs A) {
     const double pn = (FORM == 0) ? (1.0 + nrm[comp] * nrm[comp]) : 1.0;
     Dv += dA * kappa * (-2.0 * num * phi * eSn + tau * phi * phi * pn);
   }
+  if (A.mass != 0.0)                               // Helmholtz: + mass * JxW_i
+    Dv += A.mass * ((GEO == 0) ? T.w[iv[0]] * T.w[iv[1]] * T.w[iv[2]] * vol : A.jxw[(size_t)cell * n3 + i]);
   A.out[idx] = 1.0 / Dv;
 }
 
@@ -323,6 +325,11 @@ __global__ void cheb_first_kernel(const double* b, const double* dinv, double c_
 __global__ void ew_mul_kernel(const double* a, const double* b, double* out, long n) {
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
     out[i] = a[i] * b[i];
+}
+// y = alpha x + beta y  (CG updates)
+__global__ void axpby_kernel(double alpha, const double* x, double beta, double* y, long n) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+    y[i] = alpha * x[i] + beta * y[i];
 }
 // out = sqrt(a)
 __global__ void ew_sqrt_kernel(const double* a, double* out, long n) {

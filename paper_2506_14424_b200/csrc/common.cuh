@@ -56,6 +56,7 @@ struct ApplyArgs {
   const double* fJi;        // [n_total][6][9][n^2] own J^-1 at face points  (general)
   const double* Hcell;      // [n_total]                   (general)
   double pen;               // IP (k+1)^2
+  double mass;              // Helmholtz: + mass * M (diagonal, M_ii = JxW_i per component)
   // epilogue
   int mode;
   const double* b;          // RESID / CHEB
@@ -93,6 +94,8 @@ struct DiagArgs {
   const double* fJi;
   const double* Hcell;
   double pen;
+  double mass;              // + mass * JxW_i on the diagonal (Helmholtz operator)
+  const double* jxw;        // general geometry: JxW [n_owned][n^3]
   double* out;              // 1 / D
 };
 

@@ -178,6 +178,10 @@ cudaError_t launch_ew_mul(const double* a, const double* b, double* out, long n,
   ew_mul_kernel<<<gs_blocks(n), 256, 0, s>>>(a, b, out, n);
   return cudaGetLastError();
 }
+cudaError_t launch_axpby(double alpha, const double* x, double beta, double* y, long n, cudaStream_t s) {
+  axpby_kernel<<<gs_blocks(n), 256, 0, s>>>(alpha, x, beta, y, n);
+  return cudaGetLastError();
+}
 cudaError_t launch_ew_sqrt(const double* a, double* out, long n, cudaStream_t s) {
   ew_sqrt_kernel<<<gs_blocks(n), 256, 0, s>>>(a, out, n);
   return cudaGetLastError();

@@ -44,6 +44,7 @@ cudaError_t launch_dot(const double* a, const double* b, long n, double* part, i
 cudaError_t launch_cheb_first(const double* b, const double* dinv, double c_r, double* d, double* x, long n,
                               cudaStream_t s);
 cudaError_t launch_ew_mul(const double* a, const double* b, double* out, long n, cudaStream_t s);
+cudaError_t launch_axpby(double alpha, const double* x, double beta, double* y, long n, cudaStream_t s);
 cudaError_t launch_ew_sqrt(const double* a, double* out, long n, cudaStream_t s);
 cudaError_t launch_ew_div(const double* a, const double* b, double* out, long n, cudaStream_t s);
 cudaError_t launch_lanczos_update(double* w, const double* q, const double* qprev, const double* alpha,

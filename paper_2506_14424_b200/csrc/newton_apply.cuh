@@ -68,7 +68,11 @@ __global__ void __launch_bounds__(CPB * n * n, MINB) newton_apply_kernel(const A
 #pragma unroll
   for (int c = 0; c < 3; ++c)
 #pragma unroll
-    for (int z = 0; z < n; ++z) y[c][z] = 0.0;
+    for (int z = 0; z < n; ++z) {        // Helmholtz mass term
+      double jw = 0.0;
+      if (A.mass != 0.0) jw = (GEO == 0) ? T.w[a] * T.w[b] * T.w[z] * vol : A.jxw[(size_t)cell * n3 + z * n2 + p];
+      y[c][z] = A.mass * jw * sw[c * n3 + z * n2 + p];
+    }
 
   auto to_phys = [&](const double (&gx)[3][3], const double (&Ji)[9], double (&G)[3][3]) {
 #pragma unroll

@@ -81,7 +81,8 @@ __global__ void __launch_bounds__(CPB * n * n, MINB) newton_apply2_kernel(const 
 #pragma unroll
   for (int c = 0; c < 3; ++c)
 #pragma unroll
-    for (int z = 0; z < n; ++z) y[c][z] = 0.0;
+    for (int z = 0; z < n; ++z)          // Helmholtz mass term (the mass part of J is M itself)
+      y[c][z] = A.mass == 0.0 ? 0.0 : A.mass * T.w[a] * T.w[b] * T.w[z] * vol * sf[0][c * CST + z * PS + b * RS + a];
 
   // =============================================================== volume
   {

@@ -171,13 +171,20 @@ sipg_apply2_kernel(const ApplyArgs A) {
   double ucol[NC][n], y[NC][n];
   {
     const double* gsrc = A.src + (size_t)cell * NC * n3;
+    double mjw[n];                       // Helmholtz mass term: mass * JxW at the column points
+#pragma unroll
+    for (int z = 0; z < n; ++z) {
+      if (A.mass == 0.0) mjw[z] = 0.0;
+      else if constexpr (GEO == 0) mjw[z] = A.mass * T.w[a] * T.w[b] * T.w[z] * A.cart[(size_t)cell * CART_STRIDE + 4];
+      else mjw[z] = A.mass * A.jxw[(size_t)cell * n3 + z * n2 + p];
+    }
 #pragma unroll
     for (int c = 0; c < NC; ++c)
 #pragma unroll
       for (int z = 0; z < n; ++z) {
         const double v = __ldg(gsrc + c * n3 + z * n2 + p);
         ucol[c][z] = v;
-        y[c][z] = 0.0;
+        y[c][z] = mjw[z] * v;
         su[c * CST + z * PS + b * RS + a] = v;
         if (USE_ST) sT[c * CST + z * PS + a * RS + b] = v;
       }

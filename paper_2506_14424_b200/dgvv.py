@@ -178,6 +178,23 @@ class Context:
         A.check(self._L.dgvv_vcycle(self.h, op, _ptr(b, n, "b"), _ptr(x, n, "x"), arr, _stream()))
         return x
 
+    def set_mass(self, op, mass):
+        """Helmholtz form mass * M + A_op for every later call on op (dgvv_set_mass)."""
+        A.check(self._L.dgvv_set_mass(self.h, op, float(mass)))
+
+    def cg_solve(self, op, b, x, rtol=1e-8, maxit=200, precond="vcycle", lam_hi_per_level=None):
+        """Preconditioned CG on level 0 (dgvv_cg_solve); x = initial guess in, solution out.
+        precond: "none", "jacobi" or "vcycle".  Returns (iterations, ||r|| / ||b||)."""
+        n = self._n(op, 0)
+        pc = {"none": A.PRECOND_NONE, "jacobi": A.PRECOND_JACOBI, "vcycle": A.PRECOND_VCYCLE}[precond]
+        arr = None
+        if lam_hi_per_level is not None:
+            arr = (C.c_double * len(self.degrees))(*[float(v) for v in lam_hi_per_level])
+        it, rr = C.c_int32(), C.c_double()
+        A.check(self._L.dgvv_cg_solve(self.h, op, _ptr(b, n, "b"), _ptr(x, n, "x"), float(rtol), int(maxit), pc,
+                                      arr, C.byref(it), C.byref(rr), _stream()))
+        return it.value, rr.value
+
     def dot(self, a, b, ncomp=1, level=0):
         out = C.c_double()
         n = ncomp * self.n_dofs(level)

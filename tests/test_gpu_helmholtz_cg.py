@@ -1,0 +1,152 @@
+"""§8(f) f1 on the GPU: Helmholtz form mass*M + A (apply, Newton apply, diagonal) and the
+preconditioned CG solve (none / Jacobi / V-cycle) against the CPU oracle (dg.helmholtz_apply,
+dense diagonals, mg.pcg with the oracle V-cycle) on the same seeded inputs."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from inputs import bfs, cube, deformed_cube, uniform                       # noqa: E402
+from inputs.vectors import c3_linearization                               # noqa: E402
+from oracle import dense, dg, laws, mg                                    # noqa: E402
+
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def Ctx(*a, **k):
+    from paper_2506_14424_b200.dgvv import Context
+    return Context(*a, **k)
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+CASES = [("cube3 k3", lambda: cube(3), 3, laws.C1_LAW), ("deformed3 k3", lambda: deformed_cube(3, 3), 3, laws.C2_LAW),
+         ("bfs k2", lambda: bfs(nx_in=2, ny_in=1, nx_out=4, nz=3), 2, laws.C1_LAW)]
+
+
+@pytest.mark.parametrize("name,mk,k,law", CASES, ids=[c[0] for c in CASES])
+def test_helmholtz_apply_and_diagonal(name, mk, k, law):
+    m = mk()
+    d = dg.Disc(m, k)
+    nu = dg.AnalyticNu(d, law)
+    mass = 37.5
+    ctx = Ctx(m, k, visc_law=law)
+    ctx.set_mass(0, mass)
+    u = uniform(0, m.n_cells * 3 * d.N)
+    y = torch.empty(len(u), dtype=torch.float64, device="cuda")
+    ctx.apply_viscous(dev(u), y)
+    assert rel(host(y), dg.helmholtz_apply(d, u, nu, mass)) < TOL
+    if m.n_cells <= 8:
+        H = dense.assemble_viscous(d, nu) + mass * np.diag(dg.mass_apply(d, np.ones(len(u))))
+        dinv = torch.empty_like(y)
+        ctx.inverse_diagonal(0, dinv)
+        assert rel(host(dinv), 1.0 / np.diag(H)) < TOL
+    ctx.set_mass(0, 0.0)                      # back to the plain operator
+    ctx.apply_viscous(dev(u), y)
+    assert rel(host(y), dg.viscous_apply(d, u, nu)) < TOL
+    from paper_2506_14424_b200 import DgvvError
+    with pytest.raises(DgvvError):
+        ctx.set_mass(0, -1.0)
+
+
+def test_helmholtz_newton_apply():
+    m = cube(3)
+    k = 4
+    d = dg.Disc(m, k)
+    u0 = c3_linearization(m, k)
+    w = uniform(0, len(u0))
+    mass = 12.0
+    ctx = Ctx(m, k, visc_law=laws.C3_CARREAU)
+    ctx.set_mass(0, mass)
+    ul = dev(u0)
+    ctx.update_viscosity(ul)
+    y = torch.empty_like(ul)
+    ctx.apply_linearized_viscous(dev(w), y)
+    ref = dg.newton_apply(d, u0, w, laws.C3_CARREAU) + mass * dg.mass_apply(d, w)
+    assert rel(host(y), ref) < TOL
+
+
+def _viscous_levels(m, degs, law, mass):
+    levels = []
+    for li, k in enumerate(degs):
+        d = dg.Disc(m, k)
+        nu = dg.AnalyticNu(d, law)
+        A = dense.assemble_viscous(d, nu)
+        A = A + mass * np.diag(dg.mass_apply(d, np.ones(A.shape[0])))
+        L = {"apply": (lambda x, A=A: A @ x), "Dinv": 1.0 / np.diag(A)}
+        if li + 1 < len(degs):
+            kc = degs[li + 1]
+            L["restrict"] = lambda r, k=k, kc=kc: mg.restrict(r, k, kc, m.n_cells, ncomp=3)
+            L["prolongate"] = lambda x, k=k, kc=kc: mg.prolongate(x, k, kc, m.n_cells, ncomp=3)
+        levels.append(L)
+    return levels
+
+
+@pytest.mark.parametrize("precond", ["none", "jacobi", "vcycle"])
+def test_cg_parity_fixed_iterations(precond):
+    """rtol = 0, maxit = 6: GPU and oracle run exactly the same 6 PCG iterations."""
+    m = deformed_cube(2, 3)
+    degs = [3, 2, 1]
+    mass = 20.0
+    law = laws.C2_LAW
+    ctx = Ctx(m, 3, visc_law=law, degrees=degs)
+    ctx.set_mass(0, mass)
+    levels = _viscous_levels(m, degs, law, mass)
+    lams = []
+    for l, L in enumerate(levels):
+        v0 = uniform(2, len(L["Dinv"]))
+        lo = mg.lanczos_lambda_max(L["apply"], L["Dinv"], v0, 20)
+        lg = ctx.estimate_lambda_max(0, dev(v0), level=l, steps=20)
+        assert abs(lg - lo) < 1e-10 * lo
+        lams.append(1.2 * lo)
+        L["lam_hi"] = 1.2 * lo
+    n0 = len(levels[0]["Dinv"])
+    b = uniform(0, n0)
+    x0 = 0.1 * uniform(5, n0)
+    P = {"none": lambda r: r, "jacobi": lambda r: levels[0]["Dinv"] * r,
+         "vcycle": lambda r: mg.vcycle(levels, r)}[precond]
+    xr, itr, rrr = mg.pcg(levels[0]["apply"], b, x0, P, 0.0, 6)
+    x = dev(x0)
+    it, rr = ctx.cg_solve(0, dev(b), x, rtol=0.0, maxit=6, precond=precond, lam_hi_per_level=lams)
+    assert it == itr == 6
+    assert rel(host(x), xr) < 1e-10
+    assert abs(rr - rrr) < 1e-8 * rrr
+
+
+def test_cg_vcycle_converges_full_size_c3():
+    """C3 at full size (98.3M DoFs), Helmholtz viscous step (mass = 1/dt-like) with the Carreau
+    viscosity: V-cycle-preconditioned CG to rtol 1e-8; the returned residual is checked with an
+    independent apply, ||b - H x|| / ||b|| <= rtol."""
+    m = cube(64)
+    degs = [4, 2, 1]
+    ctx = Ctx(m, 4, visc_law=laws.C3_CARREAU, degrees=degs)
+    ctx.set_mass(0, 1.0e3)
+    ctx.update_viscosity(dev(c3_linearization(m, 4)))
+    lams = [1.2 * ctx.estimate_lambda_max(0, dev(uniform(2, 3 * ctx.n_dofs(l))), level=l, steps=20)
+            for l in range(len(degs))]
+    n0 = 3 * ctx.n_dofs(0)
+    b = dev(uniform(0, n0))
+    x = torch.zeros(n0, dtype=torch.float64, device="cuda")
+    it, rr = ctx.cg_solve(0, b, x, rtol=1e-8, maxit=100, precond="vcycle", lam_hi_per_level=lams)
+    assert rr <= 1e-8 and it < 100
+    y = torch.empty_like(x)
+    ctx.apply_viscous(x, y)
+    assert float(torch.linalg.norm(b - y) / torch.linalg.norm(b)) <= 1.01e-8
