@@ -38,10 +38,11 @@ struct Tab1D {
 
 enum { MODE_APPLY = 0, MODE_RESID = 1, MODE_CHEB = 2 };
 
-struct ApplyArgs {
-  const double* src;        // owned cells [n_owned][NC][n^3]
-  const double* ghost;      // ghost cells [n_ghost][NC][n^3] (may be null)
-  double* dst;
+template <typename R>
+struct ApplyArgsT {  // R = double (operators) or float (FP32 multigrid levels)
+  const R* src;        // owned cells [n_owned][NC][n^3]
+  const R* ghost;      // ghost cells [n_ghost][NC][n^3] (may be null)
+  R* dst;
   const int* nbr;           // [n_total][6]
   const int* cell_list;     // cells to process (null: cell_base .. cell_base+n_proc-1)
   int n_proc;
@@ -49,28 +50,29 @@ struct ApplyArgs {
   int n_owned;
   // coefficient at quadrature points.  Cartesian: nu itself; general geometry:
   // premultiplied weights nu*JxW (cells) and nu*dA (own face points).
-  const double* nu_cell;    // [n_owned][n^3]
-  const double* nu_face;    // [n_total][6][n^2]
-  const double* cart;       // [n_total][CART_STRIDE]      (Cartesian)
-  const double* vJi;        // [n_total][9][n^3]  J^-1 at cell points        (general)
-  const double* fJi;        // [n_total][6][9][n^2] own J^-1 at face points  (general)
-  const double* Hcell;      // [n_total]                   (general)
+  const R* nu_cell;    // [n_owned][n^3]
+  const R* nu_face;    // [n_total][6][n^2]
+  const R* cart;       // [n_total][CART_STRIDE]      (Cartesian)
+  const R* vJi;        // [n_total][9][n^3]  J^-1 at cell points        (general)
+  const R* fJi;        // [n_total][6][9][n^2] own J^-1 at face points  (general)
+  const R* Hcell;      // [n_total]                   (general)
   double pen;               // IP (k+1)^2
   double mass;              // Helmholtz: + mass * M (diagonal, M_ii = JxW_i per component)
   // epilogue
   int mode;
-  const double* b;          // RESID / CHEB
-  const double* dinv;       // CHEB
-  double* dvec;             // CHEB: d in/out
-  double* xout;             // CHEB: x_{j+1}
+  const R* b;          // RESID / CHEB
+  const R* dinv;       // CHEB
+  R* dvec;             // CHEB: d in/out
+  R* xout;             // CHEB: x_{j+1}
   double c_rho, c_r;        // CHEB: d = c_rho d + c_r Dinv r
   // Newton (linearised) extras
-  const double* ulin;       // owned u_lin
-  const double* ulin_ghost; // ghost u_lin
-  const double* jxw;        // general geometry: JxW [n_owned][n^3]
-  const double* fdA;        // general geometry: dA  [n_total][6][n^2]
+  const R* ulin;       // owned u_lin
+  const R* ulin_ghost; // ghost u_lin
+  const R* jxw;        // general geometry: JxW [n_owned][n^3]
+  const R* fdA;        // general geometry: dA  [n_total][6][n^2]
   double law[4];            // eta0, eta_inf, lambda, n
 };
+using ApplyArgs = ApplyArgsT<double>;
 
 struct NuArgs {
   const double* u;          // owned [n_owned][3][n^3]

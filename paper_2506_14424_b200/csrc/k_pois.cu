@@ -6,6 +6,7 @@
 namespace dgvv {
 
 cudaError_t launch_apply_visc(int n, int form, int geo, const ApplyArgs& a, cudaStream_t s);
+cudaError_t launch_apply_visc_f(int n, int form, int geo, const ApplyArgsT<float>& a, cudaStream_t s);
 
 cudaError_t upload_tables_pois(const Tab1D* tabs) { return tu_upload_tables(tabs); }
 
@@ -24,11 +25,11 @@ cudaError_t upload_tables_pois(const Tab1D* tabs) { return tu_upload_tables(tabs
 template <int n> constexpr int cpb_pois() { return n == 2 ? 32 : n == 3 ? PCPB3 : n == 4 ? PCPB4 : n == 5 ? 5 : n == 6 ? PCPB6 : 3; }
 template <int n> constexpr int minb_pois() { return n <= 3 ? 3 : n == 6 ? PMINB6 : 4; }
 
-template <int n, int GEO>
-static cudaError_t run(const ApplyArgs& a, cudaStream_t s) {
+template <typename R, int n, int GEO>
+static cudaError_t run(const ApplyArgsT<R>& a, cudaStream_t s) {
   constexpr int CPB = cpb_pois<n>();
-  const size_t smem = (size_t)CPB * Apply2Cfg<n, 1, 1, GEO>::CS * sizeof(double);
-  auto k = sipg_apply2_kernel<n, 1, 1, GEO, CPB, minb_pois<n>()>;
+  const size_t smem = (size_t)CPB * Apply2Cfg<n, 1, 1, GEO>::CS * sizeof(R);
+  auto k = sipg_apply2_kernel<R, n, 1, 1, GEO, CPB, minb_pois<n>()>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -41,17 +42,26 @@ static cudaError_t run(const ApplyArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_apply(int nc, int n, int form, int geo, const ApplyArgs& a, cudaStream_t s) {
-  if (nc == 3) return launch_apply_visc(n, form, geo, a, s);
+template <typename R>
+static cudaError_t launch_pois_t(int n, int geo, const ApplyArgsT<R>& a, cudaStream_t s) {
   switch (n) {
-    case 2: return geo ? run<2, 1>(a, s) : run<2, 0>(a, s);
-    case 3: return geo ? run<3, 1>(a, s) : run<3, 0>(a, s);
-    case 4: return geo ? run<4, 1>(a, s) : run<4, 0>(a, s);
-    case 5: return geo ? run<5, 1>(a, s) : run<5, 0>(a, s);
-    case 6: return geo ? run<6, 1>(a, s) : run<6, 0>(a, s);
-    case 7: return geo ? run<7, 1>(a, s) : run<7, 0>(a, s);
+    case 2: return geo ? run<R, 2, 1>(a, s) : run<R, 2, 0>(a, s);
+    case 3: return geo ? run<R, 3, 1>(a, s) : run<R, 3, 0>(a, s);
+    case 4: return geo ? run<R, 4, 1>(a, s) : run<R, 4, 0>(a, s);
+    case 5: return geo ? run<R, 5, 1>(a, s) : run<R, 5, 0>(a, s);
+    case 6: return geo ? run<R, 6, 1>(a, s) : run<R, 6, 0>(a, s);
+    case 7: return geo ? run<R, 7, 1>(a, s) : run<R, 7, 0>(a, s);
     default: return cudaErrorInvalidValue;
   }
+}
+
+cudaError_t launch_apply(int nc, int n, int form, int geo, const ApplyArgs& a, cudaStream_t s) {
+  if (nc == 3) return launch_apply_visc(n, form, geo, a, s);
+  return launch_pois_t<double>(n, geo, a, s);
+}
+cudaError_t launch_apply_f(int nc, int n, int form, int geo, const ApplyArgsT<float>& a, cudaStream_t s) {
+  if (nc == 3) return launch_apply_visc_f(n, form, geo, a, s);
+  return launch_pois_t<float>(n, geo, a, s);
 }
 
 }  // namespace dgvv

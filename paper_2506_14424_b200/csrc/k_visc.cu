@@ -35,12 +35,12 @@ template <int n, int GEO> constexpr int minb_visc() {
   return n == 2 ? 2 : n == 3 ? 3 : n == 4 ? (GEO ? MINB4G : MINB4) : n == 5 ? MINB5 : 2;
 }
 
-template <int n, int FORM, int GEO>
-static cudaError_t run(const ApplyArgs& a, cudaStream_t s) {
+template <typename R, int n, int FORM, int GEO>
+static cudaError_t run(const ApplyArgsT<R>& a, cudaStream_t s) {
   constexpr int CPB = cpb_visc<n, GEO>();
   constexpr int NC = 3;
-  const size_t smem = (size_t)CPB * Apply2Cfg<n, NC, FORM, GEO>::CS * sizeof(double);
-  auto k = sipg_apply2_kernel<n, NC, FORM, GEO, CPB, minb_visc<n, GEO>()>;
+  const size_t smem = (size_t)CPB * Apply2Cfg<n, NC, FORM, GEO>::CS * sizeof(R);
+  auto k = sipg_apply2_kernel<R, n, NC, FORM, GEO, CPB, minb_visc<n, GEO>()>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -53,21 +53,30 @@ static cudaError_t run(const ApplyArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-template <int n>
-static cudaError_t run_n(int form, int geo, const ApplyArgs& a, cudaStream_t s) {
-  if (form == 0) return geo == 0 ? run<n, 0, 0>(a, s) : run<n, 0, 1>(a, s);
-  return geo == 0 ? run<n, 1, 0>(a, s) : run<n, 1, 1>(a, s);
+template <typename R, int n>
+static cudaError_t run_n(int form, int geo, const ApplyArgsT<R>& a, cudaStream_t s) {
+  if (form == 0) return geo == 0 ? run<R, n, 0, 0>(a, s) : run<R, n, 0, 1>(a, s);
+  return geo == 0 ? run<R, n, 1, 0>(a, s) : run<R, n, 1, 1>(a, s);
+}
+
+template <typename R>
+static cudaError_t launch_visc_t(int n, int form, int geo, const ApplyArgsT<R>& a, cudaStream_t s) {
+  switch (n) {
+    case 2: return run_n<R, 2>(form, geo, a, s);
+    case 3: return run_n<R, 3>(form, geo, a, s);
+    case 4: return run_n<R, 4>(form, geo, a, s);
+    case 5: return run_n<R, 5>(form, geo, a, s);
+    case 6: return run_n<R, 6>(form, geo, a, s);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 cudaError_t launch_apply_visc(int n, int form, int geo, const ApplyArgs& a, cudaStream_t s) {
-  switch (n) {
-    case 2: return run_n<2>(form, geo, a, s);
-    case 3: return run_n<3>(form, geo, a, s);
-    case 4: return run_n<4>(form, geo, a, s);
-    case 5: return run_n<5>(form, geo, a, s);
-    case 6: return run_n<6>(form, geo, a, s);
-    default: return cudaErrorInvalidValue;
-  }
+  return launch_visc_t<double>(n, form, geo, a, s);
+}
+// FP32 levels of the multigrid preconditioner
+cudaError_t launch_apply_visc_f(int n, int form, int geo, const ApplyArgsT<float>& a, cudaStream_t s) {
+  return launch_visc_t<float>(n, form, geo, a, s);
 }
 
 }  // namespace dgvv

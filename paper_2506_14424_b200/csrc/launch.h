@@ -14,6 +14,8 @@ cudaError_t upload_tables_newton(const Tab1D* tabs);
 
 // K1 / K4 / K6: SIPG apply with epilogue (nc = 3 viscous, 1 Poisson)
 cudaError_t launch_apply(int nc, int n, int form, int geo, const ApplyArgs& a, cudaStream_t s);
+// FP32 variant (multigrid preconditioner levels)
+cudaError_t launch_apply_f(int nc, int n, int form, int geo, const ApplyArgsT<float>& a, cudaStream_t s);
 // K2: Newton-linearised viscous apply
 cudaError_t launch_newton(int n, int geo, const ApplyArgs& a, cudaStream_t s);
 // K3: Carreau viscosity at all points

@@ -74,54 +74,66 @@ __device__ __forceinline__ void mbar_wait(uint64_t* m, uint32_t parity) {
                " @!P bra WAIT_%=;\n}" ::"r"(smem_u32(m)), "r"(parity) : "memory");
 }
 
-// row of n doubles (16-byte aligned) into registers
-template <int n>
-__device__ __forceinline__ void ld_row(const double* __restrict__ r, double (&x)[n]) {
+// 2-element vector type of the real type (16-byte rows for double, 8-byte for float)
+template <typename R> struct V2;
+template <> struct V2<double> {
+  using t = double2;
+  static __device__ __forceinline__ t mk(double a, double b) { return make_double2(a, b); }
+};
+template <> struct V2<float> {
+  using t = float2;
+  static __device__ __forceinline__ t mk(float a, float b) { return make_float2(a, b); }
+};
+
+// row of n values (2-element aligned) into registers
+template <int n, typename R>
+__device__ __forceinline__ void ld_row(const R* __restrict__ r, R (&x)[n]) {
 #pragma unroll
   for (int k = 0; k + 1 < n; k += 2) {
-    const double2 v = *reinterpret_cast<const double2*>(r + k);
+    const typename V2<R>::t v = *reinterpret_cast<const typename V2<R>::t*>(r + k);
     x[k] = v.x;
     x[k + 1] = v.y;
   }
   if constexpr (n & 1) x[n - 1] = r[n - 1];
 }
-template <int n>
-__device__ __forceinline__ void ldg_row(const double* __restrict__ r, double (&x)[n]) {
+template <int n, typename R>
+__device__ __forceinline__ void ldg_row(const R* __restrict__ r, R (&x)[n]) {
 #pragma unroll
   for (int k = 0; k + 1 < n; k += 2) {
-    const double2 v = __ldg(reinterpret_cast<const double2*>(r + k));
+    const typename V2<R>::t v = __ldg(reinterpret_cast<const typename V2<R>::t*>(r + k));
     x[k] = v.x;
     x[k + 1] = v.y;
   }
   if constexpr (n & 1) x[n - 1] = __ldg(r + n - 1);
 }
-template <int n>
-__device__ __forceinline__ void st_row(double* __restrict__ r, const double (&x)[n]) {
+template <int n, typename R>
+__device__ __forceinline__ void st_row(R* __restrict__ r, const R (&x)[n]) {
 #pragma unroll
-  for (int k = 0; k + 1 < n; k += 2) *reinterpret_cast<double2*>(r + k) = make_double2(x[k], x[k + 1]);
+  for (int k = 0; k + 1 < n; k += 2) *reinterpret_cast<typename V2<R>::t*>(r + k) = V2<R>::mk(x[k], x[k + 1]);
   if constexpr (n & 1) r[n - 1] = x[n - 1];
 }
-template <int n>
-__device__ __forceinline__ double rowdot(const double* __restrict__ r, const double (&w)[n]) {
-  double x[n];
+template <int n, typename R>
+__device__ __forceinline__ R rowdot(const R* __restrict__ r, const R (&w)[n]) {
+  R x[n];
   ld_row<n>(r, x);
-  double s = 0.0;
+  R s = R(0);
 #pragma unroll
   for (int k = 0; k < n; ++k) s = fma(w[k], x[k], s);
   return s;
 }
 
-template <int n, int NC, int FORM, int GEO, int CPB, int MINB>
+template <typename R, int n, int NC, int FORM, int GEO, int CPB, int MINB>
 __global__ void __launch_bounds__(CPB * n * n, MINB)
-sipg_apply2_kernel(const ApplyArgs A) {
+sipg_apply2_kernel(const ApplyArgsT<R> A) {
   static_assert(FORM == 1 || NC == 3, "divergence form needs 3 components");
   using L = Lay<n>;
   using Cf = Apply2Cfg<n, NC, FORM, GEO>;
   constexpr int n2 = L::n2, n3 = L::n3, RS = L::RS, PS = L::PS, CST = L::CST, FA = L::FA;
   constexpr int NT = Cf::NT, VOL = Cf::VOL;
-  extern __shared__ __align__(16) double smem[];
-  __shared__ __align__(16) double sD[n * RS];    // sD[i][k]  = l_k'(x_i)
-  __shared__ __align__(16) double sDT[n * RS];   // sDT[i][k] = l_i'(x_k)
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  R* smem = reinterpret_cast<R*>(smem_raw);
+  __shared__ __align__(16) R sD[n * RS];    // sD[i][k]  = l_k'(x_i)
+  __shared__ __align__(16) R sDT[n * RS];   // sDT[i][k] = l_i'(x_k)
   __shared__ int sid[CPB];
   const Tab1D& T = c_tab[n];
 
@@ -135,16 +147,16 @@ sipg_apply2_kernel(const ApplyArgs A) {
 
   for (int i = threadIdx.x; i < n * RS; i += blockDim.x) {
     const int r = i / RS, k = i - r * RS;
-    sD[i] = k < n ? T.D[r * DGVV_NMAX + k] : 0.0;
-    sDT[i] = k < n ? T.D[k * DGVV_NMAX + r] : 0.0;
+    sD[i] = k < n ? R(T.D[r * DGVV_NMAX + k]) : R(0.0);
+    sDT[i] = k < n ? R(T.D[k * DGVV_NMAX + r]) : R(0.0);
   }
   if (p == 0) sid[lc] = active ? cell : -1;
   __shared__ __align__(8) uint64_t mbar[CPB];
-  double* stg = smem + lc * Cf::CS + (Cf::CS - Cf::STG);   // face-metric stage (TMA)
+  R* stg = smem + lc * Cf::CS + (Cf::CS - Cf::STG);   // face-metric stage (TMA)
   // issue the TMA bulk copies of direction d's face metric for this cell (thread p == 0)
   auto stage_issue = [&](int d, const int (&nb)[6]) {
     if constexpr (Cf::TMA) {
-      constexpr uint32_t BJ = 9 * n2 * 8, BN = n2 * 8;
+      constexpr uint32_t BJ = 9 * n2 * sizeof(R), BN = n2 * sizeof(R);
       uint32_t bytes = 2 * (BJ + BN);
 #pragma unroll
       for (int s = 0; s < 2; ++s) bytes += nb[2 * d + s] >= 0 ? BJ + BN : 0;
@@ -164,34 +176,34 @@ sipg_apply2_kernel(const ApplyArgs A) {
     }
   };
 
-  double* su = smem + lc * Cf::CS;      // values     [NC][z][y][x]
-  double* sT = su + VOL;                // transposed [NC][z][x][y] (USE_ST)
-  double* R = su + (1 + USE_ST) * VOL;  // work: W1 | W2T (volume); Y | face buffers (faces)
+  R* su = smem + lc * Cf::CS;      // values     [NC][z][y][x]
+  R* sT = su + VOL;                // transposed [NC][z][x][y] (USE_ST)
+  R* WK = su + (1 + USE_ST) * VOL;  // work: W1 | W2T (volume); Y | face buffers (faces)
 
-  double ucol[NC][n], y[NC][n];
+  R ucol[NC][n], y[NC][n];
   {
-    const double* gsrc = A.src + (size_t)cell * NC * n3;
-    double mjw[n];                       // Helmholtz mass term: mass * JxW at the column points
+    const R* gsrc = A.src + (size_t)cell * NC * n3;
+    R mjw[n];                       // Helmholtz mass term: mass * JxW at the column points
 #pragma unroll
     for (int z = 0; z < n; ++z) {
-      if (A.mass == 0.0) mjw[z] = 0.0;
-      else if constexpr (GEO == 0) mjw[z] = A.mass * T.w[a] * T.w[b] * T.w[z] * A.cart[(size_t)cell * CART_STRIDE + 4];
-      else mjw[z] = A.mass * A.jxw[(size_t)cell * n3 + z * n2 + p];
+      if (R(A.mass) == R(0.0)) mjw[z] = R(0.0);
+      else if constexpr (GEO == 0) mjw[z] = R(A.mass) * R(T.w[a]) * R(T.w[b]) * R(T.w[z]) * A.cart[(size_t)cell * CART_STRIDE + 4];
+      else mjw[z] = R(A.mass) * A.jxw[(size_t)cell * n3 + z * n2 + p];
     }
 #pragma unroll
     for (int c = 0; c < NC; ++c)
 #pragma unroll
       for (int z = 0; z < n; ++z) {
-        const double v = __ldg(gsrc + c * n3 + z * n2 + p);
+        const R v = __ldg(gsrc + c * n3 + z * n2 + p);
         ucol[c][z] = v;
         y[c][z] = mjw[z] * v;
         su[c * CST + z * PS + b * RS + a] = v;
         if (USE_ST) sT[c * CST + z * PS + a * RS + b] = v;
       }
   }
-  double ih[3] = {0, 0, 0}, vol = 0.0, Hm;
+  R ih[3] = {0, 0, 0}, vol = R(0.0), Hm;
   if constexpr (GEO == 0) {
-    const double* cg = A.cart + (size_t)cell * CART_STRIDE;
+    const R* cg = A.cart + (size_t)cell * CART_STRIDE;
     ih[0] = cg[0]; ih[1] = cg[1]; ih[2] = cg[2]; Hm = cg[3]; vol = cg[4];
   } else {
     Hm = A.Hcell[cell];
@@ -210,40 +222,40 @@ sipg_apply2_kernel(const ApplyArgs A) {
 
   // =============================================================== volume term
   {
-    double Da[n], Db[n];
+    R Da[n], Db[n];
     ld_row<n>(sD + a * RS, Da);
     ld_row<n>(sD + b * RS, Db);
-    const double wab = T.w[a] * T.w[b];
+    const R wab = R(T.w[a]) * R(T.w[b]);
 #pragma unroll
     for (int z = 0; z < n; ++z) {
       const int q = z * n2 + p;
-      double gxi[NC][3];
+      R gxi[NC][3];
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
         gxi[c][0] = rowdot<n>(su + c * CST + z * PS + b * RS, Da);
         if (USE_ST) {
           gxi[c][1] = rowdot<n>(sT + c * CST + z * PS + a * RS, Db);
         } else {
-          double sy = 0.0;
+          R sy = R(0.0);
 #pragma unroll
           for (int k = 0; k < n; ++k) sy = fma(Db[k], su[c * CST + z * PS + k * RS + a], sy);
           gxi[c][1] = sy;
         }
-        double sz = 0.0;
+        R sz = R(0.0);
 #pragma unroll
-        for (int k = 0; k < n; ++k) sz = fma(T.D[z * DGVV_NMAX + k], ucol[c][k], sz);
+        for (int k = 0; k < n; ++k) sz = fma(R(T.D[z * DGVV_NMAX + k]), ucol[c][k], sz);
         gxi[c][2] = sz;
       }
-      double Ji[9], w;
+      R Ji[9], w;
       if constexpr (GEO == 0) {
-        w = A.nu_cell[(size_t)cell * n3 + q] * wab * T.w[z] * vol;
+        w = A.nu_cell[(size_t)cell * n3 + q] * wab * R(T.w[z]) * vol;
       } else {
-        const double* vm = A.vJi + (size_t)cell * 9 * n3 + q;
+        const R* vm = A.vJi + (size_t)cell * 9 * n3 + q;
 #pragma unroll
         for (int r = 0; r < 9; ++r) Ji[r] = __ldg(vm + r * n3);
         w = A.nu_cell[(size_t)cell * n3 + q];                  // nu * JxW
       }
-      double G[NC][3];
+      R G[NC][3];
 #pragma unroll
       for (int c = 0; c < NC; ++c)
 #pragma unroll
@@ -253,33 +265,33 @@ sipg_apply2_kernel(const ApplyArgs A) {
         }
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
-        double Tc[3];
+        R Tc[3];
 #pragma unroll
         for (int j = 0; j < 3; ++j) {
           if constexpr (FORM == 0) Tc[j] = w * (G[c][j] + G[j][c]);
           else Tc[j] = w * G[c][j];
         }
-        double F[3];
+        R F[3];
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
           if constexpr (GEO == 0) F[k] = Tc[k] * ih[k];
           else F[k] = Tc[0] * Ji[3 * k] + Tc[1] * Ji[3 * k + 1] + Tc[2] * Ji[3 * k + 2];
         }
-        R[c * CST + z * PS + b * RS + a] = F[0];               // W1  [c][z][y][x]
-        R[VOL + c * CST + z * PS + a * RS + b] = F[1];         // W2T [c][z][x][y]
+        WK[c * CST + z * PS + b * RS + a] = F[0];               // W1  [c][z][y][x]
+        WK[VOL + c * CST + z * PS + a * RS + b] = F[1];         // W2T [c][z][x][y]
 #pragma unroll
-        for (int z2 = 0; z2 < n; ++z2) y[c][z2] = fma(T.D[z * DGVV_NMAX + z2], F[2], y[c][z2]);
+        for (int z2 = 0; z2 < n; ++z2) y[c][z2] = fma(R(T.D[z * DGVV_NMAX + z2]), F[2], y[c][z2]);
       }
     }
     __syncthreads();
-    double DTa[n], DTb[n];
+    R DTa[n], DTb[n];
     ld_row<n>(sDT + a * RS, DTa);
     ld_row<n>(sDT + b * RS, DTb);
 #pragma unroll
     for (int c = 0; c < NC; ++c)
 #pragma unroll
       for (int z = 0; z < n; ++z)
-        y[c][z] += rowdot<n>(R + c * CST + z * PS + b * RS, DTa) + rowdot<n>(R + VOL + c * CST + z * PS + a * RS, DTb);
+        y[c][z] += rowdot<n>(WK + c * CST + z * PS + b * RS, DTa) + rowdot<n>(WK + VOL + c * CST + z * PS + a * RS, DTb);
     __syncthreads();
   }
 
@@ -293,10 +305,10 @@ sipg_apply2_kernel(const ApplyArgs A) {
     const int d = (dd == 0) ? 2 : dd - 1;
     const int t1 = face_t1(d), t2 = face_t2(d);
 
-    double um[2][NC], dm[2][NC], up[2][NC], dp[2][NC];
+    R um[2][NC], dm[2][NC], up[2][NC], dp[2][NC];
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
-      double x[n];
+      R x[n];
       if (d == 2) {
 #pragma unroll
         for (int i = 0; i < n; ++i) x[i] = ucol[c][i];
@@ -306,11 +318,11 @@ sipg_apply2_kernel(const ApplyArgs A) {
 #pragma unroll
         for (int i = 0; i < n; ++i) x[i] = su[c * CST + b * PS + i * RS + a];
       }
-      double v0 = 0.0, g0 = 0.0, v1 = 0.0, g1 = 0.0;
+      R v0 = R(0.0), g0 = R(0.0), v1 = R(0.0), g1 = R(0.0);
 #pragma unroll
       for (int i = 0; i < n; ++i) {
-        v0 = fma(T.l0[i], x[i], v0); g0 = fma(T.d0[i], x[i], g0);
-        v1 = fma(T.l1[i], x[i], v1); g1 = fma(T.d1[i], x[i], g1);
+        v0 = fma(R(T.l0[i]), x[i], v0); g0 = fma(R(T.d0[i]), x[i], g0);
+        v1 = fma(R(T.l1[i]), x[i], v1); g1 = fma(R(T.d1[i]), x[i], g1);
       }
       um[0][c] = v0; dm[0][c] = g0; um[1][c] = v1; dm[1][c] = g1;
     }
@@ -323,12 +335,12 @@ sipg_apply2_kernel(const ApplyArgs A) {
         const double* dO = s ? T.d0 : T.d1;
         const int sl = lc + (nbv - cell);
         const bool in_cta = sl >= 0 && sl < CPB && sid[sl] == nbv;
-        const double* pn = nbv < A.n_owned ? A.src + (size_t)nbv * NC * n3
+        const R* pn = nbv < A.n_owned ? A.src + (size_t)nbv * NC * n3
                                            : A.ghost + (size_t)(nbv - A.n_owned) * NC * n3;
-        const double* ns = smem + (in_cta ? sl : 0) * Cf::CS;
+        const R* ns = smem + (in_cta ? sl : 0) * Cf::CS;
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
-          double x[n];
+          R x[n];
           if (in_cta) {
             if (d == 2) {
 #pragma unroll
@@ -354,9 +366,9 @@ sipg_apply2_kernel(const ApplyArgs A) {
               for (int i = 0; i < n; ++i) x[i] = __ldg(pn + c * n3 + i * n2 + p);
             }
           }
-          double v = 0.0, g = 0.0;
+          R v = R(0.0), g = R(0.0);
 #pragma unroll
-          for (int i = 0; i < n; ++i) { v = fma(lO[i], x[i], v); g = fma(dO[i], x[i], g); }
+          for (int i = 0; i < n; ++i) { v = fma(R(lO[i]), x[i], v); g = fma(R(dO[i]), x[i], g); }
           up[s][c] = v; dp[s][c] = g;
         }
       } else {
@@ -370,23 +382,23 @@ sipg_apply2_kernel(const ApplyArgs A) {
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
           const int c = (GEO == 1) ? t : d;
-          R[VOL + ((s * 4 + 0) * NT + t) * FA + b * RS + a] = um[s][c];
-          R[VOL + ((s * 4 + 1) * NT + t) * FA + b * RS + a] = up[s][c];
+          WK[VOL + ((s * 4 + 0) * NT + t) * FA + b * RS + a] = um[s][c];
+          WK[VOL + ((s * 4 + 1) * NT + t) * FA + b * RS + a] = up[s][c];
         }
       __syncthreads();
     }
 
-    double fv[2][NC], gn[2][NC];
+    R fv[2][NC], gn[2][NC];
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
       const int f = 2 * d + s;
       const int nbv = nbf[f];
       const bool inter = nbv >= 0;
       const bool act = inter || (nbv == NB_DIRICHLET);
-      const double* Tm = R + VOL + (s * 4 + 0) * NT * FA;
-      const double* Tp = R + VOL + (s * 4 + 1) * NT * FA;
+      const R* Tm = WK + VOL + (s * 4 + 0) * NT * FA;
+      const R* Tp = WK + VOL + (s * 4 + 1) * NT * FA;
       // general geometry: every global load of this face issued up front (one round trip)
-      double Jim[9], Jip[9], wm = 0.0, wp = 0.0, Hp = Hm;
+      R Jim[9], Jip[9], wm = R(0.0), wp = R(0.0), Hp = Hm;
       if constexpr (Cf::TMA) {
         if (s == 0) mbar_wait(&mbar[lc], dd & 1);
 #pragma unroll
@@ -400,13 +412,13 @@ sipg_apply2_kernel(const ApplyArgs A) {
           Hp = A.Hcell[nbv];
         }
       } else if constexpr (GEO == 1) {
-        const double* fm = A.fJi + ((size_t)cell * 6 + f) * 9 * n2 + p;
+        const R* fm = A.fJi + ((size_t)cell * 6 + f) * 9 * n2 + p;
 #pragma unroll
         for (int r = 0; r < 9; ++r) Jim[r] = __ldg(fm + r * n2);
         wm = A.nu_face[((size_t)cell * 6 + f) * n2 + p];      // nu * dA
         wp = wm;
         if (inter) {
-          const double* fp = A.fJi + ((size_t)nbv * 6 + (f ^ 1)) * 9 * n2 + p;
+          const R* fp = A.fJi + ((size_t)nbv * 6 + (f ^ 1)) * 9 * n2 + p;
 #pragma unroll
           for (int r = 0; r < 9; ++r) Jip[r] = __ldg(fp + r * n2);
           wp = A.nu_face[((size_t)nbv * 6 + (f ^ 1)) * n2 + p];
@@ -414,15 +426,15 @@ sipg_apply2_kernel(const ApplyArgs A) {
         }
       }
       // tangential reference derivatives of the traces (NT components)
-      double tm1[NT > 0 ? NT : 1], tm2[NT > 0 ? NT : 1], tp1[NT > 0 ? NT : 1], tp2[NT > 0 ? NT : 1];
+      R tm1[NT > 0 ? NT : 1], tm2[NT > 0 ? NT : 1], tp1[NT > 0 ? NT : 1], tp2[NT > 0 ? NT : 1];
       if constexpr (NT > 0) {
-        double Da[n], Db[n];
+        R Da[n], Db[n];
         ld_row<n>(sD + a * RS, Da);
         ld_row<n>(sD + b * RS, Db);
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
           tm1[t] = rowdot<n>(Tm + t * FA + b * RS, Da);
-          double m2 = 0.0, p2 = 0.0;
+          R m2 = R(0.0), p2 = R(0.0);
 #pragma unroll
           for (int k = 0; k < n; ++k) m2 = fma(Db[k], Tm[t * FA + k * RS + a], m2);
           tm2[t] = m2;
@@ -438,50 +450,50 @@ sipg_apply2_kernel(const ApplyArgs A) {
         }
       }
 
-      double gt1[NT > 0 ? NT : 1], gt2[NT > 0 ? NT : 1];
+      R gt1[NT > 0 ? NT : 1], gt2[NT > 0 ? NT : 1];
       if constexpr (GEO == 0) {
         // ---------------- Cartesian: n = sgn e_d, J^-1 = diag(1/h)
-        const double sgn = s ? 1.0 : -1.0;
-        const double num = A.nu_face[((size_t)cell * 6 + f) * n2 + p];
-        double nup = num, Hp = Hm;
-        double ihp[3] = {ih[0], ih[1], ih[2]};
+        const R sgn = s ? R(1.0) : -R(1.0);
+        const R num = A.nu_face[((size_t)cell * 6 + f) * n2 + p];
+        R nup = num, Hp = Hm;
+        R ihp[3] = {ih[0], ih[1], ih[2]};
         if (inter) {
-          const double* cg = A.cart + (size_t)nbv * CART_STRIDE;
+          const R* cg = A.cart + (size_t)nbv * CART_STRIDE;
           ihp[0] = cg[0]; ihp[1] = cg[1]; ihp[2] = cg[2]; Hp = cg[3];
           nup = A.nu_face[((size_t)nbv * 6 + (f ^ 1)) * n2 + p];
         }
-        const double dA = T.w[a] * T.w[b] * vol * ih[d];
-        const double tau = A.pen * fmax(Hm, Hp) * 0.5 * (num + nup);
-        double Sm[NC], Sp[NC];
+        const R dA = R(T.w[a]) * R(T.w[b]) * vol * ih[d];
+        const R tau = R(A.pen) * fmax(Hm, Hp) * R(0.5) * (num + nup);
+        R Sm[NC], Sp[NC];
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
-          const double gnm = dm[s][c] * ih[d], gnp = dp[s][c] * ihp[d];
+          const R gnm = dm[s][c] * ih[d], gnp = dp[s][c] * ihp[d];
           if constexpr (FORM == 0) {
             if (c == d) { Sm[c] = gnm; Sp[c] = gnp; }
             else {
               const bool c_is_t1 = (c == t1);
-              const double gtm = (c_is_t1 ? tm1[0] : tm2[0]) * ih[c];
-              const double gtp = (c_is_t1 ? tp1[0] : tp2[0]) * ihp[c];
-              Sm[c] = 0.5 * (gnm + gtm);
-              Sp[c] = 0.5 * (gnp + gtp);
+              const R gtm = (c_is_t1 ? tm1[0] : tm2[0]) * ih[c];
+              const R gtp = (c_is_t1 ? tp1[0] : tp2[0]) * ihp[c];
+              Sm[c] = R(0.5) * (gnm + gtm);
+              Sp[c] = R(0.5) * (gnp + gtp);
             }
           } else {
-            Sm[c] = 0.5 * gnm;
-            Sp[c] = 0.5 * gnp;
+            Sm[c] = R(0.5) * gnm;
+            Sp[c] = R(0.5) * gnp;
           }
         }
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
-          const double jmp = um[s][c] - up[s][c];
-          const double sbn = sgn * (num * Sm[c] + nup * Sp[c]);
-          const double pv = (FORM == 0 && c == d) ? 2.0 * jmp : jmp;
+          const R jmp = um[s][c] - up[s][c];
+          const R sbn = sgn * (num * Sm[c] + nup * Sp[c]);
+          const R pv = (FORM == 0 && c == d) ? R(2.0) * jmp : jmp;
           fv[s][c] = dA * (-sbn + tau * pv);
-          const double Gcd = (FORM == 0 && c == d) ? -num * jmp * sgn : -0.5 * num * jmp * sgn;
+          const R Gcd = (FORM == 0 && c == d) ? -num * jmp * sgn : -R(0.5) * num * jmp * sgn;
           gn[s][c] = dA * Gcd * ih[d];
         }
         if constexpr (NT > 0) {
-          gt1[0] = dA * (-0.5 * num * (um[s][t1] - up[s][t1]) * sgn) * ih[t1];
-          gt2[0] = dA * (-0.5 * num * (um[s][t2] - up[s][t2]) * sgn) * ih[t2];
+          gt1[0] = dA * (-R(0.5) * num * (um[s][t1] - up[s][t1]) * sgn) * ih[t1];
+          gt2[0] = dA * (-R(0.5) * num * (um[s][t2] - up[s][t2]) * sgn) * ih[t2];
         }
       } else {
         // ---------------- general geometry: own / neighbour J^-1 at the face point
@@ -489,36 +501,36 @@ sipg_apply2_kernel(const ApplyArgs A) {
         // to be formed:  (G n)_c = gx[c].v,  (G^T n)_c = sum_k (n.gx[.][k]) Ji[k][c],  and the
         // test-side coefficients of d v_c / d xi_k are -1/2 w (jmp_c v_k + n_c (J^-1 jmp)_k)
         // (divergence form) or -1/2 w jmp_c v_k (Laplace form).
-        const double sgn = s ? 1.0 : -1.0;
-        double nrm[3];
+        const R sgn = s ? R(1.0) : -R(1.0);
+        R nrm[3];
         {
-          const double v0 = Jim[3 * d], v1 = Jim[3 * d + 1], v2 = Jim[3 * d + 2];
-          const double il = sgn * rsqrt(v0 * v0 + v1 * v1 + v2 * v2);
+          const R v0 = Jim[3 * d], v1 = Jim[3 * d + 1], v2 = Jim[3 * d + 2];
+          const R il = sgn * rsqrt(v0 * v0 + v1 * v1 + v2 * v2);
           nrm[0] = v0 * il; nrm[1] = v1 * il; nrm[2] = v2 * il;
         }
-        auto sigma_n = [&](const double (&Ji)[9], const double* gd, const double* g1, const double* g2,
-                           double (&v)[3], double (&out)[NC]) {
+        auto sigma_n = [&](const R (&Ji)[9], const R* gd, const R* g1, const R* g2,
+                           R (&v)[3], R (&out)[NC]) {
 #pragma unroll
           for (int k = 0; k < 3; ++k) v[k] = Ji[3 * k] * nrm[0] + Ji[3 * k + 1] * nrm[1] + Ji[3 * k + 2] * nrm[2];
-          double gx[NC][3];
+          R gx[NC][3];
 #pragma unroll
           for (int c = 0; c < NC; ++c) { gx[c][d] = gd[c]; gx[c][t1] = g1[c]; gx[c][t2] = g2[c]; }
 #pragma unroll
           for (int c = 0; c < NC; ++c) out[c] = gx[c][0] * v[0] + gx[c][1] * v[1] + gx[c][2] * v[2];
           if constexpr (FORM == 0) {
-            double w[3];
+            R w[3];
 #pragma unroll
             for (int k = 0; k < 3; ++k) w[k] = nrm[0] * gx[0][k] + nrm[1] * gx[1][k] + nrm[2] * gx[2][k];
 #pragma unroll
-            for (int c = 0; c < NC; ++c) out[c] = 0.5 * (out[c] + w[0] * Ji[c] + w[1] * Ji[3 + c] + w[2] * Ji[6 + c]);
+            for (int c = 0; c < NC; ++c) out[c] = R(0.5) * (out[c] + w[0] * Ji[c] + w[1] * Ji[3 + c] + w[2] * Ji[6 + c]);
           } else {
 #pragma unroll
-            for (int c = 0; c < NC; ++c) out[c] *= 0.5;
+            for (int c = 0; c < NC; ++c) out[c] *= R(0.5);
           }
         };
-        double spn[NC], smn[NC], vm[3];
+        R spn[NC], smn[NC], vm[3];
         if (inter) {
-          double vp[3];
+          R vp[3];
           sigma_n(Jip, dp[s], tp1, tp2, vp, spn);
         }
         sigma_n(Jim, dm[s], tm1, tm2, vm, smn);
@@ -526,23 +538,23 @@ sipg_apply2_kernel(const ApplyArgs A) {
 #pragma unroll
           for (int c = 0; c < NC; ++c) spn[c] = smn[c];
         }
-        const double tau = A.pen * fmax(Hm, Hp) * 0.5 * (wm + wp);
-        double jmp[NC], jn = 0.0;
+        const R tau = R(A.pen) * fmax(Hm, Hp) * R(0.5) * (wm + wp);
+        R jmp[NC], jn = R(0.0);
 #pragma unroll
         for (int c = 0; c < NC; ++c) jmp[c] = um[s][c] - up[s][c];
-        double q[3] = {0.0, 0.0, 0.0};
+        R q[3] = {R(0.0), R(0.0), R(0.0)};
         if constexpr (FORM == 0) {
 #pragma unroll
           for (int c = 0; c < NC; ++c) jn += jmp[c] * nrm[c];
 #pragma unroll
           for (int k = 0; k < 3; ++k) q[k] = Jim[3 * k] * jmp[0] + Jim[3 * k + 1] * jmp[1] + Jim[3 * k + 2] * jmp[2];
         }
-        const double hw = -0.5 * wm;
+        const R hw = -R(0.5) * wm;
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
-          const double pv = (FORM == 0) ? (jmp[c] + nrm[c] * jn) : jmp[c];
+          const R pv = (FORM == 0) ? (jmp[c] + nrm[c] * jn) : jmp[c];
           fv[s][c] = -(wm * smn[c] + wp * spn[c]) + tau * pv;
-          double gk[3];
+          R gk[3];
 #pragma unroll
           for (int k = 0; k < 3; ++k) gk[k] = (FORM == 0) ? hw * (jmp[c] * vm[k] + nrm[c] * q[k]) : hw * jmp[c] * vm[k];
           gn[s][c] = gk[d];
@@ -552,17 +564,17 @@ sipg_apply2_kernel(const ApplyArgs A) {
       }
       if (!act) {
 #pragma unroll
-        for (int c = 0; c < NC; ++c) { fv[s][c] = 0.0; gn[s][c] = 0.0; }
+        for (int c = 0; c < NC; ++c) { fv[s][c] = R(0.0); gn[s][c] = R(0.0); }
         if constexpr (NT > 0) {
 #pragma unroll
-          for (int t = 0; t < NT; ++t) { gt1[t] = 0.0; gt2[t] = 0.0; }
+          for (int t = 0; t < NT; ++t) { gt1[t] = R(0.0); gt2[t] = R(0.0); }
         }
       }
       if constexpr (NT > 0) {
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
-          R[VOL + ((s * 4 + 2) * NT + t) * FA + b * RS + a] = gt1[t];
-          R[VOL + ((s * 4 + 3) * NT + t) * FA + a * RS + b] = gt2[t];
+          WK[VOL + ((s * 4 + 2) * NT + t) * FA + b * RS + a] = gt1[t];
+          WK[VOL + ((s * 4 + 3) * NT + t) * FA + a * RS + b] = gt2[t];
         }
       }
     }
@@ -572,7 +584,7 @@ sipg_apply2_kernel(const ApplyArgs A) {
       if constexpr (Cf::TMA) {
         if (dd < 2 && p == 0) stage_issue(dd == 0 ? 0 : 1, nbf);   // stage is free: next direction
       }
-      double DTa[n], DTb[n];
+      R DTa[n], DTb[n];
       ld_row<n>(sDT + a * RS, DTa);
       ld_row<n>(sDT + b * RS, DTb);
 #pragma unroll
@@ -580,8 +592,8 @@ sipg_apply2_kernel(const ApplyArgs A) {
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
           const int c = (GEO == 1) ? t : d;
-          fv[s][c] += rowdot<n>(R + VOL + ((s * 4 + 2) * NT + t) * FA + b * RS, DTa) +
-                      rowdot<n>(R + VOL + ((s * 4 + 3) * NT + t) * FA + a * RS, DTb);
+          fv[s][c] += rowdot<n>(WK + VOL + ((s * 4 + 2) * NT + t) * FA + b * RS, DTa) +
+                      rowdot<n>(WK + VOL + ((s * 4 + 3) * NT + t) * FA + a * RS, DTb);
         }
     }
 
@@ -589,15 +601,15 @@ sipg_apply2_kernel(const ApplyArgs A) {
     if (NT == 0 && d == 1) __syncthreads();   // x-fold reads of Y are complete
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
-      double add[n];
+      R add[n];
 #pragma unroll
       for (int i = 0; i < n; ++i)
-        add[i] = T.l0[i] * fv[0][c] + T.d0[i] * gn[0][c] + T.l1[i] * fv[1][c] + T.d1[i] * gn[1][c];
+        add[i] = R(T.l0[i]) * fv[0][c] + R(T.d0[i]) * gn[0][c] + R(T.l1[i]) * fv[1][c] + R(T.d1[i]) * gn[1][c];
       if (d == 2) {
 #pragma unroll
         for (int i = 0; i < n; ++i) y[c][i] += add[i];
       } else {
-        st_row<n>(R + c * CST + b * PS + a * RS, add);
+        st_row<n>(WK + c * CST + b * PS + a * RS, add);
       }
     }
     if (d != 2) {
@@ -606,7 +618,7 @@ sipg_apply2_kernel(const ApplyArgs A) {
       for (int c = 0; c < NC; ++c)
 #pragma unroll
         for (int z = 0; z < n; ++z)
-          y[c][z] += (d == 0) ? R[c * CST + z * PS + b * RS + a] : R[c * CST + z * PS + a * RS + b];
+          y[c][z] += (d == 0) ? WK[c * CST + z * PS + b * RS + a] : WK[c * CST + z * PS + a * RS + b];
     }
   }
 
@@ -623,9 +635,9 @@ sipg_apply2_kernel(const ApplyArgs A) {
         } else if (A.mode == MODE_RESID) {
           A.dst[i] = __ldg(A.b + i) - y[c][z];
         } else {
-          const double r = __ldg(A.b + i) - y[c][z];
-          double dn = A.c_r * __ldg(A.dinv + i) * r;
-          if (A.c_rho != 0.0) dn += A.c_rho * A.dvec[i];
+          const R r = __ldg(A.b + i) - y[c][z];
+          R dn = R(A.c_r) * __ldg(A.dinv + i) * r;
+          if (R(A.c_rho) != R(0.0)) dn += R(A.c_rho) * A.dvec[i];
           A.dvec[i] = dn;
           A.xout[i] = su[c * CST + z * PS + b * RS + a] + dn;
         }
