@@ -145,14 +145,15 @@ dgvv_status dgvv_apply_poisson(dgvv_ctx* ctx, int32_t level, const double* src, 
  * default) gives the plain operator.  DGVV_EDOMAIN for mass < 0 or non-finite. */
 dgvv_status dgvv_set_mass(dgvv_ctx* ctx, int32_t op, double mass);
 
-enum { DGVV_PRECOND_NONE = 0, DGVV_PRECOND_JACOBI = 1, DGVV_PRECOND_VCYCLE = 2 };
+enum { DGVV_PRECOND_NONE = 0, DGVV_PRECOND_JACOBI = 1, DGVV_PRECOND_VCYCLE = 2, DGVV_PRECOND_VCYCLE_FP32 = 3 };
 
 /* Preconditioned conjugate gradients on (mass M +) A_op, level 0 (the Krylov solver of the
  * symmetric viscous and pressure steps):
  *   r = b - A x; z = P r; p = z;  repeat q = A p, alpha = (r,z)/(p,q), x += alpha p,
  *   r -= alpha q, stop when ||r|| <= rtol ||b||, z = P r, p = z + beta p.
  * x is the initial guess on entry, the solution on return.  P = identity, inverse diagonal
- * (Jacobi) or one V-cycle (dgvv_vcycle, lambda_hi_per_level required).  Synchronous (one host
+ * (Jacobi), one V-cycle (dgvv_vcycle) or one FP32 V-cycle (dgvv_vcycle_fp32); the V-cycles need
+ * lambda_hi_per_level.  Synchronous (one host
  * read per dot product); *iters and *relres = ||r||/||b|| returned.  Work vectors are owned
  * by the library.  Multi-GPU: every rank calls collectively; dots are allreduced. */
 dgvv_status dgvv_cg_solve(dgvv_ctx* ctx, int32_t op, const double* b, double* x, double rtol,
@@ -162,6 +163,15 @@ dgvv_status dgvv_cg_solve(dgvv_ctx* ctx, int32_t op, const double* b, double* x,
 /* dst = 1 / diag(A) for op = DGVV_OP_* on `level`. */
 dgvv_status dgvv_inverse_diagonal(dgvv_ctx* ctx, int32_t op, int32_t level, double* dst,
                                   dgvv_stream stream);
+
+/* x = V(b) with every multigrid level (smoother applies, Chebyshev updates, transfers,
+ * coefficients, inverse diagonals) in single precision — the paper's choice for the
+ * preconditioner; b and x are FP64 and converted at
+ * entry and exit.  Same algorithm as dgvv_vcycle; FP32 mirrors of the level data are built on
+ * first use and refreshed after dgvv_update_viscosity / dgvv_set_mass.  Single-GPU contexts
+ * only in this build (DGVV_EUNSUPPORTED with ghosts). */
+dgvv_status dgvv_vcycle_fp32(dgvv_ctx* ctx, int32_t op, const double* b, double* x,
+                             const double* lambda_hi_per_level, dgvv_stream stream);
 
 /* lambda_max(D^-1 A) estimate (reading G12): `steps` Lanczos steps on D^-1/2 A D^-1/2 from
  * the caller's start vector v0 (device, level layout; random inputs are generated by the

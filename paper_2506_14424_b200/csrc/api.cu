@@ -128,6 +128,20 @@ struct Level {
   std::vector<double*> scratch[2];         // V-cycle scratch per op
 };
 
+// FP32 mirror of a level for the single-precision multigrid preconditioner (PAPER.md:1546-1551,
+// SURVEY §8(f) f1): coefficient/geometry arrays converted from the FP64 level, per-op epochs.
+struct LevelF {
+  float* nu_cell[2] = {nullptr, nullptr};   // per op: raw (Cartesian) or premultiplied (general)
+  float* nu_face[2] = {nullptr, nullptr};
+  float* dinv[2] = {nullptr, nullptr};
+  int epoch[2] = {-1, -1};
+  float* vJi = nullptr;
+  float* fJi = nullptr;
+  float* Hc = nullptr;
+  float* jxw = nullptr;
+  std::vector<float*> scratch[2];           // [0] r, [1] work (2N), [3] b, [4] x
+};
+
 struct Peer {
   int rank;
   int* d_send = nullptr;      // owned local cells to send (sorted by global id)
@@ -150,6 +164,9 @@ struct dgvv_ctx {
   double ip = 1.0;
   double mass[2] = {0.0, 0.0};  // Helmholtz mass coefficient per op (dgvv_set_mass)
   double* cg_work[2] = {nullptr, nullptr};   // CG vectors r, z, p, q per op (level 0)
+  std::vector<LevelF> LF;                    // FP32 levels (lazily built)
+  float* d_cart_f = nullptr;
+  int coef_epoch = 0;                        // bumped whenever coefficients or the mass change
   const double* ulin = nullptr;
   // comm: peers exist whenever there are ghosts; NCCL transport only with a communicator
   // (without one the caller fills the ghost buffers: external-exchange mode, used by tests)
@@ -820,6 +837,7 @@ dgvv_status dgvv_update_viscosity(dgvv_ctx* c, const double* u_lin, dgvv_stream 
   }
   c->ulin = u_lin;
   c->nu_ready = true;
+  ++c->coef_epoch;
   return DGVV_OK;
 }
 
@@ -965,6 +983,7 @@ dgvv_status dgvv_set_mass(dgvv_ctx* c, int32_t op, double mass) {
   if (!std::isfinite(mass) || mass < 0.0) return dgvv_fail(DGVV_EDOMAIN, "mass coefficient %g must be finite and >= 0", mass);
   if (c->mass[op] == mass) return DGVV_OK;
   c->mass[op] = mass;
+  ++c->coef_epoch;
   for (auto& L : c->L)                 // the diagonal changes: recompute lazily
     if (L.dinv[op]) {
       cudaFree(L.dinv[op]);
@@ -1081,6 +1100,170 @@ static dgvv_status vcycle_rec(dgvv_ctx* c, int op, int l, const double* b, doubl
   return DGVV_OK;
 }
 
+// ------------------------------------------------------------------ FP32 multigrid (f1)
+static dgvv_status d2f_alloc(dgvv_ctx* c, float** dst, const double* src, long n, cudaStream_t s) {
+  if (!*dst) TRY(dalloc(c, dst, (size_t)n));
+  DGVV_CUDA_TRY(launch_d2f(src, *dst, n, s));
+  return DGVV_OK;
+}
+
+static dgvv_status ensure_fp32(dgvv_ctx* c, int op, cudaStream_t s) {
+  if (!c->peers.empty()) return dgvv_fail(DGVV_EUNSUPPORTED, "FP32 multigrid: single-GPU contexts only (this build)");
+  const int oi = op == DGVV_OP_VISCOUS ? 0 : 1;
+  const int nc = op == DGVV_OP_VISCOUS ? 3 : 1;
+  if (c->LF.size() != c->L.size()) c->LF.resize(c->L.size());
+  if (c->geo == 0 && !c->d_cart_f) TRY(d2f_alloc(c, &c->d_cart_f, c->d_cart, (long)c->n_total * CART_STRIDE, s));
+  for (size_t l = 0; l < c->L.size(); ++l) {
+    Level& L = c->L[l];
+    LevelF& F = c->LF[l];
+    const long n3 = (long)L.n * L.n * L.n, n2 = (long)L.n * L.n;
+    if (c->geo == 1 && !F.vJi) {
+      TRY(d2f_alloc(c, &F.vJi, L.vJi, (long)c->n_total * 9 * n3, s));
+      TRY(d2f_alloc(c, &F.fJi, L.fJi, (long)c->n_total * 6 * 9 * n2, s));
+      TRY(d2f_alloc(c, &F.Hc, L.Hc, (long)c->n_total, s));
+      TRY(d2f_alloc(c, &F.jxw, L.jxw, (long)c->n_owned * n3, s));
+    }
+    if (F.epoch[oi] != c->coef_epoch) {
+      const double* nuc = c->geo == 0 ? (oi == 0 ? L.nu_cell : L.c_cell) : (oi == 0 ? L.wv_cell : L.wc_cell);
+      const double* nuf = c->geo == 0 ? (oi == 0 ? L.nu_face : L.c_face) : (oi == 0 ? L.wv_face : L.wc_face);
+      TRY(d2f_alloc(c, &F.nu_cell[oi], nuc, (long)c->n_owned * n3, s));
+      TRY(d2f_alloc(c, &F.nu_face[oi], nuf, (long)c->n_total * 6 * n2, s));
+      TRY(ensure_dinv(c, op, (int)l, s));
+      TRY(d2f_alloc(c, &F.dinv[oi], L.dinv[oi], (long)nc * c->n_owned * n3, s));
+      F.epoch[oi] = c->coef_epoch;
+    }
+    auto& S = F.scratch[oi];
+    if (S.empty()) {
+      const size_t N = (size_t)nc * c->n_owned * n3;
+      S.resize(5, nullptr);
+      TRY(dalloc(c, &S[0], N));
+      TRY(dalloc(c, &S[1], 2 * N));
+      S[2] = S[1] + N;
+      TRY(dalloc(c, &S[3], N));
+      TRY(dalloc(c, &S[4], N));
+    }
+  }
+  return DGVV_OK;
+}
+
+static ApplyArgsT<float> base_args_f(dgvv_ctx* c, int l, int op) {
+  ApplyArgsT<float> a;
+  std::memset(&a, 0, sizeof(a));
+  const int oi = op == DGVV_OP_VISCOUS ? 0 : 1;
+  LevelF& F = c->LF[l];
+  a.nbr = c->d_nbr;
+  a.n_proc = c->n_owned;
+  a.n_owned = c->n_owned;
+  a.nu_cell = F.nu_cell[oi];
+  a.nu_face = F.nu_face[oi];
+  a.cart = c->d_cart_f;
+  a.vJi = F.vJi;
+  a.fJi = F.fJi;
+  a.jxw = F.jxw;
+  a.Hcell = F.Hc;
+  a.pen = c->ip * (double)(c->L[l].k + 1) * (double)(c->L[l].k + 1);
+  a.mass = c->mass[oi];
+  a.mode = MODE_APPLY;
+  return a;
+}
+
+static dgvv_status run_apply_f(dgvv_ctx* c, int op, int l, const ApplyArgsT<float>& a, cudaStream_t s) {
+  const int nc = op == DGVV_OP_VISCOUS ? 3 : 1;
+  const int form = op == DGVV_OP_VISCOUS ? c->form : DGVV_FORM_LAPLACE;
+  cudaError_t e = launch_apply_f(nc, c->L[l].n, form, c->geo, a, s);
+  if (e != cudaSuccess) return dgvv_fail(DGVV_ECUDA, "FP32 apply kernel: %s", cudaGetErrorString(e));
+  return DGVV_OK;
+}
+
+static dgvv_status cheb_impl_f(dgvv_ctx* c, int op, int l, float* x, const float* b, int degree, double lo,
+                               double hi, int x_is_zero, float* work, cudaStream_t s) {
+  const int oi = op == DGVV_OP_VISCOUS ? 0 : 1;
+  const int nc = op == DGVV_OP_VISCOUS ? 3 : 1;
+  const long N = (long)nc * level_dofs(c, l);
+  const float* dinv = c->LF[l].dinv[oi];
+  const double theta = 0.5 * (hi + lo), delta = 0.5 * (hi - lo), sigma = theta / delta;
+  double rho = 1.0 / sigma;
+  float* bufs[2] = {x, work};
+  float* d = work + N;
+  int cur;
+  if (x_is_zero) {
+    DGVV_CUDA_TRY(launch_cheb_first_f(b, dinv, 1.0 / theta, d, x, N, s));
+    cur = 0;
+  } else {
+    ApplyArgsT<float> a = base_args_f(c, l, op);
+    a.src = x; a.b = b; a.dinv = dinv; a.dvec = d; a.xout = work;
+    a.mode = MODE_CHEB; a.c_rho = 0.0; a.c_r = 1.0 / theta;
+    TRY(run_apply_f(c, op, l, a, s));
+    cur = 1;
+  }
+  for (int j = 1; j < degree; ++j) {
+    const double rho_new = 1.0 / (2.0 * sigma - rho);
+    ApplyArgsT<float> a = base_args_f(c, l, op);
+    a.src = bufs[cur]; a.b = b; a.dinv = dinv; a.dvec = d; a.xout = bufs[1 - cur];
+    a.mode = MODE_CHEB; a.c_rho = rho_new * rho; a.c_r = 2.0 * rho_new / delta;
+    TRY(run_apply_f(c, op, l, a, s));
+    cur = 1 - cur;
+    rho = rho_new;
+  }
+  if (cur != 0) DGVV_CUDA_TRY(cudaMemcpyAsync(x, work, N * sizeof(float), cudaMemcpyDeviceToDevice, s));
+  return DGVV_OK;
+}
+
+static dgvv_status transfer_f(dgvv_ctx* c, int op, int fl, const float* in, float* out, double beta, bool prol,
+                              cudaStream_t s) {
+  const int nc = op == DGVV_OP_VISCOUS ? 3 : 1;
+  const int nf = c->L[fl].n, ncs = c->L[fl + 1].n;
+  std::vector<double> P1((size_t)nf * ncs), M((size_t)nf * ncs);
+  transfer_matrix(nf, ncs, P1.data());
+  if (prol) {
+    DGVV_CUDA_TRY(launch_tensor3_f(ncs, nf, nc, P1.data(), in, out, beta, c->n_owned, s));
+  } else {
+    for (int i = 0; i < nf; ++i)
+      for (int j = 0; j < ncs; ++j) M[(size_t)j * nf + i] = P1[(size_t)i * ncs + j];
+    DGVV_CUDA_TRY(launch_tensor3_f(nf, ncs, nc, M.data(), in, out, beta, c->n_owned, s));
+  }
+  return DGVV_OK;
+}
+
+// the V-cycle of vcycle_rec with every level in FP32
+static dgvv_status vcycle_rec_f(dgvv_ctx* c, int op, int l, const float* b, float* x, const double* his,
+                                cudaStream_t s) {
+  const int oi = op == DGVV_OP_VISCOUS ? 0 : 1;
+  auto& S = c->LF[l].scratch[oi];
+  const double hi = his[l], lo = hi / 20.0;
+  const int last = (int)c->L.size() - 1;
+  TRY(cheb_impl_f(c, op, l, x, b, 5, lo, hi, 1, S[1], s));
+  if (l == last) return DGVV_OK;
+  ApplyArgsT<float> a = base_args_f(c, l, op);
+  a.src = x; a.dst = S[0]; a.b = b; a.mode = MODE_RESID;
+  TRY(run_apply_f(c, op, l, a, s));
+  auto& C = c->LF[l + 1].scratch[oi];
+  TRY(transfer_f(c, op, l, S[0], C[3], 0.0, false, s));
+  TRY(vcycle_rec_f(c, op, l + 1, C[3], C[4], his, s));
+  TRY(transfer_f(c, op, l, C[4], x, 1.0, true, s));
+  TRY(cheb_impl_f(c, op, l, x, b, 5, lo, hi, 0, S[1], s));
+  return DGVV_OK;
+}
+
+// z = V_fp32(r) for FP64 vectors (conversion in and out)
+static dgvv_status vcycle_fp32_d(dgvv_ctx* c, int op, const double* r, double* z, const double* his, cudaStream_t s) {
+  TRY(ensure_fp32(c, op, s));
+  const int oi = op == DGVV_OP_VISCOUS ? 0 : 1;
+  const long N = (long)(op == DGVV_OP_VISCOUS ? 3 : 1) * level_dofs(c, 0);
+  auto& S = c->LF[0].scratch[oi];
+  DGVV_CUDA_TRY(launch_d2f(r, S[3], N, s));
+  TRY(vcycle_rec_f(c, op, 0, S[3], S[4], his, s));
+  DGVV_CUDA_TRY(launch_f2d(S[4], z, N, s));
+  return DGVV_OK;
+}
+
+dgvv_status dgvv_vcycle_fp32(dgvv_ctx* c, int32_t op, const double* b, double* x, const double* his,
+                             dgvv_stream stream) {
+  if (!c || !b || !x || !his) return dgvv_fail(DGVV_EINVAL, "null argument");
+  TRY(op_ready(c, op));
+  return vcycle_fp32_d(c, op, b, x, his, (cudaStream_t)stream);
+}
+
 dgvv_status dgvv_vcycle(dgvv_ctx* c, int32_t op, const double* b, double* x, const double* his,
                         dgvv_stream stream) {
   if (!c || !b || !x || !his) return dgvv_fail(DGVV_EINVAL, "null argument");
@@ -1116,9 +1299,9 @@ dgvv_status dgvv_cg_solve(dgvv_ctx* c, int32_t op, const double* b, double* x, d
   TRY(op_ready(c, op));
   if (b == x) return dgvv_fail(DGVV_EINVAL, "b and x alias");
   if (!(rtol >= 0.0) || maxit < 0) return dgvv_fail(DGVV_EINVAL, "rtol >= 0 and maxit >= 0 required");
-  if (precond < DGVV_PRECOND_NONE || precond > DGVV_PRECOND_VCYCLE)
+  if (precond < DGVV_PRECOND_NONE || precond > DGVV_PRECOND_VCYCLE_FP32)
     return dgvv_fail(DGVV_EINVAL, "unknown preconditioner %d", precond);
-  if (precond == DGVV_PRECOND_VCYCLE && !lambda_hi_per_level)
+  if ((precond == DGVV_PRECOND_VCYCLE || precond == DGVV_PRECOND_VCYCLE_FP32) && !lambda_hi_per_level)
     return dgvv_fail(DGVV_EINVAL, "V-cycle preconditioner needs lambda_hi_per_level");
   cudaStream_t s = (cudaStream_t)stream;
   const int oi = op == DGVV_OP_VISCOUS ? 0 : 1;
@@ -1152,6 +1335,8 @@ dgvv_status dgvv_cg_solve(dgvv_ctx* c, int32_t op, const double* b, double* x, d
       DGVV_CUDA_TRY(launch_ew_mul(c->L[0].dinv[oi], rr, zz, N, s));
     } else if (precond == DGVV_PRECOND_VCYCLE) {
       TRY(vcycle_rec(c, op, 0, rr, zz, lambda_hi_per_level, s));
+    } else if (precond == DGVV_PRECOND_VCYCLE_FP32) {
+      TRY(vcycle_fp32_d(c, op, rr, zz, lambda_hi_per_level, s));
     } else {
       DGVV_CUDA_TRY(cudaMemcpyAsync(zz, rr, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
     }

@@ -236,47 +236,47 @@ __global__ void diag_kernel(const DiagArgs A) {
 // prolongation: M = P1 (nf x nc); restriction: M = P1^T; u_lin interpolation: M = I1.
 struct Mat8 { double m[DGVV_NMAX * DGVV_NMAX]; };
 
-template <int nin, int nout, int NC, int CPB>
-__global__ void __launch_bounds__(CPB * 64) tensor3_kernel(Mat8 M, const double* in, double* out,
-                                                             double beta, int n_cells) {
+template <typename R, int nin, int nout, int NC, int CPB>
+__global__ void __launch_bounds__(CPB * 64) tensor3_kernel(Mat8 M, const R* in, R* out, R beta, int n_cells) {
   constexpr int ni3 = nin * nin * nin, no3 = nout * nout * nout;
   constexpr int S1 = nin * nin * nout, S2 = nin * nout * nout;
   constexpr int CS = ni3 + S1 + S2;
-  extern __shared__ double smem[];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  R* smem = reinterpret_cast<R*>(smem_raw);
   const int lc = threadIdx.x / 64, t = threadIdx.x % 64;
   const int cell = blockIdx.x * CPB + lc;
   const bool active = cell < n_cells;
-  double* sin_ = smem + lc * CS;
-  double* s1 = sin_ + ni3;
-  double* s2 = s1 + S1;
+  R* sin_ = smem + lc * CS;
+  R* s1 = sin_ + ni3;
+  R* s2 = s1 + S1;
   for (int c = 0; c < NC; ++c) {
     if (active)
       for (int i = t; i < ni3; i += 64) sin_[i] = in[((size_t)cell * NC + c) * ni3 + i];
     __syncthreads();
     for (int i = t; i < S1; i += 64) {           // [z_i][y_i][x_o]
       const int xo = i % nout, r = i / nout;
-      double acc = 0.0;
+      R acc = R(0);
 #pragma unroll
-      for (int k = 0; k < nin; ++k) acc += M.m[xo * nin + k] * sin_[r * nin + k];
+      for (int k = 0; k < nin; ++k) acc += R(M.m[xo * nin + k]) * sin_[r * nin + k];
       s1[i] = acc;
     }
     __syncthreads();
     for (int i = t; i < S2; i += 64) {           // [z_i][y_o][x_o]
       const int xo = i % nout, yo = (i / nout) % nout, zi = i / (nout * nout);
-      double acc = 0.0;
+      R acc = R(0);
 #pragma unroll
-      for (int k = 0; k < nin; ++k) acc += M.m[yo * nin + k] * s1[(zi * nin + k) * nout + xo];
+      for (int k = 0; k < nin; ++k) acc += R(M.m[yo * nin + k]) * s1[(zi * nin + k) * nout + xo];
       s2[i] = acc;
     }
     __syncthreads();
     if (active)
       for (int i = t; i < no3; i += 64) {        // [z_o][y_o][x_o]
         const int r = i % (nout * nout), zo = i / (nout * nout);
-        double acc = 0.0;
+        R acc = R(0);
 #pragma unroll
-        for (int k = 0; k < nin; ++k) acc += M.m[zo * nin + k] * s2[k * nout * nout + r];
+        for (int k = 0; k < nin; ++k) acc += R(M.m[zo * nin + k]) * s2[k * nout * nout + r];
         const size_t o = ((size_t)cell * NC + c) * no3 + i;
-        out[o] = (beta == 0.0) ? acc : acc + beta * out[o];
+        out[o] = (beta == R(0)) ? acc : acc + beta * out[o];
       }
     __syncthreads();
   }
@@ -312,13 +312,22 @@ __global__ void sum_partials_kernel(const double* part, int np, double* out) {
 }
 
 // Chebyshev iteration 0 from x0 = 0: r0 = b, d0 = D^-1 b / theta, x1 = d0
-__global__ void cheb_first_kernel(const double* b, const double* dinv, double c_r, double* d,
-                                  double* x, long n) {
+template <typename R>
+__global__ void cheb_first_kernel(const R* b, const R* dinv, R c_r, R* d, R* x, long n) {
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
-    const double v = c_r * dinv[i] * b[i];
+    const R v = c_r * dinv[i] * b[i];
     d[i] = v;
     x[i] = v;
   }
+}
+// precision conversions for the FP32 multigrid preconditioner
+__global__ void d2f_kernel(const double* a, float* out, long n) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+    out[i] = (float)a[i];
+}
+__global__ void f2d_kernel(const float* a, double* out, long n) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+    out[i] = (double)a[i];
 }
 
 // out = a .* b

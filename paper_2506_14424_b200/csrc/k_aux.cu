@@ -71,47 +71,55 @@ cudaError_t launch_diag(int nc, int n, int form, int geo, const DiagArgs& a, cud
 }
 
 // ---------------------------------------------------------------- K7
-template <int nin, int nout>
-static cudaError_t t3_run(int nc, const Mat8& M, const double* in, double* out, double beta, int ncells,
-                          cudaStream_t s) {
+template <typename R, int nin, int nout>
+static cudaError_t t3_run(int nc, const Mat8& M, const R* in, R* out, double beta, int ncells, cudaStream_t s) {
   constexpr int CPB = 2;
   constexpr int CS = nin * nin * nin + nin * nin * nout + nin * nout * nout;
-  const size_t smem = (size_t)CPB * CS * sizeof(double);
+  const size_t smem = (size_t)CPB * CS * sizeof(R);
   if (ncells <= 0) return cudaSuccess;
   const int grid = (ncells + CPB - 1) / CPB;
-  if (nc == 3) tensor3_kernel<nin, nout, 3, CPB><<<grid, CPB * 64, smem, s>>>(M, in, out, beta, ncells);
-  else tensor3_kernel<nin, nout, 1, CPB><<<grid, CPB * 64, smem, s>>>(M, in, out, beta, ncells);
+  if (nc == 3) tensor3_kernel<R, nin, nout, 3, CPB><<<grid, CPB * 64, smem, s>>>(M, in, out, (R)beta, ncells);
+  else tensor3_kernel<R, nin, nout, 1, CPB><<<grid, CPB * 64, smem, s>>>(M, in, out, (R)beta, ncells);
   return cudaGetLastError();
 }
 
-template <int nin>
-static cudaError_t t3_in(int nout, int nc, const Mat8& M, const double* in, double* out, double beta,
-                         int ncells, cudaStream_t s) {
+template <typename R, int nin>
+static cudaError_t t3_in(int nout, int nc, const Mat8& M, const R* in, R* out, double beta, int ncells,
+                         cudaStream_t s) {
   switch (nout) {
-    case 2: return t3_run<nin, 2>(nc, M, in, out, beta, ncells, s);
-    case 3: return t3_run<nin, 3>(nc, M, in, out, beta, ncells, s);
-    case 4: return t3_run<nin, 4>(nc, M, in, out, beta, ncells, s);
-    case 5: return t3_run<nin, 5>(nc, M, in, out, beta, ncells, s);
-    case 6: return t3_run<nin, 6>(nc, M, in, out, beta, ncells, s);
-    case 7: return t3_run<nin, 7>(nc, M, in, out, beta, ncells, s);
+    case 2: return t3_run<R, nin, 2>(nc, M, in, out, beta, ncells, s);
+    case 3: return t3_run<R, nin, 3>(nc, M, in, out, beta, ncells, s);
+    case 4: return t3_run<R, nin, 4>(nc, M, in, out, beta, ncells, s);
+    case 5: return t3_run<R, nin, 5>(nc, M, in, out, beta, ncells, s);
+    case 6: return t3_run<R, nin, 6>(nc, M, in, out, beta, ncells, s);
+    case 7: return t3_run<R, nin, 7>(nc, M, in, out, beta, ncells, s);
     default: return cudaErrorInvalidValue;
   }
 }
 
-cudaError_t launch_tensor3(int nin, int nout, int nc, const double* M, const double* in, double* out,
-                           double beta, int ncells, cudaStream_t s) {
+template <typename R>
+static cudaError_t tensor3_t(int nin, int nout, int nc, const double* M, const R* in, R* out, double beta,
+                             int ncells, cudaStream_t s) {
   Mat8 m;
   for (int i = 0; i < DGVV_NMAX * DGVV_NMAX; ++i) m.m[i] = 0.0;
   for (int i = 0; i < nin * nout; ++i) m.m[i] = M[i];
   switch (nin) {
-    case 2: return t3_in<2>(nout, nc, m, in, out, beta, ncells, s);
-    case 3: return t3_in<3>(nout, nc, m, in, out, beta, ncells, s);
-    case 4: return t3_in<4>(nout, nc, m, in, out, beta, ncells, s);
-    case 5: return t3_in<5>(nout, nc, m, in, out, beta, ncells, s);
-    case 6: return t3_in<6>(nout, nc, m, in, out, beta, ncells, s);
-    case 7: return t3_in<7>(nout, nc, m, in, out, beta, ncells, s);
+    case 2: return t3_in<R, 2>(nout, nc, m, in, out, beta, ncells, s);
+    case 3: return t3_in<R, 3>(nout, nc, m, in, out, beta, ncells, s);
+    case 4: return t3_in<R, 4>(nout, nc, m, in, out, beta, ncells, s);
+    case 5: return t3_in<R, 5>(nout, nc, m, in, out, beta, ncells, s);
+    case 6: return t3_in<R, 6>(nout, nc, m, in, out, beta, ncells, s);
+    case 7: return t3_in<R, 7>(nout, nc, m, in, out, beta, ncells, s);
     default: return cudaErrorInvalidValue;
   }
+}
+cudaError_t launch_tensor3(int nin, int nout, int nc, const double* M, const double* in, double* out,
+                           double beta, int ncells, cudaStream_t s) {
+  return tensor3_t<double>(nin, nout, nc, M, in, out, beta, ncells, s);
+}
+cudaError_t launch_tensor3_f(int nin, int nout, int nc, const double* M, const float* in, float* out,
+                             double beta, int ncells, cudaStream_t s) {
+  return tensor3_t<float>(nin, nout, nc, M, in, out, beta, ncells, s);
 }
 
 // ---------------------------------------------------------------- setup
@@ -171,7 +179,20 @@ cudaError_t launch_dot(const double* a, const double* b, long n, double* part, i
 
 cudaError_t launch_cheb_first(const double* b, const double* dinv, double c_r, double* d, double* x, long n,
                               cudaStream_t s) {
-  cheb_first_kernel<<<gs_blocks(n), 256, 0, s>>>(b, dinv, c_r, d, x, n);
+  cheb_first_kernel<double><<<gs_blocks(n), 256, 0, s>>>(b, dinv, c_r, d, x, n);
+  return cudaGetLastError();
+}
+cudaError_t launch_cheb_first_f(const float* b, const float* dinv, double c_r, float* d, float* x, long n,
+                                cudaStream_t s) {
+  cheb_first_kernel<float><<<gs_blocks(n), 256, 0, s>>>(b, dinv, (float)c_r, d, x, n);
+  return cudaGetLastError();
+}
+cudaError_t launch_d2f(const double* a, float* out, long n, cudaStream_t s) {
+  d2f_kernel<<<gs_blocks(n), 256, 0, s>>>(a, out, n);
+  return cudaGetLastError();
+}
+cudaError_t launch_f2d(const float* a, double* out, long n, cudaStream_t s) {
+  f2d_kernel<<<gs_blocks(n), 256, 0, s>>>(a, out, n);
   return cudaGetLastError();
 }
 cudaError_t launch_ew_mul(const double* a, const double* b, double* out, long n, cudaStream_t s) {

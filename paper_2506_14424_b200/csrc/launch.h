@@ -25,6 +25,8 @@ cudaError_t launch_diag(int nc, int n, int form, int geo, const DiagArgs& a, cud
 // K7: out = (M x M x M) in + beta out
 cudaError_t launch_tensor3(int nin, int nout, int nc, const double* M, const double* in, double* out,
                            double beta, int ncells, cudaStream_t s);
+cudaError_t launch_tensor3_f(int nin, int nout, int nc, const double* M, const float* in, float* out,
+                             double beta, int ncells, cudaStream_t s);
 
 // setup kernels
 cudaError_t launch_cart_geom(const double* nodes, const int* nbr, int n_total, double* cart, cudaStream_t s);
@@ -45,6 +47,10 @@ cudaError_t launch_dot(const double* a, const double* b, long n, double* part, i
                        cudaStream_t s);
 cudaError_t launch_cheb_first(const double* b, const double* dinv, double c_r, double* d, double* x, long n,
                               cudaStream_t s);
+cudaError_t launch_cheb_first_f(const float* b, const float* dinv, double c_r, float* d, float* x, long n,
+                                cudaStream_t s);
+cudaError_t launch_d2f(const double* a, float* out, long n, cudaStream_t s);
+cudaError_t launch_f2d(const float* a, double* out, long n, cudaStream_t s);
 cudaError_t launch_ew_mul(const double* a, const double* b, double* out, long n, cudaStream_t s);
 cudaError_t launch_axpby(double alpha, const double* x, double beta, double* y, long n, cudaStream_t s);
 cudaError_t launch_ew_sqrt(const double* a, double* out, long n, cudaStream_t s);

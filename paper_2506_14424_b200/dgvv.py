@@ -184,9 +184,10 @@ class Context:
 
     def cg_solve(self, op, b, x, rtol=1e-8, maxit=200, precond="vcycle", lam_hi_per_level=None):
         """Preconditioned CG on level 0 (dgvv_cg_solve); x = initial guess in, solution out.
-        precond: "none", "jacobi" or "vcycle".  Returns (iterations, ||r|| / ||b||)."""
+        precond: "none", "jacobi", "vcycle" or "vcycle_fp32".  Returns (iterations, ||r|| / ||b||)."""
         n = self._n(op, 0)
-        pc = {"none": A.PRECOND_NONE, "jacobi": A.PRECOND_JACOBI, "vcycle": A.PRECOND_VCYCLE}[precond]
+        pc = {"none": A.PRECOND_NONE, "jacobi": A.PRECOND_JACOBI, "vcycle": A.PRECOND_VCYCLE,
+              "vcycle_fp32": A.PRECOND_VCYCLE_FP32}[precond]
         arr = None
         if lam_hi_per_level is not None:
             arr = (C.c_double * len(self.degrees))(*[float(v) for v in lam_hi_per_level])
@@ -194,6 +195,13 @@ class Context:
         A.check(self._L.dgvv_cg_solve(self.h, op, _ptr(b, n, "b"), _ptr(x, n, "x"), float(rtol), int(maxit), pc,
                                       arr, C.byref(it), C.byref(rr), _stream()))
         return it.value, rr.value
+
+    def vcycle_fp32(self, op, b, x, lam_hi_per_level):
+        """x = V(b) with all multigrid levels in FP32 (dgvv_vcycle_fp32); b, x FP64 device vectors."""
+        n = self._n(op, 0)
+        arr = (C.c_double * len(self.degrees))(*[float(v) for v in lam_hi_per_level])
+        A.check(self._L.dgvv_vcycle_fp32(self.h, op, _ptr(b, n, "b"), _ptr(x, n, "x"), arr, _stream()))
+        return x
 
     def dot(self, a, b, ncomp=1, level=0):
         out = C.c_double()
