@@ -40,16 +40,20 @@ static cudaError_t run(const ApplyArgsT<R>& a, cudaStream_t s) {
   constexpr int CPB = cpb_visc<n, GEO>();
   constexpr int NC = 3;
   const size_t smem = (size_t)CPB * Apply2Cfg<n, NC, FORM, GEO>::CS * sizeof(R);
-  auto k = sipg_apply2_kernel<R, n, NC, FORM, GEO, CPB, minb_visc<n, GEO>()>;
+  // the Helmholtz mass term is a separate instantiation: the plain operator pays nothing for it
+  auto k0 = sipg_apply2_kernel<R, n, NC, FORM, GEO, CPB, minb_visc<n, GEO>(), false>;
+  auto k1 = sipg_apply2_kernel<R, n, NC, FORM, GEO, CPB, minb_visc<n, GEO>(), true>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   if (a.n_proc <= 0) return cudaSuccess;
   const int grid = (a.n_proc + CPB - 1) / CPB;
-  k<<<grid, CPB * n * n, smem, s>>>(a);
+  if (a.mass != 0.0) k1<<<grid, CPB * n * n, smem, s>>>(a);
+  else k0<<<grid, CPB * n * n, smem, s>>>(a);
   return cudaGetLastError();
 }
 

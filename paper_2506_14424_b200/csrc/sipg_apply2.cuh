@@ -122,7 +122,7 @@ __device__ __forceinline__ R rowdot(const R* __restrict__ r, const R (&w)[n]) {
   return s;
 }
 
-template <typename R, int n, int NC, int FORM, int GEO, int CPB, int MINB>
+template <typename R, int n, int NC, int FORM, int GEO, int CPB, int MINB, bool MASS>
 __global__ void __launch_bounds__(CPB * n * n, MINB)
 sipg_apply2_kernel(const ApplyArgsT<R> A) {
   static_assert(FORM == 1 || NC == 3, "divergence form needs 3 components");
@@ -183,20 +183,13 @@ sipg_apply2_kernel(const ApplyArgsT<R> A) {
   R ucol[NC][n], y[NC][n];
   {
     const R* gsrc = A.src + (size_t)cell * NC * n3;
-    R mjw[n];                       // Helmholtz mass term: mass * JxW at the column points
-#pragma unroll
-    for (int z = 0; z < n; ++z) {
-      if (R(A.mass) == R(0.0)) mjw[z] = R(0.0);
-      else if constexpr (GEO == 0) mjw[z] = R(A.mass) * R(T.w[a]) * R(T.w[b]) * R(T.w[z]) * A.cart[(size_t)cell * CART_STRIDE + 4];
-      else mjw[z] = R(A.mass) * A.jxw[(size_t)cell * n3 + z * n2 + p];
-    }
 #pragma unroll
     for (int c = 0; c < NC; ++c)
 #pragma unroll
       for (int z = 0; z < n; ++z) {
         const R v = __ldg(gsrc + c * n3 + z * n2 + p);
         ucol[c][z] = v;
-        y[c][z] = mjw[z] * v;
+        y[c][z] = R(0.0);
         su[c * CST + z * PS + b * RS + a] = v;
         if (USE_ST) sT[c * CST + z * PS + a * RS + b] = v;
       }
@@ -623,6 +616,16 @@ sipg_apply2_kernel(const ApplyArgsT<R> A) {
   }
 
   // =============================================================== epilogue
+  if constexpr (MASS) {                 // Helmholtz mass term: + mass * JxW * u (diagonal M)
+#pragma unroll
+    for (int z = 0; z < n; ++z) {
+      R mjw;
+      if constexpr (GEO == 0) mjw = R(A.mass) * R(T.w[a]) * R(T.w[b]) * R(T.w[z]) * vol;
+      else mjw = R(A.mass) * A.jxw[(size_t)cell * n3 + z * n2 + p];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) y[c][z] += mjw * su[c * CST + z * PS + b * RS + a];
+    }
+  }
   if (active) {
     const size_t off = (size_t)cell * NC * n3;
 #pragma unroll

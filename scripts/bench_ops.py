@@ -143,11 +143,45 @@ def run_c4(reps):
     report("C4", "chebyshev5_from_x0_k5", ms, N, 5 * pb + 8 * N * (2 + 6 * 5), None, "includes one vector copy")
     ms = timeit(lambda: ctx.vcycle(A.OP_POISSON, b, x, lam), 10, reps)
     report("C4", "vcycle_5_3_2_1", ms, N, None, None, "fine-level DoFs per V-cycle second")
+    ms = timeit(lambda: ctx.vcycle_fp32(A.OP_POISSON, b, x, lam), 10, reps)
+    report("C4", "vcycle_5_3_2_1_fp32", ms, N, None, None, "every level in FP32 (f1); FP64 b/x converted")
     c = torch.empty(ctx.n_dofs(1), dtype=torch.float64, device="cuda")
     ms = timeit(lambda: ctx.restrict(A.OP_POISSON, 0, b, c), 20, reps)
     report("C4", "restrict_5_to_3", ms, N, 8 * cells * (216 + 64))
     ms = timeit(lambda: ctx.prolongate(A.OP_POISSON, 0, c, x, 1.0), 20, reps)
     report("C4", "prolongate_add_3_to_5", ms, N, 8 * cells * (64 + 2 * 216))
+
+
+def run_f1(reps):
+    """f1: Helmholtz viscous step (mass = 1e3) on C3, PCG to rtol 1e-8, FP64 vs FP32 V-cycle."""
+    m = cube(64)
+    degs = [4, 2, 1]
+    ctx = Context(m, 4, visc_law=C3_LAW, degrees=degs)
+    ctx.set_mass(A.OP_VISCOUS, 1.0e3)
+    ctx.update_viscosity(dev(c3_linearization(m, 4)))
+    lams = [1.2 * ctx.estimate_lambda_max(A.OP_VISCOUS, dev(uniform(2, 3 * ctx.n_dofs(l))), level=l, steps=20)
+            for l in range(len(degs))]
+    N = 3 * ctx.n_dofs(0)
+    b = dev(uniform(0, N))
+    for pc in ("vcycle", "vcycle_fp32", "jacobi"):
+        x = torch.zeros(N, dtype=torch.float64, device="cuda")
+        ctx.cg_solve(A.OP_VISCOUS, b, x, rtol=1e-8, maxit=400, precond=pc, lam_hi_per_level=lams)   # warm-up
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        x.zero_()
+        e0.record()
+        it, rr = ctx.cg_solve(A.OP_VISCOUS, b, x, rtol=1e-8, maxit=400, precond=pc, lam_hi_per_level=lams)
+        e1.record()
+        e1.synchronize()
+        ms = e0.elapsed_time(e1)
+        report("C3+f1", f"helmholtz_pcg_{pc}", ms, N, None, None,
+               f"{it} iterations to rtol 1e-8 (relres {rr:.2e}); {ms / max(it, 1):.3f} ms/iteration")
+        x2 = torch.zeros(N, dtype=torch.float64, device="cuda")
+        if pc != "jacobi":
+            r = dev(uniform(5, N))
+            f = ctx.vcycle if pc == "vcycle" else ctx.vcycle_fp32
+            ms = timeit(lambda: f(A.OP_VISCOUS, r, x2, lams), 5, reps)
+            report("C3+f1", f"viscous_{pc}_4_2_1", ms, N, None, None, "one V-cycle of the Helmholtz operator")
 
 
 def run_c5(reps):
@@ -165,12 +199,12 @@ def run_c5(reps):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--configs", default="2,3,4,5")
+    ap.add_argument("--configs", default="2,3,4,5,f1")
     ap.add_argument("--reps", type=int, default=5)
     a = ap.parse_args()
     torch.cuda.set_device(0)
     for c in a.configs.split(","):
-        {"2": run_c2, "3": run_c3, "4": run_c4, "5": run_c5}[c](a.reps)
+        {"2": run_c2, "3": run_c3, "4": run_c4, "5": run_c5, "f1": run_f1}[c](a.reps)
         torch.cuda.empty_cache()
 
 
