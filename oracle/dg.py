@@ -528,3 +528,69 @@ def helmholtz_apply(disc: Disc, u: np.ndarray, nu, mass: float, cells=None) -> n
     if mass != 0.0:
         y = y + mass * mass_apply(disc, u, 3, cells=cells)
     return y
+
+
+def penalty_apply(disc: Disc, u: np.ndarray, tau_div: np.ndarray, tau_cont: np.ndarray, cells=None,
+                  chunk: int = 4096) -> np.ndarray:
+    """y = A_pen u, the left-hand side of the divergence/continuity penalty step
+    (eqn:penalty_step), homogeneous part:
+      sum_e (v, u)_e + (div v, tau_div^e div u)_e + (v.n, tau_cont [[u]].n)_{boundary of e}
+    with the oriented jump [[u]] = u(e) - u(neighbour) on interior/periodic faces, [[u]] = u on
+    Dirichlet faces (boundary data g_u moves to the right-hand side), nothing on Neumann faces.
+    Readings (P1/P2): tau_div^e, tau_cont^e are per-cell inputs (the paper takes them
+    from Fehn2018b without formulas); on an interior face the continuity weight is
+    (tau_cont^- + tau_cont^+)/2 from both sides (symmetric operator), on a Dirichlet face the
+    cell's own tau_cont.  Full-tensor quadrature, Gauss n_q = k+1 (G1).  Output [cell][c][i]."""
+    full = cells is None
+    d = disc
+    nc, N = d.mesh.n_cells, d.N
+    U = u.reshape(nc, 3, N)
+    cells, row = _prepare(d, cells)
+    y = np.zeros((len(cells), 3, N))
+    for sl in _chunks(len(cells), chunk):
+        cs = cells[sl]
+        _, JxW, Jinv = d.vol_geom(cs)
+        uq = np.einsum("qj,kcj->kcq", d.Phi, U[cs])
+        y[sl] += np.einsum("qi,kq,kcq->kci", d.Phi, JxW, uq)                  # (v, u)
+        G = grad_at(d, U[cs], d.dPhi, Jinv)                                    # [C,Q,3,3] du_i/dx_j
+        div = np.einsum("cqii->cq", G)
+        w = (tau_div[cs][:, None] * JxW) * div                                 # tau_div JxW div u
+        # div v for v = e_c phi_n: d phi_n / d x_c = sum_d dPhi[d,q,n] Jinv[q,d,c]
+        y[sl] += np.einsum("kq,dqn,kqdc->kcn", w, d.dPhi, Jinv)
+
+    inter, bnd = d.unique_faces(cells)
+
+    def add(cs, contrib):
+        r = row[cs]
+        m = r >= 0
+        np.add.at(y, r[m], contrib[m])
+
+    def side(cs, f, perm=None):
+        _, _, n, dA = d.face_geom(cs, f)
+        val = np.einsum("pn,kcn->kcp", d.PhiF[f], U[cs])                      # [C,3,P]
+        Phi = d.PhiF[f]
+        if perm is not None:
+            val = np.take_along_axis(val, perm[:, None, :], axis=2)
+            Phi_c = Phi[perm]
+        else:
+            Phi_c = np.broadcast_to(Phi, (len(cs),) + Phi.shape)
+        return val, Phi_c, n, dA
+
+    for (fa, fb), (a_all, b_all, perm_all) in _group_faces(d, inter).items():
+        for sl in _chunks(len(a_all), chunk):
+            a, b, perm = a_all[sl], b_all[sl], perm_all[sl]
+            ua, Phia, n, dA = side(a, fa)
+            ub, Phib, _, _ = side(b, fb, perm)
+            tau = 0.5 * (tau_cont[a] + tau_cont[b])[:, None]
+            jn = np.einsum("kcp,kpc->kp", ua - ub, n)                          # [[u]].n from K-
+            coef = dA * tau * jn                                               # times v.n
+            add(a, np.einsum("kp,kpc,kpn->kcn", coef, n, Phia))
+            add(b, np.einsum("kp,kpc,kpn->kcn", -coef, n, Phib))                # v+ . n- = -(v+ . n+)
+    for f in range(6):
+        cs = np.array([c for (c, g, t) in bnd if g == f and t == 1], dtype=np.int64)
+        if len(cs) == 0:
+            continue
+        ua, Phia, n, dA = side(cs, f)
+        jn = np.einsum("kcp,kpc->kp", ua, n)
+        add(cs, np.einsum("kp,kpc,kpn->kcn", dA * tau_cont[cs][:, None] * jn, n, Phia))
+    return y.reshape(-1) if full else y
