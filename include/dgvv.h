@@ -63,7 +63,7 @@ enum {                                  /* coefficient laws (S
                              gd = sqrt(2 eps:eps)  (G9)  (C3, C5) */
 };
 
-enum { DGVV_OP_VISCOUS = 0, DGVV_OP_POISSON = 1 };
+enum { DGVV_OP_VISCOUS = 0, DGVV_OP_POISSON = 1, DGVV_OP_PENALTY = 2 };
 enum { DGVV_FORM_DIVERGENCE = 0,   /* the paper's -div(2 nu eps(u)) (eqn:viscous_term_weak) */
        DGVV_FORM_LAPLACE = 1 };    /* tau_1 terms only: -div(nu grad u)  */
 
@@ -146,6 +146,19 @@ dgvv_status dgvv_apply_poisson(dgvv_ctx* ctx, int32_t level, const double* src, 
 dgvv_status dgvv_set_mass(dgvv_ctx* ctx, int32_t op, double mass);
 
 enum { DGVV_PRECOND_NONE = 0, DGVV_PRECOND_JACOBI = 1, DGVV_PRECOND_VCYCLE = 2, DGVV_PRECOND_VCYCLE_FP32 = 3 };
+
+/* Divergence/continuity penalty-step operator (PAPER.md:1190-1224,
+ * eqn:penalty_step), homogeneous part, on level 0:
+ *   dst_e = (v, u)_e + (div v, tau_div^e div u)_e + (v.n, tau_F [[u]].n)_{boundary of e}
+ * [[u]] = u(e) - u(neighbour) on interior/periodic faces (tau_F = (tau_cont^e + tau_cont^nb)/2),
+ * [[u]] = u on Dirichlet faces (tau_F = tau_cont^e; the data g_u belongs to the right-hand
+ * side), no term on Neumann faces.  The paper takes tau_div, tau_cont from Fehn2018b without
+ * formulas: they are inputs here, one value per cell (host arrays of n_cells + n_ghost
+ * entries, owned cells then ghosts in the dgvv_mesh ghost order; copied).  DGVV_EDOMAIN for
+ * negative or non-finite values.  Usable with dgvv_inverse_diagonal (level 0) and
+ * dgvv_cg_solve (preconditioner none or Jacobi) as op = DGVV_OP_PENALTY. */
+dgvv_status dgvv_set_penalty_parameters(dgvv_ctx* ctx, const double* tau_div, const double* tau_cont);
+dgvv_status dgvv_apply_penalty(dgvv_ctx* ctx, const double* src, double* dst, dgvv_stream stream);
 
 /* Preconditioned conjugate gradients on (mass M +) A_op, level 0 (the Krylov solver of the
  * symmetric viscous and pressure steps):

@@ -17,7 +17,7 @@ STATUS = {0: "DGVV_OK", 1: "DGVV_EINVAL", 2: "DGVV_EDOMAIN", 3: "DGVV_ENOMEM", 4
 OK, EINVAL, EDOMAIN, ENOMEM, ECUDA, ENCCL, ESTATE, EUNSUPPORTED = range(8)
 BC_DIRICHLET, BC_NEUMANN = 1, 2
 LAW_CONST, LAW_SIN3, LAW_EXP, LAW_CARREAU = 0, 1, 2, 3
-OP_VISCOUS, OP_POISSON = 0, 1
+OP_VISCOUS, OP_POISSON, OP_PENALTY = 0, 1, 2
 PRECOND_NONE, PRECOND_JACOBI, PRECOND_VCYCLE, PRECOND_VCYCLE_FP32 = 0, 1, 2, 3
 FORM_DIVERGENCE, FORM_LAPLACE = 0, 1
 GHOST_VISCOUS, GHOST_POISSON, GHOST_ULIN = 0, 1, 2
@@ -56,6 +56,8 @@ _SIGS = {
     "dgvv_apply_viscous_host": [VP, I32, VP, VP, VP],
     "dgvv_set_mass": [VP, I32, D],
     "dgvv_vcycle_fp32": [VP, I32, VP, VP, PD, VP],
+    "dgvv_set_penalty_parameters": [VP, PD, PD],
+    "dgvv_apply_penalty": [VP, VP, VP, VP],
     "dgvv_cg_solve": [VP, I32, VP, VP, D, I32, I32, PD, C.POINTER(I32), PD, VP],
     "dgvv_apply_linearized_viscous": [VP, VP, VP, VP],
     "dgvv_apply_poisson": [VP, I32, VP, VP, VP],

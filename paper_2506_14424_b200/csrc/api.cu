@@ -100,6 +100,7 @@ dgvv_status upload_tables() {
   DGVV_CUDA_TRY(upload_tables_pois(tabs.data()));
   DGVV_CUDA_TRY(upload_tables_aux(tabs.data()));
   DGVV_CUDA_TRY(upload_tables_newton(tabs.data()));
+  DGVV_CUDA_TRY(upload_tables_pen(tabs.data()));
   g_tab_done = true;
   return DGVV_OK;
 }
@@ -163,7 +164,13 @@ struct dgvv_ctx {
   int form = 0;
   double ip = 1.0;
   double mass[2] = {0.0, 0.0};  // Helmholtz mass coefficient per op (dgvv_set_mass)
-  double* cg_work[2] = {nullptr, nullptr};   // CG vectors r, z, p, q per op (level 0)
+  double* cg_work[3] = {nullptr, nullptr, nullptr};   // CG vectors r, z, p, q per op (level 0)
+  // f2 penalty-step operator: per-cell parameters (owned then ghosts, internal order)
+  double* d_tau_div = nullptr;
+  double* d_tau_cont = nullptr;
+  double* dinv_pen = nullptr;
+  bool has_pen = false;
+  std::vector<int> h_gperm;                  // internal ghost i -> mesh ghost row
   std::vector<LevelF> LF;                    // FP32 levels (lazily built)
   float* d_cart_f = nullptr;
   int coef_epoch = 0;                        // bumped whenever coefficients or the mass change
@@ -319,6 +326,8 @@ dgvv_status op_ready(dgvv_ctx* c, int op) {
     if (c->carreau && !c->nu_ready) return dgvv_fail(DGVV_ESTATE, "Carreau law: call dgvv_update_viscosity first");
   } else if (op == DGVV_OP_POISSON) {
     if (!c->has_pois) return dgvv_fail(DGVV_ESTATE, "no Poisson coefficient law given at setup");
+  } else if (op == DGVV_OP_PENALTY) {
+    if (!c->has_pen) return dgvv_fail(DGVV_ESTATE, "penalty operator: call dgvv_set_penalty_parameters first");
   } else {
     return dgvv_fail(DGVV_EINVAL, "unknown op %d", op);
   }
@@ -549,6 +558,7 @@ static dgvv_status setup_impl(const dgvv_mesh* m, int32_t degree, const dgvv_law
   std::unordered_map<long long, int> gmap;
   for (int i = 0; i < c->n_ghost; ++i) gmap[m->ghost_global_id[gperm[i]]] = c->n_owned + i;
   auto row_of = [&](int local) -> int { return local < c->n_owned ? local : c->n_owned + gperm[local - c->n_owned]; };
+  c->h_gperm = gperm;
   std::vector<int> nbr((size_t)c->n_total * 6);
   for (int lc = 0; lc < c->n_total; ++lc) {
     const int r = row_of(lc);
@@ -977,6 +987,8 @@ dgvv_status dgvv_apply_linearized_viscous(dgvv_ctx* c, const double* src, double
   return run_apply(c, DGVV_OP_VISCOUS, 0, a, s, true);
 }
 
+static dgvv_status ensure_dinv_pen(dgvv_ctx* c, cudaStream_t s);
+
 dgvv_status dgvv_set_mass(dgvv_ctx* c, int32_t op, double mass) {
   if (!c) return dgvv_fail(DGVV_EINVAL, "null context");
   if (op != DGVV_OP_VISCOUS && op != DGVV_OP_POISSON) return dgvv_fail(DGVV_EINVAL, "unknown op %d", op);
@@ -998,6 +1010,13 @@ dgvv_status dgvv_inverse_diagonal(dgvv_ctx* c, int32_t op, int32_t level, double
   TRY(op_ready(c, op));
   if (!dst) return dgvv_fail(DGVV_EINVAL, "null dst");
   cudaStream_t s = (cudaStream_t)stream;
+  if (op == DGVV_OP_PENALTY) {
+    if (level != 0) return dgvv_fail(DGVV_EINVAL, "penalty operator: level 0 only");
+    TRY(ensure_dinv_pen(c, s));
+    DGVV_CUDA_TRY(cudaMemcpyAsync(dst, c->dinv_pen, (size_t)3 * level_dofs(c, 0) * sizeof(double),
+                                  cudaMemcpyDeviceToDevice, s));
+    return DGVV_OK;
+  }
   TRY(ensure_dinv(c, op, level, s));
   const int nc = op == DGVV_OP_VISCOUS ? 3 : 1;
   DGVV_CUDA_TRY(cudaMemcpyAsync(dst, c->L[level].dinv[op == DGVV_OP_VISCOUS ? 0 : 1],
@@ -1292,6 +1311,81 @@ static dgvv_status dot_host(dgvv_ctx* c, const double* a, const double* b, long 
   return DGVV_OK;
 }
 
+// ------------------------------------------------------------------ f2: penalty-step operator
+static PenaltyArgs penalty_args(dgvv_ctx* c) {
+  PenaltyArgs a;
+  std::memset(&a, 0, sizeof(a));
+  Level& L = c->L[0];
+  a.nbr = c->d_nbr;
+  a.n_proc = c->n_owned;
+  a.n_owned = c->n_owned;
+  a.cart = c->d_cart;
+  a.vJi = L.vJi;
+  a.jxw = L.jxw;
+  a.fJi = L.fJi;
+  a.fdA = L.fdA;
+  a.tau_div = c->d_tau_div;
+  a.tau_cont = c->d_tau_cont;
+  a.ghost = L.ghost[0];
+  return a;
+}
+
+static dgvv_status apply_penalty_impl(dgvv_ctx* c, const double* src, double* dst, cudaStream_t s) {
+  PenaltyArgs a = penalty_args(c);
+  a.src = src;
+  a.dst = dst;
+  if (c->n_ghost) {
+    if (!c->L[0].ghost[0]) TRY(dalloc(c, &c->L[0].ghost[0], (size_t)c->n_ghost * 3 * c->L[0].n * c->L[0].n * c->L[0].n));
+    a.ghost = c->L[0].ghost[0];
+    TRY(exchange_sync(c, 0, 3, src, c->L[0].ghost[0], s));
+  }
+  cudaError_t e = launch_penalty(c->L[0].n, c->geo, a, false, s);
+  if (e == cudaErrorNotSupported) return dgvv_fail(DGVV_EUNSUPPORTED, "penalty kernel not built for degree %d", c->L[0].k);
+  if (e != cudaSuccess) return dgvv_fail(DGVV_ECUDA, "penalty kernel: %s", cudaGetErrorString(e));
+  return DGVV_OK;
+}
+
+static dgvv_status ensure_dinv_pen(dgvv_ctx* c, cudaStream_t s) {
+  if (c->dinv_pen) return DGVV_OK;
+  TRY(dalloc(c, &c->dinv_pen, (size_t)3 * level_dofs(c, 0)));
+  PenaltyArgs a = penalty_args(c);
+  a.dst = c->dinv_pen;
+  cudaError_t e = launch_penalty(c->L[0].n, c->geo, a, true, s);
+  if (e != cudaSuccess) return dgvv_fail(DGVV_ECUDA, "penalty diagonal: %s", cudaGetErrorString(e));
+  return DGVV_OK;
+}
+
+dgvv_status dgvv_set_penalty_parameters(dgvv_ctx* c, const double* tau_div, const double* tau_cont) {
+  if (!c || !tau_div || !tau_cont) return dgvv_fail(DGVV_EINVAL, "null argument");
+  const int nt = c->n_total;
+  std::vector<double> td(nt), tc(nt);
+  for (int i = 0; i < nt; ++i) {
+    const int r = i < c->n_owned ? i : c->n_owned + c->h_gperm[i - c->n_owned];
+    td[i] = tau_div[r];
+    tc[i] = tau_cont[r];
+    if (!std::isfinite(td[i]) || !std::isfinite(tc[i]) || td[i] < 0.0 || tc[i] < 0.0)
+      return dgvv_fail(DGVV_EDOMAIN, "penalty parameters must be finite and >= 0 (cell row %d)", r);
+  }
+  if (!c->d_tau_div) TRY(dalloc(c, &c->d_tau_div, (size_t)nt));
+  if (!c->d_tau_cont) TRY(dalloc(c, &c->d_tau_cont, (size_t)nt));
+  DGVV_CUDA_TRY(cudaMemcpy(c->d_tau_div, td.data(), nt * sizeof(double), cudaMemcpyHostToDevice));
+  DGVV_CUDA_TRY(cudaMemcpy(c->d_tau_cont, tc.data(), nt * sizeof(double), cudaMemcpyHostToDevice));
+  if (c->dinv_pen) {
+    cudaFree(c->dinv_pen);
+    c->allocs.erase(std::remove(c->allocs.begin(), c->allocs.end(), (void*)c->dinv_pen), c->allocs.end());
+    c->dinv_pen = nullptr;
+  }
+  c->has_pen = true;
+  return DGVV_OK;
+}
+
+dgvv_status dgvv_apply_penalty(dgvv_ctx* c, const double* src, double* dst, dgvv_stream stream) {
+  if (!c || !src || !dst) return dgvv_fail(DGVV_EINVAL, "null argument");
+  if (src == dst) return dgvv_fail(DGVV_EINVAL, "src and dst alias");
+  TRY(op_ready(c, DGVV_OP_PENALTY));
+  return apply_penalty_impl(c, src, dst, (cudaStream_t)stream);
+}
+
 dgvv_status dgvv_cg_solve(dgvv_ctx* c, int32_t op, const double* b, double* x, double rtol, int32_t maxit,
                           int32_t precond, const double* lambda_hi_per_level, int32_t* iters, double* relres,
                           dgvv_stream stream) {
@@ -1304,13 +1398,16 @@ dgvv_status dgvv_cg_solve(dgvv_ctx* c, int32_t op, const double* b, double* x, d
   if ((precond == DGVV_PRECOND_VCYCLE || precond == DGVV_PRECOND_VCYCLE_FP32) && !lambda_hi_per_level)
     return dgvv_fail(DGVV_EINVAL, "V-cycle preconditioner needs lambda_hi_per_level");
   cudaStream_t s = (cudaStream_t)stream;
+  const bool pen = op == DGVV_OP_PENALTY;
+  if (pen && (precond == DGVV_PRECOND_VCYCLE || precond == DGVV_PRECOND_VCYCLE_FP32))
+    return dgvv_fail(DGVV_EUNSUPPORTED, "penalty operator: no multigrid hierarchy (use none or Jacobi)");
   const int oi = op == DGVV_OP_VISCOUS ? 0 : 1;
-  const int nc = op == DGVV_OP_VISCOUS ? 3 : 1;
+  const int nc = op == DGVV_OP_POISSON ? 1 : 3;
   const long N = (long)nc * level_dofs(c, 0);
-  auto& W = c->cg_work[oi];
+  auto& W = c->cg_work[pen ? 2 : oi];
   if (!W) TRY(dalloc(c, &W, (size_t)4 * N));
   double *r = W, *z = W + N, *pv = W + 2 * N, *q = W + 3 * N;
-  if (precond == DGVV_PRECOND_JACOBI) TRY(ensure_dinv(c, op, 0, s));
+  if (precond == DGVV_PRECOND_JACOBI) TRY(pen ? ensure_dinv_pen(c, s) : ensure_dinv(c, op, 0, s));
   if (precond == DGVV_PRECOND_VCYCLE) {      // scratch of every level (as dgvv_vcycle)
     for (size_t l = 0; l < c->L.size(); ++l) {
       auto& S = c->L[l].scratch[oi];
@@ -1325,6 +1422,11 @@ dgvv_status dgvv_cg_solve(dgvv_ctx* c, int32_t op, const double* b, double* x, d
     }
   }
   auto apply_A = [&](const double* src, double* dst, const double* rhs) -> dgvv_status {
+    if (pen) {
+      TRY(apply_penalty_impl(c, src, dst, s));
+      if (rhs) DGVV_CUDA_TRY(launch_axpby(1.0, rhs, -1.0, dst, N, s));   // dst = rhs - A src
+      return DGVV_OK;
+    }
     ApplyArgs a = base_args(c, 0, op);
     a.src = src; a.dst = dst;
     if (rhs) { a.b = rhs; a.mode = MODE_RESID; }
@@ -1332,7 +1434,7 @@ dgvv_status dgvv_cg_solve(dgvv_ctx* c, int32_t op, const double* b, double* x, d
   };
   auto prec = [&](const double* rr, double* zz) -> dgvv_status {
     if (precond == DGVV_PRECOND_JACOBI) {
-      DGVV_CUDA_TRY(launch_ew_mul(c->L[0].dinv[oi], rr, zz, N, s));
+      DGVV_CUDA_TRY(launch_ew_mul(pen ? c->dinv_pen : c->L[0].dinv[oi], rr, zz, N, s));
     } else if (precond == DGVV_PRECOND_VCYCLE) {
       TRY(vcycle_rec(c, op, 0, rr, zz, lambda_hi_per_level, s));
     } else if (precond == DGVV_PRECOND_VCYCLE_FP32) {

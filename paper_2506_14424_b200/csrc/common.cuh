@@ -74,6 +74,22 @@ struct ApplyArgsT {  // R = double (operators) or float (FP32 multigrid levels, 
 };
 using ApplyArgs = ApplyArgsT<double>;
 
+// f2 penalty-step operator (penalty_apply.cuh)
+struct PenaltyArgs {
+  const double* src;
+  const double* ghost;
+  double* dst;
+  const int* nbr;
+  int n_proc, n_owned, cell_base;
+  const double* cart;       // Cartesian geometry
+  const double* vJi;        // general: J^-1 at cell points
+  const double* jxw;        // general: JxW at cell points
+  const double* fJi;        // general: own J^-1 at face points (normal)
+  const double* fdA;        // general: dA at own face points
+  const double* tau_div;    // [n_total]
+  const double* tau_cont;   // [n_total]
+};
+
 struct NuArgs {
   const double* u;          // owned [n_owned][3][n^3]
   const double* ughost;     // ghost [n_ghost][3][n^3]

@@ -1,0 +1,45 @@
+// k_pen.cu — instantiations of the penalty-step operator (§8(f) f2): apply and inverse diagonal.
+#include "tu_tables.cuh"
+#include "penalty_apply.cuh"
+#include "launch.h"
+
+namespace dgvv {
+
+cudaError_t upload_tables_pen(const Tab1D* tabs) { return tu_upload_tables(tabs); }
+
+template <int n> constexpr int cpb_pen() { return n == 2 ? 32 : n == 3 ? 14 : n == 4 ? 8 : n == 5 ? 5 : 3; }
+
+template <int n, int GEO>
+static cudaError_t pen_run(const PenaltyArgs& a, bool diag, cudaStream_t s) {
+  if (diag) {
+    const long tot = (long)a.n_owned * 3 * n * n * n;
+    if (tot <= 0) return cudaSuccess;
+    penalty_diag_kernel<n, GEO><<<(int)((tot + 255) / 256), 256, 0, s>>>(a);
+    return cudaGetLastError();
+  }
+  constexpr int CPB = cpb_pen<n>();
+  const size_t smem = (size_t)CPB * PenaltyCfg<n, GEO>::CS * sizeof(double);
+  auto k = penalty_apply_kernel<n, GEO, CPB>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  if (a.n_proc <= 0) return cudaSuccess;
+  k<<<(a.n_proc + CPB - 1) / CPB, CPB * n * n, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_penalty(int n, int geo, const PenaltyArgs& a, bool diag, cudaStream_t s) {
+  switch (n) {
+    case 2: return geo ? pen_run<2, 1>(a, diag, s) : pen_run<2, 0>(a, diag, s);
+    case 3: return geo ? pen_run<3, 1>(a, diag, s) : pen_run<3, 0>(a, diag, s);
+    case 4: return geo ? pen_run<4, 1>(a, diag, s) : pen_run<4, 0>(a, diag, s);
+    case 5: return geo ? pen_run<5, 1>(a, diag, s) : pen_run<5, 0>(a, diag, s);
+    case 6: return geo ? pen_run<6, 1>(a, diag, s) : pen_run<6, 0>(a, diag, s);
+    default: return cudaErrorNotSupported;
+  }
+}
+
+}  // namespace dgvv

@@ -11,11 +11,14 @@ cudaError_t upload_tables_visc(const Tab1D* tabs);
 cudaError_t upload_tables_pois(const Tab1D* tabs);
 cudaError_t upload_tables_aux(const Tab1D* tabs);
 cudaError_t upload_tables_newton(const Tab1D* tabs);
+cudaError_t upload_tables_pen(const Tab1D* tabs);
 
 // K1 / K4 / K6: SIPG apply with epilogue (nc = 3 viscous, 1 Poisson)
 cudaError_t launch_apply(int nc, int n, int form, int geo, const ApplyArgs& a, cudaStream_t s);
 // FP32 variant (multigrid preconditioner levels)
 cudaError_t launch_apply_f(int nc, int n, int form, int geo, const ApplyArgsT<float>& a, cudaStream_t s);
+// f2: divergence/continuity penalty operator (apply, or inverse diagonal when diag = true)
+cudaError_t launch_penalty(int n, int geo, const PenaltyArgs& a, bool diag, cudaStream_t s);
 // K2: Newton-linearised viscous apply
 cudaError_t launch_newton(int n, int geo, const ApplyArgs& a, cudaStream_t s);
 // K3: Carreau viscosity at all points

@@ -111,7 +111,7 @@ class Context:
         return ng.value
 
     def _n(self, op, level):
-        return (3 if op == A.OP_VISCOUS else 1) * self.n_dofs(level)
+        return (1 if op == A.OP_POISSON else 3) * self.n_dofs(level)
 
     # ------------------------------------------------------------------ calls
     def update_viscosity(self, u_lin):
@@ -202,6 +202,19 @@ class Context:
         arr = (C.c_double * len(self.degrees))(*[float(v) for v in lam_hi_per_level])
         A.check(self._L.dgvv_vcycle_fp32(self.h, op, _ptr(b, n, "b"), _ptr(x, n, "x"), arr, _stream()))
         return x
+
+    def set_penalty_parameters(self, tau_div, tau_cont):
+        """Per-cell penalty parameters (owned cells, then ghosts in mesh ghost order) of the
+        penalty-step operator (dgvv_set_penalty_parameters)."""
+        td = np.ascontiguousarray(tau_div, dtype=np.float64)
+        tc = np.ascontiguousarray(tau_cont, dtype=np.float64)
+        A.check(self._L.dgvv_set_penalty_parameters(self.h, td.ctypes.data_as(C.POINTER(C.c_double)),
+                                                    tc.ctypes.data_as(C.POINTER(C.c_double))))
+
+    def apply_penalty(self, src, dst):
+        n = 3 * self.n_dofs(0)
+        A.check(self._L.dgvv_apply_penalty(self.h, _ptr(src, n, "src"), _ptr(dst, n, "dst"), _stream()))
+        return dst
 
     def dot(self, a, b, ncomp=1, level=0):
         out = C.c_double()
