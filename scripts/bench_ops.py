@@ -184,6 +184,37 @@ def run_f1(reps):
             report("C3+f1", f"viscous_{pc}_4_2_1", ms, N, None, None, "one V-cycle of the Helmholtz operator")
 
 
+def run_f2(reps):
+    """f2: penalty-step operator on the C2 mesh (32^3 deformed, k=3) and on C3's 64^3 k=4 mesh,
+    tau ~ |u| h dt (Fehn2018b-sized, P1), apply + Jacobi-PCG to rtol 1e-10."""
+    for name, m, k in (("C2", deformed_cube(32, 3), 3), ("C3", cube(64), 4)):
+        ctx = Context(m, k, visc_law=C2_LAW)
+        rng = np.random.default_rng(11)
+        h = 1.0 / round(m.n_cells ** (1 / 3))
+        speed = rng.uniform(0.1, 2.0, m.n_cells)
+        ctx.set_penalty_parameters(speed * h * 1e-3, speed * 1e-3)
+        N = 3 * ctx.n_dofs(0)
+        src = dev(uniform(0, N))
+        dst = torch.empty_like(src)
+        n = k + 1
+        general = m.map_degree > 1
+        byt = m.n_cells * 8 * (2 * 3 * n ** 3 + 2 + (10 * n ** 3 + 6 * 4 * n * n if general else 8))
+        ms = timeit(lambda: ctx.apply_penalty(src, dst), 20, reps)
+        report(name + "+f2", "apply_penalty", ms, N, byt, None, "mass + div-div + continuity penalty")
+        x = torch.zeros_like(src)
+        ctx.cg_solve(A.OP_PENALTY, src, x, rtol=1e-10, maxit=500, precond="jacobi")
+        x.zero_()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        it, rr = ctx.cg_solve(A.OP_PENALTY, src, x, rtol=1e-10, maxit=500, precond="jacobi")
+        e1.record()
+        e1.synchronize()
+        ms = e0.elapsed_time(e1)
+        report(name + "+f2", "penalty_pcg_jacobi", ms, N, None, None,
+               f"{it} iterations to rtol 1e-10 (relres {rr:.2e}); {ms / max(it, 1):.3f} ms/iteration")
+
+
 def run_c5(reps):
     m = bfs()
     ctx = Context(m, 3, visc_law=C5_LAW)
@@ -199,12 +230,12 @@ def run_c5(reps):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--configs", default="2,3,4,5,f1")
+    ap.add_argument("--configs", default="2,3,4,5,f1,f2")
     ap.add_argument("--reps", type=int, default=5)
     a = ap.parse_args()
     torch.cuda.set_device(0)
     for c in a.configs.split(","):
-        {"2": run_c2, "3": run_c3, "4": run_c4, "5": run_c5, "f1": run_f1}[c](a.reps)
+        {"2": run_c2, "3": run_c3, "4": run_c4, "5": run_c5, "f1": run_f1, "f2": run_f2}[c](a.reps)
         torch.cuda.empty_cache()
 
 
