@@ -4,15 +4,61 @@
 // evaluated pointwise at every cell point and, per side, at every face point from that side's
 // own traces (G8); the penalty uses (nu0- + nu0+)/2 and (dnu- + dnu+)/2.  nu0 and g are
 // recomputed from eps(u0) in the kernel (the ε(u0) needed for delta_nu is formed anyway), so
-// the stream is src + u_lin + dst.  Same cell-centric structure as sipg_apply.cuh: a team of
+// the stream is src + u_lin + dst.  Cell-centric like sipg_apply2.cuh: a team of
 // n^2 threads per cell, z-columns in registers, faces one at a time (two fields double the
 // live state), both fields' full face gradients (delta_nu needs all of eps).
 #pragma once
 #include "common.cuh"
 #include "laws.cuh"
-#include "sipg_apply.cuh"
+
 
 namespace dgvv {
+
+// Flux coefficients at one face point from the own side ("-"), general geometry.
+// Gm/Gp: physical gradients G[c][j] = d u_c / d x_j; um/up values; wm/wp = nu-*dA, nu+*dA;
+// returns fv[c] (coefficient of v_c) and gk[c][k] (coefficient of d v_c / d xi_k).
+template <int NC, int FORM>
+__device__ __forceinline__ void face_flux_gen(const double (&um)[NC], const double (&up)[NC],
+                                              const double (&Gm)[NC][3], const double (&Gp)[NC][3],
+                                              const double* nrm, double wm, double wp, double tau,
+                                              const double (&Jim)[9], double (&fv)[NC], double (&gk)[NC][3]) {
+  static_assert(FORM == 1 || NC == 3, "divergence form needs 3 components");
+  double jmp[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) jmp[c] = um[c] - up[c];
+  double jn = 0.0;
+  if constexpr (FORM == 0) {
+#pragma unroll
+    for (int c = 0; c < NC; ++c) jn += jmp[c] * nrm[c];
+  }
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      double sm, sp;
+      if constexpr (FORM == 0) {
+        sm = 0.5 * (Gm[c][j] + Gm[j][c]);
+        sp = 0.5 * (Gp[c][j] + Gp[j][c]);
+      } else {
+        sm = 0.5 * Gm[c][j];
+        sp = 0.5 * Gp[c][j];
+      }
+      acc += (wm * sm + wp * sp) * nrm[j];
+    }
+    const double pv = (FORM == 0) ? (jmp[c] + nrm[c] * jn) : jmp[c];
+    fv[c] = -acc + tau * pv;
+    double Gc[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      if constexpr (FORM == 0) Gc[j] = -wm * 0.5 * (jmp[c] * nrm[j] + jmp[j] * nrm[c]);
+      else Gc[j] = -wm * 0.5 * jmp[c] * nrm[j];
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) gk[c][k] = Gc[0] * Jim[3 * k] + Gc[1] * Jim[3 * k + 1] + Gc[2] * Jim[3 * k + 2];
+  }
+}
+
 
 template <int n, int GEO>
 struct NewtonCfg {
