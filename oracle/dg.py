@@ -594,3 +594,62 @@ def penalty_apply(disc: Disc, u: np.ndarray, tau_div: np.ndarray, tau_cont: np.n
         jn = np.einsum("kcp,kpc->kp", ua, n)
         add(cs, np.einsum("kp,kpc,kpn->kcn", dA * tau_cont[cs][:, None] * jn, n, Phia))
     return y.reshape(-1) if full else y
+
+
+def convective_apply(disc: Disc, u: np.ndarray, w: np.ndarray, cells=None, chunk: int = 4096) -> np.ndarray:
+    """y = C(w) u, the upwind DG convective term of eqn:convective_term_weak (PAPER.md:686-711;
+    SURVEY §8(f) f4), homogeneous part, linear in u for a given transport field w:
+      c_h^e(v, u; w) = (v, (w.grad) u)_e - (v, ({{w}}.n) u)_{de} + (v, ({{w}}.n) u^dag)_{de},
+      u^dag = {{u}} + 1/2 sign({{w}}.n) [[u]],  [[u]] = u(e) - u(neighbour),
+    so the face integrand from e is ({{w}}.n)(u^dag - u) = min({{w}}.n, 0) (u(nb) - u(e)).
+    Readings (F4a-F4c): the operator written \\convectiveterm{u}{w} is (w.grad)u (the
+    strong/convective form the boundary terms above belong to); on Dirichlet faces the exterior
+    states are the mirror states u+ = -u, w+ = -w (homogeneous data, as G7), so {{w}} = 0 there;
+    on Neumann faces u+ = u, w+ = w (no jump: no term); periodic faces are interior.
+    Full-tensor quadrature, Gauss n_q = k+1 (G1).  Output [cell][c][i]."""
+    full = cells is None
+    d = disc
+    nc, N = d.mesh.n_cells, d.N
+    U = u.reshape(nc, 3, N)
+    Wf = w.reshape(nc, 3, N)
+    cells, row = _prepare(d, cells)
+    y = np.zeros((len(cells), 3, N))
+    for sl in _chunks(len(cells), chunk):
+        cs = cells[sl]
+        _, JxW, Jinv = d.vol_geom(cs)
+        G = grad_at(d, U[cs], d.dPhi, Jinv)                            # [C,Q,3,3] du_i/dx_j
+        wq = np.einsum("qj,kcj->kqc", d.Phi, Wf[cs])                   # w at the points [C,Q,3]
+        conv = np.einsum("kqij,kqj->kqi", G, wq)                       # (w.grad) u  [C,Q,3]
+        y[sl] += np.einsum("qn,kq,kqi->kin", d.Phi, JxW, conv)
+
+    inter, bnd = d.unique_faces(cells)
+
+    def add(cs, contrib):
+        r = row[cs]
+        m = r >= 0
+        np.add.at(y, r[m], contrib[m])
+
+    def side(cs, f, perm=None):
+        _, _, n, dA = d.face_geom(cs, f)
+        uu = np.einsum("pn,kcn->kpc", d.PhiF[f], U[cs])
+        ww = np.einsum("pn,kcn->kpc", d.PhiF[f], Wf[cs])
+        Phi = d.PhiF[f]
+        if perm is not None:
+            uu = np.take_along_axis(uu, perm[..., None], axis=1)
+            ww = np.take_along_axis(ww, perm[..., None], axis=1)
+            Phi_c = Phi[perm]
+        else:
+            Phi_c = np.broadcast_to(Phi, (len(cs),) + Phi.shape)
+        return uu, ww, Phi_c, n, dA
+
+    for (fa, fb), (a_all, b_all, perm_all) in _group_faces(d, inter).items():
+        for sl in _chunks(len(a_all), chunk):
+            a, b, perm = a_all[sl], b_all[sl], perm_all[sl]
+            ua, wa, Phia, n, dA = side(a, fa)
+            ub, wb, Phib, _, _ = side(b, fb, perm)
+            wn = np.einsum("kpc,kpc->kp", 0.5 * (wa + wb), n)           # {{w}}.n, n from K-
+            # K- side: min(wn, 0) (u+ - u-);  K+ side (normal -n): min(-wn, 0) (u- - u+)
+            add(a, np.einsum("kp,kpc,kpn->kcn", dA * np.minimum(wn, 0.0), ub - ua, Phia))
+            add(b, np.einsum("kp,kpc,kpn->kcn", dA * np.minimum(-wn, 0.0), ua - ub, Phib))
+    # boundary faces: Dirichlet ({{w}} = 0) and Neumann (no jump) contribute nothing
+    return y.reshape(-1) if full else y

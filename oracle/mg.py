@@ -153,3 +153,61 @@ def pcg(apply, b, x0, precond, rtol, maxit):
         p = z + (rz_new / rz) * p
         rz = rz_new
     return x, it, rn / bn
+
+
+def gmres(apply, b, x0, precond, rtol, restart, maxit):
+    """Restarted GMRES(m) with right preconditioning and modified Gram-Schmidt Arnoldi (Saad,
+    Iterative Methods, Alg. 9.5) — the Krylov solver for the non-symmetric viscous step with the
+    convective term:
+      r = b - A x; beta = ||r||; V_1 = r/beta
+      for j = 1..m: z_j = P V_j; w = A z_j; h_ij = (w, V_i), w -= h_ij V_i (i <= j); h_{j+1,j} = ||w||
+        Givens-rotate column j; |g_{j+1}| = ||b - A x_j||; stop at rtol ||b||
+      x += P (V y),  y from the triangular solve;  restart.
+    Returns (x, total iterations, ||r|| / ||b||)."""
+    x = np.array(x0, dtype=np.float64, copy=True)
+    bn = np.linalg.norm(b)
+    if bn == 0.0:
+        return x, 0, 0.0
+    total = 0
+    r = b - apply(x)
+    rn = np.linalg.norm(r)
+    while rn > rtol * bn and total < maxit:
+        m = min(restart, maxit - total)
+        V = np.zeros((m + 1, len(b)))
+        Z = np.zeros((m, len(b)))
+        H = np.zeros((m + 1, m))
+        cs, sn = np.zeros(m), np.zeros(m)
+        g = np.zeros(m + 1)
+        g[0] = rn
+        V[0] = r / rn
+        j_done = 0
+        for j in range(m):
+            Z[j] = precond(V[j])
+            wv = apply(Z[j])
+            for i in range(j + 1):
+                H[i, j] = wv @ V[i]
+                wv = wv - H[i, j] * V[i]
+            H[j + 1, j] = np.linalg.norm(wv)
+            if H[j + 1, j] > 0:
+                V[j + 1] = wv / H[j + 1, j]
+            for i in range(j):                       # apply the previous rotations
+                t = cs[i] * H[i, j] + sn[i] * H[i + 1, j]
+                H[i + 1, j] = -sn[i] * H[i, j] + cs[i] * H[i + 1, j]
+                H[i, j] = t
+            den = np.hypot(H[j, j], H[j + 1, j])
+            cs[j], sn[j] = H[j, j] / den, H[j + 1, j] / den
+            H[j, j] = den
+            H[j + 1, j] = 0.0
+            g[j + 1] = -sn[j] * g[j]
+            g[j] = cs[j] * g[j]
+            total += 1
+            j_done = j + 1
+            if abs(g[j + 1]) <= rtol * bn:
+                break
+        yk = np.zeros(j_done)
+        for i in range(j_done - 1, -1, -1):
+            yk[i] = (g[i] - H[i, i + 1:j_done] @ yk[i + 1:]) / H[i, i]
+        x = x + yk @ Z[:j_done]
+        r = b - apply(x)
+        rn = np.linalg.norm(r)
+    return x, total, rn / bn
