@@ -173,6 +173,40 @@ dgvv_status dgvv_cg_solve(dgvv_ctx* ctx, int32_t op, const double* b, double* x,
                           int32_t maxit, int32_t precond, const double* lambda_hi_per_level,
                           int32_t* iters, double* relres, dgvv_stream stream);
 
+/* Upwind DG convective term (eqn:convective_term_weak),
+ * homogeneous part on level 0, linear in u for the transport field w:
+ *   c_h^e(v, u; w) = (v, (w.grad) u)_e + (v, min({{w}}.n, 0) (u(neighbour) - u(e)))_{boundary of e}
+ * i.e. the central flux {{w}}.n u plus the upwind correction 1/2 |{{w}}.n| [[u]] (u^dag =
+ * {{u}} + 1/2 sign({{w}}.n)[[u]]) written per cell side.  Readings F4a-F4c: the
+ * (w.grad)u form; Dirichlet faces take the mirror states u+ = -u, w+ = -w (homogeneous data),
+ * so {{w}}.n = 0 there; Neumann faces have no jump; both contribute nothing.
+ * dgvv_set_transport copies w (device, level-0 vector layout [cell][3][n^3]; the library keeps
+ * its own copy and, multi-GPU, exchanges its ghosts once; external-exchange mode: fill the
+ * DGVV_GHOST_TRANSPORT buffer).  Synchronous; DGVV_EDOMAIN for non-finite entries.
+ * dgvv_apply_convective: dst = C(w) src (DGVV_ESTATE before dgvv_set_transport). */
+dgvv_status dgvv_set_transport(dgvv_ctx* ctx, const double* w, dgvv_stream stream);
+dgvv_status dgvv_apply_convective(dgvv_ctx* ctx, const double* src, double* dst, dgvv_stream stream);
+
+/* The viscous-step operator with linearly implicit convection (eqn:viscous_step_with_convection,
+ * PAPER.md:525-554, variant ii with u* = w):  dst = (mass M + A(nu) + alpha_c C(w)) src on level 0,
+ * mass from dgvv_set_mass(DGVV_OP_VISCOUS, gamma_0 / dt).  alpha_c = 0 gives the Helmholtz form. */
+dgvv_status dgvv_apply_oseen(dgvv_ctx* ctx, double alpha_c, const double* src, double* dst,
+                             dgvv_stream stream);
+
+/* Right-preconditioned restarted GMRES(restart) on that non-symmetric operator (
+ * Saad Alg. 9.5 with modified Gram-Schmidt):
+ *   r = b - A x; V_1 = r/||r||; for j: z_j = P V_j, w = A z_j, h_ij = (w, V_i), w -= h_ij V_i,
+ *   h_{j+1,j} = ||w||, Givens rotation, |g_{j+1}| = ||b - A x_j||, stop at rtol ||b||;
+ *   x += Z y; restart.  P: none, Jacobi, or one (FP64 / FP32) V-cycle of the symmetric part
+ *   mass M + A(nu) (the convective term is not in the preconditioner).  1 <= restart <= 200;
+ *   the library owns 2 restart + 3 work vectors.  Synchronous (one host read per iteration);
+ *   *iters = total inner iterations, *relres = ||b - A x|| / ||b|| (recomputed).  Multi-GPU:
+ *   collective, dots allreduced. */
+dgvv_status dgvv_gmres_solve(dgvv_ctx* ctx, double alpha_c, const double* b, double* x, double rtol,
+                             int32_t restart, int32_t maxit, int32_t precond,
+                             const double* lambda_hi_per_level, int32_t* iters, double* relres,
+                             dgvv_stream stream);
+
 /* dst = 1 / diag(A) for op = DGVV_OP_* on `level`. */
 dgvv_status dgvv_inverse_diagonal(dgvv_ctx* ctx, int32_t op, int32_t level, double* dst,
                                   dgvv_stream stream);
@@ -237,7 +271,7 @@ dgvv_status dgvv_coefficient_range(dgvv_ctx* ctx, int32_t op, int32_t level, dou
  * internal stream while the interior cells are computed; the cells with a ghost neighbour
  * run after the exchange.  Without a communicator (external-exchange mode) the caller fills
  * the ghost buffers itself, using dgvv_pack_ghosts on the peer's context. */
-enum { DGVV_GHOST_VISCOUS = 0, DGVV_GHOST_POISSON = 1, DGVV_GHOST_ULIN = 2 };
+enum { DGVV_GHOST_VISCOUS = 0, DGVV_GHOST_POISSON = 1, DGVV_GHOST_ULIN = 2, DGVV_GHOST_TRANSPORT = 3 };
 /* Peers in ascending rank; arrays (may be NULL) sized by a first call that only reads n_peers. */
 dgvv_status dgvv_ghost_layout(const dgvv_ctx* ctx, int32_t* n_peers, int32_t* peer_ranks,
                               int32_t* send_counts, int32_t* recv_counts);

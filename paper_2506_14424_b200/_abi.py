@@ -20,7 +20,7 @@ LAW_CONST, LAW_SIN3, LAW_EXP, LAW_CARREAU = 0, 1, 2, 3
 OP_VISCOUS, OP_POISSON, OP_PENALTY = 0, 1, 2
 PRECOND_NONE, PRECOND_JACOBI, PRECOND_VCYCLE, PRECOND_VCYCLE_FP32 = 0, 1, 2, 3
 FORM_DIVERGENCE, FORM_LAPLACE = 0, 1
-GHOST_VISCOUS, GHOST_POISSON, GHOST_ULIN = 0, 1, 2
+GHOST_VISCOUS, GHOST_POISSON, GHOST_ULIN, GHOST_TRANSPORT = 0, 1, 2, 3
 
 
 class DgvvLaw(C.Structure):
@@ -59,6 +59,10 @@ _SIGS = {
     "dgvv_set_penalty_parameters": [VP, PD, PD],
     "dgvv_apply_penalty": [VP, VP, VP, VP],
     "dgvv_cg_solve": [VP, I32, VP, VP, D, I32, I32, PD, C.POINTER(I32), PD, VP],
+    "dgvv_set_transport": [VP, VP, VP],
+    "dgvv_apply_convective": [VP, VP, VP, VP],
+    "dgvv_apply_oseen": [VP, D, VP, VP, VP],
+    "dgvv_gmres_solve": [VP, D, VP, VP, D, I32, I32, I32, PD, C.POINTER(I32), PD, VP],
     "dgvv_apply_linearized_viscous": [VP, VP, VP, VP],
     "dgvv_apply_poisson": [VP, I32, VP, VP, VP],
     "dgvv_inverse_diagonal": [VP, I32, I32, VP, VP],

@@ -338,7 +338,7 @@ __global__ void ew_mul_kernel(const double* a, const double* b, double* out, lon
 // y = alpha x + beta y  (CG updates)
 __global__ void axpby_kernel(double alpha, const double* x, double beta, double* y, long n) {
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
-    y[i] = alpha * x[i] + beta * y[i];
+    y[i] = beta == 0.0 ? alpha * x[i] : alpha * x[i] + beta * y[i];   // beta = 0: y is not read (BLAS)
 }
 // out = sqrt(a)
 __global__ void ew_sqrt_kernel(const double* a, double* out, long n) {
@@ -356,6 +356,12 @@ __global__ void lanczos_update_kernel(double* w, const double* q, const double* 
   const double al = *alpha, be = *beta_prev;
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
     w[i] = w[i] - al * q[i] - be * qprev[i];
+}
+// y += sgn * coef[0] * x (coefficient read on the device: GMRES Gram-Schmidt without a host sync)
+__global__ void axpy_dev_kernel(const double* coef, double sgn, const double* x, double* y, long n) {
+  const double a = sgn * *coef;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+    y[i] = fma(a, x[i], y[i]);
 }
 // q_new = w / s (s = device scalar norm)
 __global__ void scale_by_inv_kernel(const double* w, const double* s2, double* q, long n) {

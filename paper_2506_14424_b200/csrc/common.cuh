@@ -90,6 +90,24 @@ struct PenaltyArgs {
   const double* tau_cont;   // [n_total]
 };
 
+// f4 convective term (convective_apply.cuh): dst += alpha C(w) src
+struct ConvArgs {
+  const double* src;
+  const double* ghost;
+  const double* w;
+  const double* wghost;
+  double* dst;
+  const int* nbr;
+  int n_proc, n_owned, cell_base;
+  const double* cart;
+  const double* vJi;
+  const double* jxw;
+  const double* fJi;
+  const double* fdA;
+  double alpha;
+  int accumulate;           // 1: dst += alpha C src, 0: dst = alpha C src
+};
+
 struct NuArgs {
   const double* u;          // owned [n_owned][3][n^3]
   const double* ughost;     // ghost [n_ghost][3][n^3]

@@ -216,6 +216,10 @@ cudaError_t launch_lanczos_update(double* w, const double* q, const double* qpre
   lanczos_update_kernel<<<gs_blocks(n), 256, 0, s>>>(w, q, qprev, alpha, beta_prev, n);
   return cudaGetLastError();
 }
+cudaError_t launch_axpy_dev(const double* coef, double sgn, const double* x, double* y, long n, cudaStream_t s) {
+  axpy_dev_kernel<<<gs_blocks(n), 256, 0, s>>>(coef, sgn, x, y, n);
+  return cudaGetLastError();
+}
 cudaError_t launch_scale_by_inv(const double* w, const double* s2, double* q, long n, cudaStream_t s) {
   scale_by_inv_kernel<<<gs_blocks(n), 256, 0, s>>>(w, s2, q, n);
   return cudaGetLastError();

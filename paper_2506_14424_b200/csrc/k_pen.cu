@@ -1,6 +1,7 @@
 // k_pen.cu — instantiations of the penalty-step operator (§8(f) f2): apply and inverse diagonal.
 #include "tu_tables.cuh"
 #include "penalty_apply.cuh"
+#include "convective_apply.cuh"
 #include "launch.h"
 
 namespace dgvv {
@@ -38,6 +39,34 @@ cudaError_t launch_penalty(int n, int geo, const PenaltyArgs& a, bool diag, cuda
     case 4: return geo ? pen_run<4, 1>(a, diag, s) : pen_run<4, 0>(a, diag, s);
     case 5: return geo ? pen_run<5, 1>(a, diag, s) : pen_run<5, 0>(a, diag, s);
     case 6: return geo ? pen_run<6, 1>(a, diag, s) : pen_run<6, 0>(a, diag, s);
+    default: return cudaErrorNotSupported;
+  }
+}
+
+// f4: upwind convective term, accumulated into dst
+template <int n, int GEO>
+static cudaError_t conv_run(const ConvArgs& a, cudaStream_t s) {
+  constexpr int CPB = cpb_pen<n>();
+  const size_t smem = (size_t)CPB * ConvCfg<n>::CS * sizeof(double);
+  auto k = convective_apply_kernel<n, GEO, CPB>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  if (a.n_proc <= 0) return cudaSuccess;
+  k<<<(a.n_proc + CPB - 1) / CPB, CPB * n * n, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_convective(int n, int geo, const ConvArgs& a, cudaStream_t s) {
+  switch (n) {
+    case 2: return geo ? conv_run<2, 1>(a, s) : conv_run<2, 0>(a, s);
+    case 3: return geo ? conv_run<3, 1>(a, s) : conv_run<3, 0>(a, s);
+    case 4: return geo ? conv_run<4, 1>(a, s) : conv_run<4, 0>(a, s);
+    case 5: return geo ? conv_run<5, 1>(a, s) : conv_run<5, 0>(a, s);
+    case 6: return geo ? conv_run<6, 1>(a, s) : conv_run<6, 0>(a, s);
     default: return cudaErrorNotSupported;
   }
 }

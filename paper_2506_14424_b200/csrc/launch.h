@@ -19,6 +19,8 @@ cudaError_t launch_apply(int nc, int n, int form, int geo, const ApplyArgs& a, c
 cudaError_t launch_apply_f(int nc, int n, int form, int geo, const ApplyArgsT<float>& a, cudaStream_t s);
 // f2: divergence/continuity penalty operator (apply, or inverse diagonal when diag = true)
 cudaError_t launch_penalty(int n, int geo, const PenaltyArgs& a, bool diag, cudaStream_t s);
+// f4: dst (+)= alpha C(w) src (upwind convective term)
+cudaError_t launch_convective(int n, int geo, const ConvArgs& a, cudaStream_t s);
 // K2: Newton-linearised viscous apply
 cudaError_t launch_newton(int n, int geo, const ApplyArgs& a, cudaStream_t s);
 // K3: Carreau viscosity at all points
@@ -60,6 +62,7 @@ cudaError_t launch_ew_sqrt(const double* a, double* out, long n, cudaStream_t s)
 cudaError_t launch_ew_div(const double* a, const double* b, double* out, long n, cudaStream_t s);
 cudaError_t launch_lanczos_update(double* w, const double* q, const double* qprev, const double* alpha,
                                   const double* beta_prev, long n, cudaStream_t s);
+cudaError_t launch_axpy_dev(const double* coef, double sgn, const double* x, double* y, long n, cudaStream_t s);
 cudaError_t launch_scale_by_inv(const double* w, const double* s2, double* q, long n, cudaStream_t s);
 cudaError_t launch_gather_cells(const double* src, const int* list, int ncells, int len, double* out,
                                 cudaStream_t s);

@@ -216,6 +216,38 @@ class Context:
         A.check(self._L.dgvv_apply_penalty(self.h, _ptr(src, n, "src"), _ptr(dst, n, "dst"), _stream()))
         return dst
 
+    def set_transport(self, w):
+        """Transport field w of the convective term (dgvv_set_transport; level-0 vector, copied)."""
+        A.check(self._L.dgvv_set_transport(self.h, _ptr(w, 3 * self.n_dofs(0), "w"), _stream()))
+
+    def apply_convective(self, src, dst):
+        """dst = C(w) src, the upwind DG convective term (dgvv_apply_convective)."""
+        n = 3 * self.n_dofs(0)
+        A.check(self._L.dgvv_apply_convective(self.h, _ptr(src, n, "src"), _ptr(dst, n, "dst"), _stream()))
+        return dst
+
+    def apply_oseen(self, src, dst, alpha_c=1.0):
+        """dst = (mass M + A(nu) + alpha_c C(w)) src (dgvv_apply_oseen)."""
+        n = 3 * self.n_dofs(0)
+        A.check(self._L.dgvv_apply_oseen(self.h, float(alpha_c), _ptr(src, n, "src"), _ptr(dst, n, "dst"),
+                                         _stream()))
+        return dst
+
+    def gmres_solve(self, b, x, alpha_c=1.0, rtol=1e-8, restart=30, maxit=300, precond="vcycle",
+                    lam_hi_per_level=None):
+        """Right-preconditioned restarted GMRES on mass M + A(nu) + alpha_c C(w) (dgvv_gmres_solve);
+        x = initial guess in, solution out.  Returns (iterations, ||b - A x|| / ||b||)."""
+        n = 3 * self.n_dofs(0)
+        pc = {"none": A.PRECOND_NONE, "jacobi": A.PRECOND_JACOBI, "vcycle": A.PRECOND_VCYCLE,
+              "vcycle_fp32": A.PRECOND_VCYCLE_FP32}[precond]
+        arr = None
+        if lam_hi_per_level is not None:
+            arr = (C.c_double * len(self.degrees))(*[float(v) for v in lam_hi_per_level])
+        it, rr = C.c_int32(), C.c_double()
+        A.check(self._L.dgvv_gmres_solve(self.h, float(alpha_c), _ptr(b, n, "b"), _ptr(x, n, "x"), float(rtol),
+                                         int(restart), int(maxit), pc, arr, C.byref(it), C.byref(rr), _stream()))
+        return it.value, rr.value
+
     def dot(self, a, b, ncomp=1, level=0):
         out = C.c_double()
         n = ncomp * self.n_dofs(level)
@@ -241,7 +273,7 @@ class Context:
         p = C.c_void_p()
         A.check(self._L.dgvv_ghost_buffer(self.h, level, kind, C.byref(p)))
         k = self.degrees[level]
-        per = (1 if kind == A.GHOST_POISSON else 3) * (k + 1) ** 3
+        per = (1 if kind == A.GHOST_POISSON else 3) * (k + 1) ** 3   # TRANSPORT: 3 components
         return _wrap_device(p.value, n_ghost * per)
 
     def coefficient_range(self, op, level=0):
