@@ -9,5 +9,5 @@ Positions of mapping nodes and of sampling points are produced with library
 primitives (numpy Legendre roots); both the oracle and the CUDA library re-derive
 every quantity they need from these positions with their own code.
 """
-from .meshes import Mesh, cube, deformed_cube, bfs, box_block, config_mesh  # noqa: F401
+from .meshes import Mesh, cube, cube_parent_map, deformed_cube, bfs, box_block, config_mesh  # noqa: F401
 from .vectors import uniform, fourier_modes, fourier_field, node_positions  # noqa: F401

@@ -129,6 +129,19 @@ def cube(N: int, lo=0.0, hi=1.0, bc=DIRICHLET, periodic=(False, False, False), g
     return m
 
 
+def cube_parent_map(N: int):
+    """Nested refinement of cube(N // 2) into cube(N) (cell id = i + N j + N^2 k): the coarse
+    parent id of every fine cell and its octant ox + 2 oy + 4 oz (which half of the parent it
+    occupies along x, y, z).  Index bookkeeping only (h-levels)."""
+    assert N % 2 == 0
+    k, j, i = np.meshgrid(np.arange(N), np.arange(N), np.arange(N), indexing="ij")
+    i, j, k = i.reshape(-1), j.reshape(-1), k.reshape(-1)
+    Nc = N // 2
+    parent = (i // 2) + Nc * (j // 2) + Nc * Nc * (k // 2)
+    octant = (i % 2) + 2 * (j % 2) + 4 * (k % 2)
+    return parent.astype(np.int32), octant.astype(np.int8)
+
+
 def deformed_cube(N: int, map_degree: int, amp: float = 0.05, bc=DIRICHLET, nz_mult: int = 1) -> Mesh:
     """C2: [0,1]^3, N^3 cells, X = x^ + amp sin(2 pi x^) sin(2 pi y^) sin(2 pi z^) (1,1,1),
     sampled at the degree-`map_degree` GLL nodes of every cell (iso-parametric map).

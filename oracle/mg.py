@@ -7,6 +7,9 @@ PAPER.md:1553-1557: V-cycles with a Chebyshev-accelerated Jacobi smoother (Adams
 inverse diagonal precomputed per level, residual via the level operator.
 Readings G12-G15: degree 5, range [lambda_hi/20, lambda_hi], lambda_hi = 1.2 lambda_hat,
 1 pre- + 1 post-smoothing, coarsest level = Chebyshev(5) from 0.
+PAPER.md:1536-1545: after p-coarsening, h-coarsening on the grids "created by
+refining an initial coarse grid" and, on the coarsest level, "a direct solver if the system size
+falls below 2000 DoFs": h-transfer (readings H1-H3) and the direct coarse solve.
 """
 from __future__ import annotations
 
@@ -41,6 +44,42 @@ def restrict(fine, kf, kc, n_cells, ncomp=1):
     return (F @ P).reshape(-1)
 
 
+def h_transfer_1d(k: int) -> np.ndarray:
+    """Ph[o, i_f, j_c] = l^(k)_j((xi_i + o) / 2), o in {0, 1}: the parent's degree-k Lagrange basis
+    (on its Gauss points, G2) evaluated at the Gauss points of the child occupying the half
+    [o/2, (o+1)/2] of the parent's reference interval (reading H1: nested refinement in
+    reference coordinates; P = exact DG embedding of the coarse space, as G18 for p)."""
+    xi, _ = B.gauss01(k + 1)
+    return np.stack([B.lagrange(xi, 0.5 * (xi + o)) for o in (0, 1)])
+
+
+def h_transfer_3d(k: int, octant: int) -> np.ndarray:
+    """Per-child prolongation (n^3 x n^3), lexicographic x fastest; octant = ox + 2 oy + 4 oz."""
+    Ph = h_transfer_1d(k)
+    ox, oy, oz = octant & 1, (octant >> 1) & 1, (octant >> 2) & 1
+    return np.kron(Ph[oz], np.kron(Ph[oy], Ph[ox]))
+
+
+def h_prolongate(coarse, k, parent, octant, ncomp=1):
+    """fine[f, c] = P_{octant[f]} coarse[parent[f], c] (reading H1)."""
+    n3 = (k + 1) ** 3
+    C = np.asarray(coarse).reshape(-1, ncomp, n3)
+    out = np.empty((len(parent), ncomp, n3))
+    for f in range(len(parent)):
+        out[f] = C[parent[f]] @ h_transfer_3d(k, int(octant[f])).T
+    return out.reshape(-1)
+
+
+def h_restrict(fine, k, parent, octant, n_coarse, ncomp=1):
+    """R = P^T: coarse[p, c] = sum over the children f of p of P_{octant[f]}^T fine[f, c] (H2)."""
+    n3 = (k + 1) ** 3
+    F = np.asarray(fine).reshape(-1, ncomp, n3)
+    out = np.zeros((n_coarse, ncomp, n3))
+    for f in range(len(parent)):
+        out[parent[f]] += F[f] @ h_transfer_3d(k, int(octant[f]))
+    return out.reshape(-1)
+
+
 def chebyshev(apply, Dinv, b, x0, lam_lo, lam_hi, m=5):
     """Chebyshev semi-iteration on D^-1 A (Adams 2003 via PAPER.md:1555):
       theta = (hi+lo)/2, delta = (hi-lo)/2, sigma = theta/delta, rho_0 = 1/sigma
@@ -68,10 +107,13 @@ def chebyshev(apply, Dinv, b, x0, lam_lo, lam_hi, m=5):
 def vcycle(levels, b, lvl=None, m=5):
     """V(l, b) per SURVEY.md §8(c) c1.7.  `levels` is finest-first; each entry a dict with
     apply, Dinv, lam_hi, and (except the coarsest) restrict(r) / prolongate(xc) to the next
-    coarser level.  lam_lo = lam_hi / 20 (G12)."""
+    coarser level.  lam_lo = lam_hi / 20 (G12).  If the coarsest entry carries "solve", that
+    direct solve replaces its Chebyshev smoothing (reading H3)."""
     if lvl is None:
         lvl = 0
     L = levels[lvl]
+    if lvl == len(levels) - 1 and "solve" in L:
+        return L["solve"](b)
     lo, hi = L["lam_hi"] / 20.0, L["lam_hi"]
     zero = np.zeros_like(b)
     if lvl == len(levels) - 1:
