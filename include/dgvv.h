@@ -251,6 +251,41 @@ dgvv_status dgvv_restrict(dgvv_ctx* ctx, int32_t op, int32_t fine_level, const d
 dgvv_status dgvv_vcycle(dgvv_ctx* ctx, int32_t op, const double* b, double* x,
                         const double* lambda_hi_per_level, dgvv_stream stream);
 
+/* h-levels of the cph hierarchy (after p-coarsening,
+ * "h-coarsening is performed … the individual h-levels are created by refining an initial coarse
+ * grid").  `coarse` is a context on the mesh whose refinement is `fine`'s mesh (every coarse cell
+ * split into 2 x 2 x 2 children); its finest degree must equal `fine`'s coarsest degree.
+ * parent[f] (host, [fine n_cells]) = local id of the coarse cell containing fine cell f,
+ * octant[f] = ox + 2 oy + 4 oz = which half of the parent's reference interval [0,1] the child
+ * occupies along each reference axis; every coarse cell needs exactly one child per octant.
+ * The transfer (reading H1) is the exact DG embedding in reference coordinates:
+ * P|child = Ph[oz] (x) Ph[oy] (x) Ph[ox], Ph[o][i][j] = l_j((xi_i + o) / 2) (parent's Lagrange basis
+ * at the child's Gauss points); R = P^T (H2).  After the call every V-cycle on `fine` (dgvv_vcycle,
+ * the V-cycle preconditioners of dgvv_cg_solve / dgvv_gmres_solve) continues below fine's
+ * coarsest p-level into `coarse`'s levels (recursively, if `coarse` has a coarse context), and
+ * lambda_hi_per_level lists every level of that chain in order.  `coarse` is borrowed: keep it
+ * alive while `fine` is used; its coefficients/mass are its own (set them consistently).
+ * Single-GPU contexts only (DGVV_EUNSUPPORTED with ghosts); the FP32 V-cycle does not follow the
+ * chain (DGVV_EUNSUPPORTED). */
+dgvv_status dgvv_set_coarse_context(dgvv_ctx* fine, dgvv_ctx* coarse, const int32_t* parent,
+                                    const int8_t* octant);
+/* fine = P coarse + beta fine (fine's coarsest level <- coarse's level 0), op selects 3 or 1
+ * components; coarse = P^T fine + beta coarse.  DGVV_ESTATE without a coarse context. */
+dgvv_status dgvv_prolongate_h(dgvv_ctx* fine, int32_t op, const double* coarse_vec, double* fine_vec,
+                              double beta, dgvv_stream stream);
+dgvv_status dgvv_restrict_h(dgvv_ctx* fine, int32_t op, const double* fine_vec, double* coarse_vec,
+                            double beta, dgvv_stream stream);
+
+/* Direct coarse solver ("a direct solver if the system size falls below 2000
+ * DoFs"; reading H3): assembles the operator of ctx's coarsest level (with its mass term) column
+ * by column from the matrix-free apply, inverts it on the GPU by Gauss-Jordan elimination (SPD:
+ * no pivoting; DGVV_EDOMAIN on a non-positive pivot) and from then on replaces the coarsest
+ * level's Chebyshev smoothing in every V-cycle that ends on this context by x = A^-1 b (dense
+ * matvec).  At most 4096 DoFs (ncomp x level DoFs).  Synchronous.  A later change of the
+ * coefficients or mass makes it stale: V-cycles then fail with DGVV_ESTATE until it is set up
+ * again.  *n_dofs (may be NULL) = the system size. */
+dgvv_status dgvv_setup_coarse_solver(dgvv_ctx* ctx, int32_t op, int32_t* n_dofs);
+
 /* out_host = sum over all ranks of a.b over `ncomp` * level-dofs entries. Synchronous. */
 dgvv_status dgvv_dot(dgvv_ctx* ctx, int32_t level, int32_t ncomp, const double* a,
                      const double* b, double* out_host, dgvv_stream stream);

@@ -60,6 +60,10 @@ _SIGS = {
     "dgvv_apply_penalty": [VP, VP, VP, VP],
     "dgvv_cg_solve": [VP, I32, VP, VP, D, I32, I32, PD, C.POINTER(I32), PD, VP],
     "dgvv_set_transport": [VP, VP, VP],
+    "dgvv_set_coarse_context": [VP, VP, C.POINTER(I32), C.POINTER(C.c_int8)],
+    "dgvv_prolongate_h": [VP, I32, VP, VP, D, VP],
+    "dgvv_restrict_h": [VP, I32, VP, VP, D, VP],
+    "dgvv_setup_coarse_solver": [VP, I32, C.POINTER(I32)],
     "dgvv_apply_convective": [VP, VP, VP, VP],
     "dgvv_apply_oseen": [VP, D, VP, VP, VP],
     "dgvv_gmres_solve": [VP, D, VP, VP, D, I32, I32, I32, PD, C.POINTER(I32), PD, VP],

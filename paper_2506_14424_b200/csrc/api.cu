@@ -177,6 +177,16 @@ struct dgvv_ctx {
   double* gm_work = nullptr;                 // r, w, V[0..m], Z[0..m-1]
   int gm_restart = 0;
   double* gm_H = nullptr;                    // device Hessenberg column
+  // f3: h-levels (a coarser context below the coarsest p-level) and the direct coarse solver
+  dgvv_ctx* coarse = nullptr;
+  int* d_parent = nullptr;                   // [n_owned] coarse cell of each fine cell
+  signed char* d_octant = nullptr;           // [n_owned] ox + 2 oy + 4 oz
+  int* d_child = nullptr;                    // [coarse n_owned][8]
+  double* hb[2] = {nullptr, nullptr};        // coarse-level right-hand side / solution per op
+  double* hx[2] = {nullptr, nullptr};
+  double* Ainv[2] = {nullptr, nullptr};      // dense inverse of the coarsest level per op
+  int direct_n[2] = {0, 0};
+  int direct_epoch[2] = {-1, -1};            // coef_epoch the inverse was built at
   std::vector<int> h_gperm;                  // internal ghost i -> mesh ghost row
   std::vector<LevelF> LF;                    // FP32 levels (lazily built)
   float* d_cart_f = nullptr;
@@ -1107,21 +1117,41 @@ dgvv_status dgvv_restrict(dgvv_ctx* c, int32_t op, int32_t fine_level, const dou
   return transfer(c, op, fine_level, fine, coarse, beta, false, (cudaStream_t)stream);
 }
 
+static dgvv_status hprolong_impl(dgvv_ctx* c, int op, const double* coarse, double* fine, double beta,
+                                 cudaStream_t s);
+static dgvv_status hrestrict_impl(dgvv_ctx* c, int op, const double* fine, double* coarse, double beta,
+                                  cudaStream_t s);
+
+// V(l, b) of SURVEY §8(c) c1.7 over the chain of contexts (p-levels of c, then — f3 — the levels
+// of c->coarse after an h-transfer); the coarsest level of the chain is either Chebyshev(5) from
+// 0 (G15) or, after dgvv_setup_coarse_solver, the direct solve (reading H3).
 static dgvv_status vcycle_rec(dgvv_ctx* c, int op, int l, const double* b, double* x, const double* his,
                               cudaStream_t s) {
   const int oi = op == DGVV_OP_VISCOUS ? 0 : 1;
   auto& S = c->L[l].scratch[oi];   // [0] r, [1..2] work, (l>0: [3] b, [4] x of coarser handled by caller)
-  const double hi = his[l], lo = hi / 20.0;
   const int last = (int)c->L.size() - 1;
+  if (l == last && !c->coarse && c->Ainv[oi]) {
+    if (c->direct_epoch[oi] != c->coef_epoch)
+      return dgvv_fail(DGVV_ESTATE, "direct coarse solver is stale (coefficients or mass changed): call dgvv_setup_coarse_solver again");
+    DGVV_CUDA_TRY(launch_dense_matvec(c->Ainv[oi], b, x, c->direct_n[oi], s));
+    return DGVV_OK;
+  }
+  const double hi = his[l], lo = hi / 20.0;
   TRY(cheb_impl(c, op, l, x, b, 5, lo, hi, 1, S[1], s));
-  if (l == last) return DGVV_OK;
+  if (l == last && !c->coarse) return DGVV_OK;
   ApplyArgs a = base_args(c, l, op);
   a.src = x; a.dst = S[0]; a.b = b; a.mode = MODE_RESID;
   TRY(run_apply(c, op, l, a, s));
-  auto& C = c->L[l + 1].scratch[oi];
-  TRY(transfer(c, op, l, S[0], C[3], 0.0, false, s));
-  TRY(vcycle_rec(c, op, l + 1, C[3], C[4], his, s));
-  TRY(transfer(c, op, l, C[4], x, 1.0, true, s));
+  if (l < last) {
+    auto& C = c->L[l + 1].scratch[oi];
+    TRY(transfer(c, op, l, S[0], C[3], 0.0, false, s));
+    TRY(vcycle_rec(c, op, l + 1, C[3], C[4], his, s));
+    TRY(transfer(c, op, l, C[4], x, 1.0, true, s));
+  } else {                                     // h-coarsening into the coarser context
+    TRY(hrestrict_impl(c, op, S[0], c->hb[oi], 0.0, s));
+    TRY(vcycle_rec(c->coarse, op, 0, c->hb[oi], c->hx[oi], his + c->L.size(), s));
+    TRY(hprolong_impl(c, op, c->hx[oi], x, 1.0, s));
+  }
   TRY(cheb_impl(c, op, l, x, b, 5, lo, hi, 0, S[1], s));
   return DGVV_OK;
 }
@@ -1273,6 +1303,7 @@ static dgvv_status vcycle_rec_f(dgvv_ctx* c, int op, int l, const float* b, floa
 
 // z = V_fp32(r) for FP64 vectors (conversion in and out)
 static dgvv_status vcycle_fp32_d(dgvv_ctx* c, int op, const double* r, double* z, const double* his, cudaStream_t s) {
+  if (c->coarse) return dgvv_fail(DGVV_EUNSUPPORTED, "FP32 V-cycle: h-levels (dgvv_set_coarse_context) not supported");
   TRY(ensure_fp32(c, op, s));
   const int oi = op == DGVV_OP_VISCOUS ? 0 : 1;
   const long N = (long)(op == DGVV_OP_VISCOUS ? 3 : 1) * level_dofs(c, 0);
@@ -1290,23 +1321,13 @@ dgvv_status dgvv_vcycle_fp32(dgvv_ctx* c, int32_t op, const double* b, double* x
   return vcycle_fp32_d(c, op, b, x, his, (cudaStream_t)stream);
 }
 
+static dgvv_status ensure_vcycle_scratch(dgvv_ctx* c, int op);
+
 dgvv_status dgvv_vcycle(dgvv_ctx* c, int32_t op, const double* b, double* x, const double* his,
                         dgvv_stream stream) {
   if (!c || !b || !x || !his) return dgvv_fail(DGVV_EINVAL, "null argument");
   TRY(op_ready(c, op));
-  const int oi = op == DGVV_OP_VISCOUS ? 0 : 1;
-  const int nc = op == DGVV_OP_VISCOUS ? 3 : 1;
-  for (size_t l = 0; l < c->L.size(); ++l) {
-    auto& S = c->L[l].scratch[oi];
-    if (S.empty()) {
-      const size_t N = (size_t)nc * level_dofs(c, (int)l);
-      S.resize(5, nullptr);
-      TRY(dalloc(c, &S[0], N));
-      TRY(dalloc(c, &S[1], 2 * N));
-      S[2] = S[1] + N;
-      if (l > 0) { TRY(dalloc(c, &S[3], N)); TRY(dalloc(c, &S[4], N)); }
-    }
-  }
+  TRY(ensure_vcycle_scratch(c, op));
   return vcycle_rec(c, op, 0, b, x, his, (cudaStream_t)stream);
 }
 
@@ -1325,6 +1346,13 @@ static dgvv_status ensure_vcycle_scratch(dgvv_ctx* c, int op) {
       S[2] = S[1] + Nl;
       if (l > 0) { TRY(dalloc(c, &S[3], Nl)); TRY(dalloc(c, &S[4], Nl)); }
     }
+  }
+  if (c->coarse) {                              // f3: the chain continues in the coarser context
+    TRY(op_ready(c->coarse, op));
+    const size_t Nc = (size_t)nc * level_dofs(c->coarse, 0);
+    if (!c->hb[oi]) TRY(dalloc(c, &c->hb[oi], Nc));
+    if (!c->hx[oi]) TRY(dalloc(c, &c->hx[oi], Nc));
+    TRY(ensure_vcycle_scratch(c->coarse, op));
   }
   return DGVV_OK;
 }
@@ -1676,6 +1704,125 @@ dgvv_status dgvv_gmres_solve(dgvv_ctx* c, double alpha_c, const double* b, doubl
   }
   if (iters) *iters = total;
   if (relres) *relres = bn > 0.0 ? rn / bn : 0.0;
+  return DGVV_OK;
+}
+
+// ------------------------------------------------------------------ f3: h-levels, direct coarse solve
+static dgvv_status hprolong_impl(dgvv_ctx* c, int op, const double* coarse, double* fine, double beta,
+                                 cudaStream_t s) {
+  const int nc = op == DGVV_OP_VISCOUS ? 3 : 1;
+  cudaError_t e = launch_hprolongate(c->L.back().n, nc, coarse, fine, c->d_parent, c->d_octant, beta, c->n_owned, s);
+  if (e == cudaErrorNotSupported) return dgvv_fail(DGVV_EUNSUPPORTED, "h-transfer not built for degree %d", c->L.back().k);
+  if (e != cudaSuccess) return dgvv_fail(DGVV_ECUDA, "h-prolongation: %s", cudaGetErrorString(e));
+  return DGVV_OK;
+}
+
+static dgvv_status hrestrict_impl(dgvv_ctx* c, int op, const double* fine, double* coarse, double beta,
+                                  cudaStream_t s) {
+  const int nc = op == DGVV_OP_VISCOUS ? 3 : 1;
+  cudaError_t e = launch_hrestrict(c->L.back().n, nc, fine, coarse, c->d_child, beta, c->coarse->n_owned, s);
+  if (e == cudaErrorNotSupported) return dgvv_fail(DGVV_EUNSUPPORTED, "h-transfer not built for degree %d", c->L.back().k);
+  if (e != cudaSuccess) return dgvv_fail(DGVV_ECUDA, "h-restriction: %s", cudaGetErrorString(e));
+  return DGVV_OK;
+}
+
+dgvv_status dgvv_set_coarse_context(dgvv_ctx* c, dgvv_ctx* cc, const int32_t* parent, const int8_t* octant) {
+  if (!c || !cc || !parent || !octant) return dgvv_fail(DGVV_EINVAL, "null argument");
+  if (c == cc) return dgvv_fail(DGVV_EINVAL, "a context cannot be its own coarse level");
+  for (dgvv_ctx* q = cc; q; q = q->coarse)
+    if (q == c) return dgvv_fail(DGVV_EINVAL, "coarse-context chain would form a cycle");
+  if (c->n_ghost || cc->n_ghost || c->comm || cc->comm)
+    return dgvv_fail(DGVV_EUNSUPPORTED, "h-levels: single-GPU contexts only in this build");
+  if (cc->L[0].k != c->L.back().k)
+    return dgvv_fail(DGVV_EINVAL, "coarse context degree %d != coarsest level degree %d", cc->L[0].k, c->L.back().k);
+  const int nf = c->n_owned, ncs = cc->n_owned;
+  if ((long)ncs * 8 != (long)nf) return dgvv_fail(DGVV_EINVAL, "fine cells (%d) != 8 x coarse cells (%d)", nf, ncs);
+  std::vector<int> child((size_t)ncs * 8, -1);
+  for (int f = 0; f < nf; ++f) {
+    const int p = parent[f], o = octant[f];
+    if (p < 0 || p >= ncs || o < 0 || o > 7) return dgvv_fail(DGVV_EINVAL, "fine cell %d: parent %d / octant %d out of range", f, p, o);
+    if (child[(size_t)p * 8 + o] >= 0) return dgvv_fail(DGVV_EINVAL, "coarse cell %d has two children in octant %d", p, o);
+    child[(size_t)p * 8 + o] = f;
+  }
+  if (!c->d_parent) TRY(dalloc(c, &c->d_parent, (size_t)nf));
+  if (!c->d_octant) TRY(dalloc(c, &c->d_octant, (size_t)nf));
+  if (!c->d_child) TRY(dalloc(c, &c->d_child, (size_t)ncs * 8));
+  DGVV_CUDA_TRY(cudaMemcpy(c->d_parent, parent, nf * sizeof(int), cudaMemcpyHostToDevice));
+  DGVV_CUDA_TRY(cudaMemcpy(c->d_octant, octant, nf, cudaMemcpyHostToDevice));
+  DGVV_CUDA_TRY(cudaMemcpy(c->d_child, child.data(), child.size() * sizeof(int), cudaMemcpyHostToDevice));
+  if (c->coarse != cc) {
+    for (int o = 0; o < 2; ++o)
+      for (double** pp : {&c->hb[o], &c->hx[o]})
+        if (*pp) {
+          cudaFree(*pp);
+          c->allocs.erase(std::remove(c->allocs.begin(), c->allocs.end(), (void*)*pp), c->allocs.end());
+          *pp = nullptr;
+        }
+  }
+  c->coarse = cc;
+  return DGVV_OK;
+}
+
+static dgvv_status h_ready(dgvv_ctx* c, int op) {
+  if (!c) return dgvv_fail(DGVV_EINVAL, "null context");
+  if (!c->coarse) return dgvv_fail(DGVV_ESTATE, "no coarse context: call dgvv_set_coarse_context first");
+  if (op != DGVV_OP_VISCOUS && op != DGVV_OP_POISSON) return dgvv_fail(DGVV_EINVAL, "unknown op %d", op);
+  return DGVV_OK;
+}
+
+dgvv_status dgvv_prolongate_h(dgvv_ctx* c, int32_t op, const double* coarse, double* fine, double beta,
+                              dgvv_stream stream) {
+  TRY(h_ready(c, op));
+  if (!coarse || !fine) return dgvv_fail(DGVV_EINVAL, "null vector");
+  return hprolong_impl(c, op, coarse, fine, beta, (cudaStream_t)stream);
+}
+
+dgvv_status dgvv_restrict_h(dgvv_ctx* c, int32_t op, const double* fine, double* coarse, double beta,
+                            dgvv_stream stream) {
+  TRY(h_ready(c, op));
+  if (!coarse || !fine) return dgvv_fail(DGVV_EINVAL, "null vector");
+  return hrestrict_impl(c, op, fine, coarse, beta, (cudaStream_t)stream);
+}
+
+dgvv_status dgvv_setup_coarse_solver(dgvv_ctx* c, int32_t op, int32_t* n_dofs) {
+  if (!c) return dgvv_fail(DGVV_EINVAL, "null context");
+  if (op != DGVV_OP_VISCOUS && op != DGVV_OP_POISSON) return dgvv_fail(DGVV_EINVAL, "unknown op %d", op);
+  TRY(op_ready(c, op));
+  if (c->n_ghost || c->comm) return dgvv_fail(DGVV_EUNSUPPORTED, "direct coarse solver: single-GPU contexts only");
+  const int oi = op == DGVV_OP_VISCOUS ? 0 : 1;
+  const int nc = op == DGVV_OP_VISCOUS ? 3 : 1;
+  const int l = (int)c->L.size() - 1;
+  const long N = (long)nc * level_dofs(c, l);
+  if (N > 4096) return dgvv_fail(DGVV_EINVAL, "direct coarse solver: %ld DoFs on the coarsest level (max 4096)", N);
+  cudaStream_t s = 0;
+  double *cols = nullptr, *W = nullptr, *fac = nullptr, *e = nullptr;
+  struct Tmp { double** p[4]; ~Tmp() { for (auto q : p) if (*q) cudaFree(*q); } } tmp{{&cols, &W, &fac, &e}};
+  DGVV_CUDA_TRY(cudaMalloc(&cols, (size_t)N * N * sizeof(double)));
+  DGVV_CUDA_TRY(cudaMalloc(&W, (size_t)2 * N * N * sizeof(double)));
+  DGVV_CUDA_TRY(cudaMalloc(&fac, (size_t)N * sizeof(double)));
+  DGVV_CUDA_TRY(cudaMalloc(&e, (size_t)N * sizeof(double)));
+  for (long j = 0; j < N; ++j) {               // column j = A e_j (the level's matrix-free apply)
+    DGVV_CUDA_TRY(launch_set_unit(e, N, j, s));
+    ApplyArgs a = base_args(c, l, op);
+    a.src = e;
+    a.dst = cols + (size_t)j * N;
+    TRY(run_apply(c, op, l, a, s));
+  }
+  if (!c->Ainv[oi]) TRY(dalloc(c, &c->Ainv[oi], (size_t)N * N));
+  DGVV_CUDA_TRY(cudaMemsetAsync(c->d_flag, 0, sizeof(int), s));
+  DGVV_CUDA_TRY(launch_gauss_jordan_inverse(cols, W, fac, c->Ainv[oi], (int)N, c->d_flag, s));
+  int bad = 0;
+  DGVV_CUDA_TRY(cudaMemcpyAsync(&bad, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+  DGVV_CUDA_TRY(cudaStreamSynchronize(s));
+  if (bad) {
+    cudaFree(c->Ainv[oi]);
+    c->allocs.erase(std::remove(c->allocs.begin(), c->allocs.end(), (void*)c->Ainv[oi]), c->allocs.end());
+    c->Ainv[oi] = nullptr;
+    return dgvv_fail(DGVV_EDOMAIN, "direct coarse solver: %d non-positive pivots (operator not SPD?)", bad);
+  }
+  c->direct_n[oi] = (int)N;
+  c->direct_epoch[oi] = c->coef_epoch;
+  if (n_dofs) *n_dofs = (int32_t)N;
   return DGVV_OK;
 }
 

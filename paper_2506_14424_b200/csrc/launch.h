@@ -21,6 +21,16 @@ cudaError_t launch_apply_f(int nc, int n, int form, int geo, const ApplyArgsT<fl
 cudaError_t launch_penalty(int n, int geo, const PenaltyArgs& a, bool diag, cudaStream_t s);
 // f4: dst (+)= alpha C(w) src (upwind convective term)
 cudaError_t launch_convective(int n, int geo, const ConvArgs& a, cudaStream_t s);
+// f3: h-transfer between nested refinements (octant = ox + 2 oy + 4 oz; child[p * 8 + octant])
+cudaError_t launch_hprolongate(int n, int nc, const double* coarse, double* fine, const int* parent,
+                               const signed char* octant, double beta, int n_fine, cudaStream_t s);
+cudaError_t launch_hrestrict(int n, int nc, const double* fine, double* coarse, const int* child, double beta,
+                             int n_coarse, cudaStream_t s);
+// f3: dense direct coarse solver (Gauss-Jordan inverse of the assembled operator, dense matvec)
+cudaError_t launch_set_unit(double* v, long n, long j, cudaStream_t s);
+cudaError_t launch_gauss_jordan_inverse(const double* cols, double* W, double* fac, double* Ainv, int N, int* bad,
+                                        cudaStream_t s);
+cudaError_t launch_dense_matvec(const double* Ainv, const double* b, double* x, int N, cudaStream_t s);
 // K2: Newton-linearised viscous apply
 cudaError_t launch_newton(int n, int geo, const ApplyArgs& a, cudaStream_t s);
 // K3: Carreau viscosity at all points

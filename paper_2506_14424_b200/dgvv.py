@@ -174,7 +174,7 @@ class Context:
 
     def vcycle(self, op, b, x, lam_hi_per_level):
         n = self._n(op, 0)
-        arr = (C.c_double * len(self.degrees))(*[float(v) for v in lam_hi_per_level])
+        arr = self._lams(lam_hi_per_level)
         A.check(self._L.dgvv_vcycle(self.h, op, _ptr(b, n, "b"), _ptr(x, n, "x"), arr, _stream()))
         return x
 
@@ -190,7 +190,7 @@ class Context:
               "vcycle_fp32": A.PRECOND_VCYCLE_FP32}[precond]
         arr = None
         if lam_hi_per_level is not None:
-            arr = (C.c_double * len(self.degrees))(*[float(v) for v in lam_hi_per_level])
+            arr = self._lams(lam_hi_per_level)
         it, rr = C.c_int32(), C.c_double()
         A.check(self._L.dgvv_cg_solve(self.h, op, _ptr(b, n, "b"), _ptr(x, n, "x"), float(rtol), int(maxit), pc,
                                       arr, C.byref(it), C.byref(rr), _stream()))
@@ -199,7 +199,7 @@ class Context:
     def vcycle_fp32(self, op, b, x, lam_hi_per_level):
         """x = V(b) with all multigrid levels in FP32 (dgvv_vcycle_fp32); b, x FP64 device vectors."""
         n = self._n(op, 0)
-        arr = (C.c_double * len(self.degrees))(*[float(v) for v in lam_hi_per_level])
+        arr = self._lams(lam_hi_per_level)
         A.check(self._L.dgvv_vcycle_fp32(self.h, op, _ptr(b, n, "b"), _ptr(x, n, "x"), arr, _stream()))
         return x
 
@@ -242,11 +242,52 @@ class Context:
               "vcycle_fp32": A.PRECOND_VCYCLE_FP32}[precond]
         arr = None
         if lam_hi_per_level is not None:
-            arr = (C.c_double * len(self.degrees))(*[float(v) for v in lam_hi_per_level])
+            arr = self._lams(lam_hi_per_level)
         it, rr = C.c_int32(), C.c_double()
         A.check(self._L.dgvv_gmres_solve(self.h, float(alpha_c), _ptr(b, n, "b"), _ptr(x, n, "x"), float(rtol),
                                          int(restart), int(maxit), pc, arr, C.byref(it), C.byref(rr), _stream()))
         return it.value, rr.value
+
+    def chain_levels(self):
+        """Number of multigrid levels of the chain (own p-levels + those of the coarse contexts)."""
+        c, n = self, 0
+        while c is not None:
+            n += len(c.degrees)
+            c = getattr(c, "_coarse", None)
+        return n
+
+    def _lams(self, lam_hi_per_level):
+        lam = [float(v) for v in lam_hi_per_level]
+        if len(lam) < self.chain_levels():
+            raise ValueError(f"lam_hi_per_level: {len(lam)} values for {self.chain_levels()} levels")
+        return (C.c_double * len(lam))(*lam)
+
+    def set_coarse_context(self, coarse, parent, octant):
+        """Append the levels of `coarse` below this context's coarsest level (h-coarsening,
+        dgvv_set_coarse_context); parent/octant per fine cell.  Keeps a reference to `coarse`."""
+        par = np.ascontiguousarray(parent, dtype=np.int32)
+        octa = np.ascontiguousarray(octant, dtype=np.int8)
+        A.check(self._L.dgvv_set_coarse_context(self.h, coarse.h, par.ctypes.data_as(C.POINTER(C.c_int32)),
+                                                octa.ctypes.data_as(C.POINTER(C.c_int8))))
+        self._coarse = coarse
+
+    def prolongate_h(self, op, coarse_vec, fine_vec, beta=0.0):
+        nf = self._n(op, len(self.degrees) - 1)
+        A.check(self._L.dgvv_prolongate_h(self.h, op, _ptr(coarse_vec, None, "coarse"), _ptr(fine_vec, nf, "fine"),
+                                          float(beta), _stream()))
+        return fine_vec
+
+    def restrict_h(self, op, fine_vec, coarse_vec, beta=0.0):
+        nf = self._n(op, len(self.degrees) - 1)
+        A.check(self._L.dgvv_restrict_h(self.h, op, _ptr(fine_vec, nf, "fine"), _ptr(coarse_vec, None, "coarse"),
+                                        float(beta), _stream()))
+        return coarse_vec
+
+    def setup_coarse_solver(self, op):
+        """Dense direct solve on the coarsest level (dgvv_setup_coarse_solver); returns its size."""
+        n = C.c_int32()
+        A.check(self._L.dgvv_setup_coarse_solver(self.h, op, C.byref(n)))
+        return n.value
 
     def dot(self, a, b, ncomp=1, level=0):
         out = C.c_double()

@@ -215,6 +215,42 @@ def run_f2(reps):
                f"{it} iterations to rtol 1e-10 (relres {rr:.2e}); {ms / max(it, 1):.3f} ms/iteration")
 
 
+def run_f4(reps):
+    """f4: upwind convective term on the C2 mesh (32^3 deformed, k=3) and C3's mesh (64^3, k=4)
+    with a random transport field w = rng(1); the Oseen-type viscous step mass M + A(nu) + C(w)
+    (mass = 1e3 ~ gamma_0/dt for a CFL-limited dt) and GMRES(30) with the FP64 / FP32 V-cycle of the
+    symmetric part to rtol 1e-8."""
+    for name, m, k, degs in (("C2", deformed_cube(32, 3), 3, [3, 2, 1]), ("C3", cube(64), 4, [4, 2, 1])):
+        ctx = Context(m, k, visc_law=C2_LAW, degrees=degs)
+        N = 3 * ctx.n_dofs(0)
+        src = dev(uniform(0, N))
+        ctx.set_transport(dev(uniform(1, N)))
+        dst = torch.empty_like(src)
+        n = k + 1
+        general = m.map_degree > 1
+        byt = m.n_cells * 8 * (3 * 3 * n ** 3 + 6 + (10 * n ** 3 + 6 * 4 * n * n if general else 8))
+        ms = timeit(lambda: ctx.apply_convective(src, dst), 20, reps)
+        report(name + "+f4", "apply_convective", ms, N, byt, None, "upwind convective term C(w) u")
+        ctx.set_mass(0, 1.0e3)
+        ms = timeit(lambda: ctx.apply_oseen(src, dst, 1.0), 20, reps)
+        report(name + "+f4", "apply_oseen", ms, N, None, None, "mass M + A(nu) + C(w): viscous apply + convective kernel")
+        lams = [1.2 * ctx.estimate_lambda_max(0, dev(uniform(2, 3 * m.n_cells * (kk + 1) ** 3)), level=l, steps=15)
+                for l, kk in enumerate(degs)]
+        for pc in ("vcycle", "vcycle_fp32"):
+            x = torch.zeros_like(src)
+            ctx.gmres_solve(src, x, rtol=1e-8, restart=30, maxit=300, precond=pc, lam_hi_per_level=lams)
+            x.zero_()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            it, rr = ctx.gmres_solve(src, x, rtol=1e-8, restart=30, maxit=300, precond=pc, lam_hi_per_level=lams)
+            e1.record()
+            e1.synchronize()
+            ms = e0.elapsed_time(e1)
+            report(name + "+f4", "gmres_" + pc, ms, N, None, None,
+                   f"{it} iterations to rtol 1e-8 (relres {rr:.2e}); {ms / max(it, 1):.3f} ms/iteration")
+
+
 def run_c5(reps):
     m = bfs()
     ctx = Context(m, 3, visc_law=C5_LAW)
@@ -235,7 +271,7 @@ def main():
     a = ap.parse_args()
     torch.cuda.set_device(0)
     for c in a.configs.split(","):
-        {"2": run_c2, "3": run_c3, "4": run_c4, "5": run_c5, "f1": run_f1, "f2": run_f2}[c](a.reps)
+        {"2": run_c2, "3": run_c3, "4": run_c4, "5": run_c5, "f1": run_f1, "f2": run_f2, "f4": run_f4}[c](a.reps)
         torch.cuda.empty_cache()
 
 
