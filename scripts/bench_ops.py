@@ -251,6 +251,68 @@ def run_f4(reps):
                    f"{it} iterations to rtol 1e-8 (relres {rr:.2e}); {ms / max(it, 1):.3f} ms/iteration")
 
 
+def _timed(fn):
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    out = fn()
+    e1.record()
+    e1.synchronize()
+    return e0.elapsed_time(e1), out
+
+
+def run_f3(reps):
+    """f3: cph hierarchy on the C4 Poisson problem (64^3, k = 5 -> 3 -> 2 -> 1, then h-levels 32^3 ... 4^3
+    at k = 1, direct solve on 4^3 = 512 DoFs) and on the C3 Helmholtz viscous step (64^3, k = 4 -> 2 -> 1,
+    h-levels to 4^3, direct solve on 1536 DoFs; mass 1 and 1e3): PCG to 1e-8 with the p-only vs the
+    cph V-cycle."""
+    from inputs import cube_parent_map
+    for name, op, k0, degs, law, masses in (("C4", A.OP_POISSON, 5, [5, 3, 2, 1], C4_LAW, [0.0]),
+                                            ("C3", A.OP_VISCOUS, 4, [4, 2, 1], C2_LAW, [1.0, 1.0e3])):
+        kw = {"poisson_law": law} if op == A.OP_POISSON else {"visc_law": law}
+        nc = 1 if op == A.OP_POISSON else 3
+        for mass in masses:
+            fine = Context(cube(64), k0, degrees=degs, **kw)
+            fine.set_mass(op, mass)
+            lams = [1.2 * fine.estimate_lambda_max(op, dev(uniform(2, nc * fine.n_dofs(l))), level=l, steps=20)
+                    for l in range(len(degs))]
+            N = nc * fine.n_dofs(0)
+            b = dev(uniform(0, N))
+            x = torch.zeros_like(b)
+            tag = f"{name}+f3" + (f" mass={mass:g}" if op == A.OP_VISCOUS else "")
+            fine.cg_solve(op, b, x, rtol=1e-8, maxit=400, precond="vcycle", lam_hi_per_level=lams)
+            x.zero_()
+            ms, (it, rr) = _timed(lambda: fine.cg_solve(op, b, x, rtol=1e-8, maxit=400, precond="vcycle",
+                                                        lam_hi_per_level=lams))
+            report(tag, "pcg_vcycle_p_only", ms, N, None, None, f"{it} iterations (relres {rr:.1e}); {ms / max(it, 1):.2f} ms/it")
+            ms = timeit(lambda: fine.vcycle(op, b, x, lams), 5, reps)
+            report(tag, "vcycle_p_only", ms, N, None, None, "coarsest: Chebyshev(5) on 64^3 k=1")
+            prev, Nc, keep = fine, 64, []
+            while Nc > 4:
+                Nc //= 2
+                c = Context(cube(Nc), 1, **kw)
+                c.set_mass(op, mass)
+                parent, octant = cube_parent_map(2 * Nc)
+                prev.set_coarse_context(c, parent, octant)
+                keep.append(c)
+                if Nc > 4:
+                    lams.append(1.2 * c.estimate_lambda_max(op, dev(uniform(2, nc * c.n_dofs(0))), level=0, steps=20))
+                prev = c
+            ms_setup, nd = _timed(lambda: keep[-1].setup_coarse_solver(op))
+            lams.append(1.0)
+            report(tag, "setup_coarse_solver", ms_setup, nd, None, None, f"assemble + Gauss-Jordan inverse of {nd} DoFs")
+            x.zero_()
+            fine.cg_solve(op, b, x, rtol=1e-8, maxit=400, precond="vcycle", lam_hi_per_level=lams)
+            x.zero_()
+            ms, (it, rr) = _timed(lambda: fine.cg_solve(op, b, x, rtol=1e-8, maxit=400, precond="vcycle",
+                                                        lam_hi_per_level=lams))
+            report(tag, "pcg_vcycle_cph", ms, N, None, None, f"{it} iterations (relres {rr:.1e}); {ms / max(it, 1):.2f} ms/it")
+            ms = timeit(lambda: fine.vcycle(op, b, x, lams), 5, reps)
+            report(tag, "vcycle_cph", ms, N, None, None, f"{fine.chain_levels()} levels, direct solve on 4^3 k=1")
+            del keep, fine
+            torch.cuda.empty_cache()
+
+
 def run_c5(reps):
     m = bfs()
     ctx = Context(m, 3, visc_law=C5_LAW)
@@ -271,7 +333,7 @@ def main():
     a = ap.parse_args()
     torch.cuda.set_device(0)
     for c in a.configs.split(","):
-        {"2": run_c2, "3": run_c3, "4": run_c4, "5": run_c5, "f1": run_f1, "f2": run_f2, "f4": run_f4}[c](a.reps)
+        {"2": run_c2, "3": run_c3, "4": run_c4, "5": run_c5, "f1": run_f1, "f2": run_f2, "f4": run_f4, "f3": run_f3}[c](a.reps)
         torch.cuda.empty_cache()
 
 
