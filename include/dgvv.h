@@ -265,8 +265,9 @@ dgvv_status dgvv_vcycle(dgvv_ctx* ctx, int32_t op, const double* b, double* x,
  * coarsest p-level into `coarse`'s levels (recursively, if `coarse` has a coarse context), and
  * lambda_hi_per_level lists every level of that chain in order.  `coarse` is borrowed: keep it
  * alive while `fine` is used; its coefficients/mass are its own (set them consistently).
- * Single-GPU contexts only (DGVV_EUNSUPPORTED with ghosts); the FP32 V-cycle does not follow the
- * chain (DGVV_EUNSUPPORTED). */
+ * The FP32 V-cycle (dgvv_vcycle_fp32, DGVV_PRECOND_VCYCLE_FP32) follows the chain as well, with
+ * the direct coarse solve in FP64 arithmetic.  Single-GPU contexts only
+ * (DGVV_EUNSUPPORTED with ghosts). */
 dgvv_status dgvv_set_coarse_context(dgvv_ctx* fine, dgvv_ctx* coarse, const int32_t* parent,
                                     const int8_t* octant);
 /* fine = P coarse + beta fine (fine's coarsest level <- coarse's level 0), op selects 3 or 1

@@ -187,6 +187,8 @@ struct dgvv_ctx {
   double* Ainv[2] = {nullptr, nullptr};      // dense inverse of the coarsest level per op
   int direct_n[2] = {0, 0};
   int direct_epoch[2] = {-1, -1};            // coef_epoch the inverse was built at
+  float* hbf[2] = {nullptr, nullptr};        // FP32 V-cycle: coarse-level b / x per op
+  float* hxf[2] = {nullptr, nullptr};
   std::vector<int> h_gperm;                  // internal ghost i -> mesh ghost row
   std::vector<LevelF> LF;                    // FP32 levels (lazily built)
   float* d_cart_f = nullptr;
@@ -1199,6 +1201,13 @@ static dgvv_status ensure_fp32(dgvv_ctx* c, int op, cudaStream_t s) {
       TRY(dalloc(c, &S[4], N));
     }
   }
+  if (c->coarse) {                              // f3: FP32 levels of the coarser contexts too
+    TRY(op_ready(c->coarse, op));
+    const size_t Nc = (size_t)nc * level_dofs(c->coarse, 0);
+    if (!c->hbf[oi]) TRY(dalloc(c, &c->hbf[oi], Nc));
+    if (!c->hxf[oi]) TRY(dalloc(c, &c->hxf[oi], Nc));
+    TRY(ensure_fp32(c->coarse, op, s));
+  }
   return DGVV_OK;
 }
 
@@ -1285,25 +1294,38 @@ static dgvv_status transfer_f(dgvv_ctx* c, int op, int fl, const float* in, floa
 static dgvv_status vcycle_rec_f(dgvv_ctx* c, int op, int l, const float* b, float* x, const double* his,
                                 cudaStream_t s) {
   const int oi = op == DGVV_OP_VISCOUS ? 0 : 1;
+  const int nc = op == DGVV_OP_VISCOUS ? 3 : 1;
   auto& S = c->LF[l].scratch[oi];
-  const double hi = his[l], lo = hi / 20.0;
   const int last = (int)c->L.size() - 1;
+  if (l == last && !c->coarse && c->Ainv[oi]) {  // direct coarse solve, FP64 arithmetic
+    if (c->direct_epoch[oi] != c->coef_epoch)
+      return dgvv_fail(DGVV_ESTATE, "direct coarse solver is stale (coefficients or mass changed): call dgvv_setup_coarse_solver again");
+    DGVV_CUDA_TRY(launch_dense_matvec_f(c->Ainv[oi], b, x, c->direct_n[oi], s));
+    return DGVV_OK;
+  }
+  const double hi = his[l], lo = hi / 20.0;
   TRY(cheb_impl_f(c, op, l, x, b, 5, lo, hi, 1, S[1], s));
-  if (l == last) return DGVV_OK;
+  if (l == last && !c->coarse) return DGVV_OK;
   ApplyArgsT<float> a = base_args_f(c, l, op);
   a.src = x; a.dst = S[0]; a.b = b; a.mode = MODE_RESID;
   TRY(run_apply_f(c, op, l, a, s));
-  auto& C = c->LF[l + 1].scratch[oi];
-  TRY(transfer_f(c, op, l, S[0], C[3], 0.0, false, s));
-  TRY(vcycle_rec_f(c, op, l + 1, C[3], C[4], his, s));
-  TRY(transfer_f(c, op, l, C[4], x, 1.0, true, s));
+  if (l < last) {
+    auto& C = c->LF[l + 1].scratch[oi];
+    TRY(transfer_f(c, op, l, S[0], C[3], 0.0, false, s));
+    TRY(vcycle_rec_f(c, op, l + 1, C[3], C[4], his, s));
+    TRY(transfer_f(c, op, l, C[4], x, 1.0, true, s));
+  } else {                                     // h-coarsening into the coarser context (f3)
+    const int n = c->L.back().n;
+    DGVV_CUDA_TRY(launch_hrestrict_f(n, nc, S[0], c->hbf[oi], c->d_child, 0.0, c->coarse->n_owned, s));
+    TRY(vcycle_rec_f(c->coarse, op, 0, c->hbf[oi], c->hxf[oi], his + c->L.size(), s));
+    DGVV_CUDA_TRY(launch_hprolongate_f(n, nc, c->hxf[oi], x, c->d_parent, c->d_octant, 1.0, c->n_owned, s));
+  }
   TRY(cheb_impl_f(c, op, l, x, b, 5, lo, hi, 0, S[1], s));
   return DGVV_OK;
 }
 
 // z = V_fp32(r) for FP64 vectors (conversion in and out)
 static dgvv_status vcycle_fp32_d(dgvv_ctx* c, int op, const double* r, double* z, const double* his, cudaStream_t s) {
-  if (c->coarse) return dgvv_fail(DGVV_EUNSUPPORTED, "FP32 V-cycle: h-levels (dgvv_set_coarse_context) not supported");
   TRY(ensure_fp32(c, op, s));
   const int oi = op == DGVV_OP_VISCOUS ? 0 : 1;
   const long N = (long)(op == DGVV_OP_VISCOUS ? 3 : 1) * level_dofs(c, 0);

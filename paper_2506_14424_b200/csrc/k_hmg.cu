@@ -22,13 +22,13 @@ namespace dgvv {
 
 // x-fastest three-pass tensor contraction of one n^3 block with per-direction matrices
 // (M?[i_out * n + j_in]); in/out in shared memory; t = thread index in the team of T threads
-template <int n, int T>
-__device__ inline void tensor3_dir(const double* Mx, const double* My, const double* Mz, const double* in,
-                                   double* s1, double* s2, double* out, int t) {
+template <int n, int T, typename R>
+__device__ inline void tensor3_dir(const R* Mx, const R* My, const R* Mz, const R* in, R* s1, R* s2, R* out,
+                                   int t) {
   constexpr int n2 = n * n, n3 = n2 * n;
   for (int i = t; i < n3; i += T) {               // x
     const int xo = i % n, r = i / n;
-    double acc = 0.0;
+    R acc = R(0);
 #pragma unroll
     for (int k = 0; k < n; ++k) acc = fma(Mx[xo * n + k], in[r * n + k], acc);
     s1[i] = acc;
@@ -37,7 +37,7 @@ __device__ inline void tensor3_dir(const double* Mx, const double* My, const dou
   __syncthreads();
   for (int i = t; i < n3; i += T) {               // y
     const int xo = i % n, yo = (i / n) % n, z = i / n2;
-    double acc = 0.0;
+    R acc = R(0);
 #pragma unroll
     for (int k = 0; k < n; ++k) acc = fma(My[yo * n + k], s1[z * n2 + k * n + xo], acc);
     s2[i] = acc;
@@ -45,7 +45,7 @@ __device__ inline void tensor3_dir(const double* Mx, const double* My, const dou
   __syncthreads();
   for (int i = t; i < n3; i += T) {               // z
     const int r = i % n2, zo = i / n2;
-    double acc = 0.0;
+    R acc = R(0);
 #pragma unroll
     for (int k = 0; k < n; ++k) acc = fma(Mz[zo * n + k], s2[k * n2 + r], acc);
     out[i] = acc;
@@ -61,55 +61,54 @@ struct HMats {
 constexpr int HT = 64;   // threads per block (one (cell, component) block at a time)
 
 // fine[f][c] = P_oct(f) coarse[parent[f]][c] + beta fine[f][c]
-template <int n>
-__global__ void __launch_bounds__(HT) hprolong_kernel(HMats M, const double* coarse, double* fine,
-                                                      const int* parent, const signed char* octant, int nc,
-                                                      double beta, int n_fine) {
+template <int n, typename R>
+__global__ void __launch_bounds__(HT) hprolong_kernel(HMats M, const R* coarse, R* fine, const int* parent,
+                                                      const signed char* octant, int nc, R beta, int n_fine) {
   constexpr int n3 = n * n * n;
-  __shared__ double sin_[n3], s1[n3], s2[n3], sout[n3];
-  __shared__ double sm[3][n * n];
+  __shared__ R sin_[n3], s1[n3], s2[n3], sout[n3];
+  __shared__ R sm[3][n * n];
   const int f = blockIdx.x;
   const int oc = octant[f];
   const int p = parent[f];
   for (int i = threadIdx.x; i < n * n; i += HT) {
-    sm[0][i] = M.P[oc & 1][i];
-    sm[1][i] = M.P[(oc >> 1) & 1][i];
-    sm[2][i] = M.P[(oc >> 2) & 1][i];
+    sm[0][i] = R(M.P[oc & 1][i]);
+    sm[1][i] = R(M.P[(oc >> 1) & 1][i]);
+    sm[2][i] = R(M.P[(oc >> 2) & 1][i]);
   }
   for (int c = 0; c < nc; ++c) {
     for (int i = threadIdx.x; i < n3; i += HT) sin_[i] = coarse[((size_t)p * nc + c) * n3 + i];
     __syncthreads();
-    tensor3_dir<n, HT>(sm[0], sm[1], sm[2], sin_, s1, s2, sout, threadIdx.x);
+    tensor3_dir<n, HT, R>(sm[0], sm[1], sm[2], sin_, s1, s2, sout, threadIdx.x);
     for (int i = threadIdx.x; i < n3; i += HT) {
       const size_t o = ((size_t)f * nc + c) * n3 + i;
-      fine[o] = beta == 0.0 ? sout[i] : sout[i] + beta * fine[o];
+      fine[o] = beta == R(0) ? sout[i] : sout[i] + beta * fine[o];
     }
     __syncthreads();
   }
 }
 
 // coarse[p][c] = sum_{oct} P_oct^T fine[child[p][oct]][c] + beta coarse[p][c]
-template <int n>
-__global__ void __launch_bounds__(HT) hrestrict_kernel(HMats M, const double* fine, double* coarse,
-                                                       const int* child, int nc, double beta, int n_coarse) {
+template <int n, typename R>
+__global__ void __launch_bounds__(HT) hrestrict_kernel(HMats M, const R* fine, R* coarse, const int* child,
+                                                       int nc, R beta, int n_coarse) {
   constexpr int n3 = n * n * n;
-  __shared__ double sin_[n3], s1[n3], s2[n3], sout[n3];
-  __shared__ double sm[2][n * n];
+  __shared__ R sin_[n3], s1[n3], s2[n3], sout[n3];
+  __shared__ R sm[2][n * n];
   const int p = blockIdx.x;
   for (int i = threadIdx.x; i < n * n; i += HT) {
-    sm[0][i] = M.PT[0][i];
-    sm[1][i] = M.PT[1][i];
+    sm[0][i] = R(M.PT[0][i]);
+    sm[1][i] = R(M.PT[1][i]);
   }
   __syncthreads();
   for (int c = 0; c < nc; ++c) {
-    double acc[(n3 + HT - 1) / HT];
+    R acc[(n3 + HT - 1) / HT];
 #pragma unroll
-    for (int r = 0; r < (n3 + HT - 1) / HT; ++r) acc[r] = 0.0;
+    for (int r = 0; r < (n3 + HT - 1) / HT; ++r) acc[r] = R(0);
     for (int oc = 0; oc < 8; ++oc) {
       const int f = child[p * 8 + oc];
       for (int i = threadIdx.x; i < n3; i += HT) sin_[i] = fine[((size_t)f * nc + c) * n3 + i];
       __syncthreads();
-      tensor3_dir<n, HT>(sm[oc & 1], sm[(oc >> 1) & 1], sm[(oc >> 2) & 1], sin_, s1, s2, sout, threadIdx.x);
+      tensor3_dir<n, HT, R>(sm[oc & 1], sm[(oc >> 1) & 1], sm[(oc >> 2) & 1], sin_, s1, s2, sout, threadIdx.x);
 #pragma unroll
       for (int r = 0; r < (n3 + HT - 1) / HT; ++r) {
         const int i = threadIdx.x + r * HT;
@@ -121,7 +120,7 @@ __global__ void __launch_bounds__(HT) hrestrict_kernel(HMats M, const double* fi
       const int i = threadIdx.x + r * HT;
       if (i < n3) {
         const size_t o = ((size_t)p * nc + c) * n3 + i;
-        coarse[o] = beta == 0.0 ? acc[r] : acc[r] + beta * coarse[o];
+        coarse[o] = beta == R(0) ? acc[r] : acc[r] + beta * coarse[o];
       }
     }
   }
@@ -144,12 +143,13 @@ static HMats make_hmats(int n) {
   return M;
 }
 
-cudaError_t launch_hprolongate(int n, int nc, const double* coarse, double* fine, const int* parent,
-                               const signed char* octant, double beta, int n_fine, cudaStream_t s) {
+template <typename R>
+static cudaError_t hprolong_t(int n, int nc, const R* coarse, R* fine, const int* parent, const signed char* octant,
+                              double beta, int n_fine, cudaStream_t s) {
   if (n_fine <= 0) return cudaSuccess;
   const HMats M = make_hmats(n);
   switch (n) {
-#define HP(N) case N: hprolong_kernel<N><<<n_fine, HT, 0, s>>>(M, coarse, fine, parent, octant, nc, beta, n_fine); break;
+#define HP(N) case N: hprolong_kernel<N, R><<<n_fine, HT, 0, s>>>(M, coarse, fine, parent, octant, nc, R(beta), n_fine); break;
     HP(2) HP(3) HP(4) HP(5) HP(6)
 #undef HP
     default: return cudaErrorNotSupported;
@@ -157,17 +157,35 @@ cudaError_t launch_hprolongate(int n, int nc, const double* coarse, double* fine
   return cudaGetLastError();
 }
 
-cudaError_t launch_hrestrict(int n, int nc, const double* fine, double* coarse, const int* child, double beta,
-                             int n_coarse, cudaStream_t s) {
+template <typename R>
+static cudaError_t hrestrict_t(int n, int nc, const R* fine, R* coarse, const int* child, double beta, int n_coarse,
+                               cudaStream_t s) {
   if (n_coarse <= 0) return cudaSuccess;
   const HMats M = make_hmats(n);
   switch (n) {
-#define HR(N) case N: hrestrict_kernel<N><<<n_coarse, HT, 0, s>>>(M, fine, coarse, child, nc, beta, n_coarse); break;
+#define HR(N) case N: hrestrict_kernel<N, R><<<n_coarse, HT, 0, s>>>(M, fine, coarse, child, nc, R(beta), n_coarse); break;
     HR(2) HR(3) HR(4) HR(5) HR(6)
 #undef HR
     default: return cudaErrorNotSupported;
   }
   return cudaGetLastError();
+}
+
+cudaError_t launch_hprolongate(int n, int nc, const double* coarse, double* fine, const int* parent,
+                               const signed char* octant, double beta, int n_fine, cudaStream_t s) {
+  return hprolong_t<double>(n, nc, coarse, fine, parent, octant, beta, n_fine, s);
+}
+cudaError_t launch_hprolongate_f(int n, int nc, const float* coarse, float* fine, const int* parent,
+                                 const signed char* octant, double beta, int n_fine, cudaStream_t s) {
+  return hprolong_t<float>(n, nc, coarse, fine, parent, octant, beta, n_fine, s);
+}
+cudaError_t launch_hrestrict(int n, int nc, const double* fine, double* coarse, const int* child, double beta,
+                             int n_coarse, cudaStream_t s) {
+  return hrestrict_t<double>(n, nc, fine, coarse, child, beta, n_coarse, s);
+}
+cudaError_t launch_hrestrict_f(int n, int nc, const float* fine, float* coarse, const int* child, double beta,
+                               int n_coarse, cudaStream_t s) {
+  return hrestrict_t<float>(n, nc, fine, coarse, child, beta, n_coarse, s);
 }
 
 // ------------------------------------------------------------------ dense direct solver
@@ -220,16 +238,18 @@ __global__ void gj_extract_kernel(const double* W, double* Ainv, int N) {
   }
 }
 
-// x = Ainv b, one warp per row (row-major, coalesced)
-__global__ void dense_matvec_kernel(const double* Ainv, const double* b, double* x, int N) {
+// x = Ainv b, one warp per row (row-major, coalesced); FP64 accumulation for FP32 vectors too
+// (the paper's coarse solver runs in double precision)
+template <typename R>
+__global__ void dense_matvec_kernel(const double* Ainv, const R* b, R* x, int N) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= N) return;
   const double* row = Ainv + (size_t)warp * N;
   double acc = 0.0;
-  for (int c = lane; c < N; c += 32) acc = fma(row[c], b[c], acc);
+  for (int c = lane; c < N; c += 32) acc = fma(row[c], (double)b[c], acc);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (lane == 0) x[warp] = acc;
+  if (lane == 0) x[warp] = R(acc);
 }
 
 static inline int blocks_for(long n) { return (int)std::min<long>(148L * 16, std::max<long>(1, (n + 255) / 256)); }
@@ -252,7 +272,11 @@ cudaError_t launch_gauss_jordan_inverse(const double* cols, double* W, double* f
 }
 
 cudaError_t launch_dense_matvec(const double* Ainv, const double* b, double* x, int N, cudaStream_t s) {
-  dense_matvec_kernel<<<(N * 32 + 255) / 256, 256, 0, s>>>(Ainv, b, x, N);
+  dense_matvec_kernel<double><<<(N * 32 + 255) / 256, 256, 0, s>>>(Ainv, b, x, N);
+  return cudaGetLastError();
+}
+cudaError_t launch_dense_matvec_f(const double* Ainv, const float* b, float* x, int N, cudaStream_t s) {
+  dense_matvec_kernel<float><<<(N * 32 + 255) / 256, 256, 0, s>>>(Ainv, b, x, N);
   return cudaGetLastError();
 }
 

@@ -26,11 +26,16 @@ cudaError_t launch_hprolongate(int n, int nc, const double* coarse, double* fine
                                const signed char* octant, double beta, int n_fine, cudaStream_t s);
 cudaError_t launch_hrestrict(int n, int nc, const double* fine, double* coarse, const int* child, double beta,
                              int n_coarse, cudaStream_t s);
+cudaError_t launch_hprolongate_f(int n, int nc, const float* coarse, float* fine, const int* parent,
+                                 const signed char* octant, double beta, int n_fine, cudaStream_t s);
+cudaError_t launch_hrestrict_f(int n, int nc, const float* fine, float* coarse, const int* child, double beta,
+                               int n_coarse, cudaStream_t s);
 // f3: dense direct coarse solver (Gauss-Jordan inverse of the assembled operator, dense matvec)
 cudaError_t launch_set_unit(double* v, long n, long j, cudaStream_t s);
 cudaError_t launch_gauss_jordan_inverse(const double* cols, double* W, double* fac, double* Ainv, int N, int* bad,
                                         cudaStream_t s);
 cudaError_t launch_dense_matvec(const double* Ainv, const double* b, double* x, int N, cudaStream_t s);
+cudaError_t launch_dense_matvec_f(const double* Ainv, const float* b, float* x, int N, cudaStream_t s);
 // K2: Newton-linearised viscous apply
 cudaError_t launch_newton(int n, int geo, const ApplyArgs& a, cudaStream_t s);
 // K3: Carreau viscosity at all points

@@ -309,6 +309,13 @@ def run_f3(reps):
             report(tag, "pcg_vcycle_cph", ms, N, None, None, f"{it} iterations (relres {rr:.1e}); {ms / max(it, 1):.2f} ms/it")
             ms = timeit(lambda: fine.vcycle(op, b, x, lams), 5, reps)
             report(tag, "vcycle_cph", ms, N, None, None, f"{fine.chain_levels()} levels, direct solve on 4^3 k=1")
+            x.zero_()
+            fine.cg_solve(op, b, x, rtol=1e-8, maxit=400, precond="vcycle_fp32", lam_hi_per_level=lams)
+            x.zero_()
+            ms, (it, rr) = _timed(lambda: fine.cg_solve(op, b, x, rtol=1e-8, maxit=400, precond="vcycle_fp32",
+                                                        lam_hi_per_level=lams))
+            report(tag, "pcg_vcycle_cph_fp32", ms, N, None, None,
+                   f"{it} iterations (relres {rr:.1e}); {ms / max(it, 1):.2f} ms/it; FP32 levels, FP64 direct solve")
             del keep, fine
             torch.cuda.empty_cache()
 

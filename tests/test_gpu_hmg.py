@@ -153,7 +153,12 @@ def test_cph_vcycle_parity(op):
     b = uniform(0, len(levels[0]["Dinv"]))
     x = torch.zeros(len(b), dtype=torch.float64, device="cuda")
     fine.vcycle(op, dev(b), x, lams)
-    assert rel(host(x), mg.vcycle(levels, b)) < 1e-10
+    ref = mg.vcycle(levels, b)
+    assert rel(host(x), ref) < 1e-10
+    # the FP32 V-cycle follows the same chain (direct solve in FP64): within the FP32 reading F1
+    xf = torch.zeros_like(x)
+    fine.vcycle_fp32(op, dev(b), xf, lams)
+    assert rel(host(xf), ref) < 2e-5
 
 
 def test_cph_pcg_full_size_c4():
@@ -188,3 +193,6 @@ def test_cph_pcg_full_size_c4():
     y = torch.empty_like(b)
     fine.apply_poisson(x, y)
     assert float(torch.linalg.norm(b - y) / torch.linalg.norm(b)) <= 1.01e-8
+    x.zero_()                                     # the paper's configuration: FP32 cph V-cycle in FP64 CG
+    it_f, rr_f = fine.cg_solve(A.OP_POISSON, b, x, rtol=1e-8, maxit=300, precond="vcycle_fp32", lam_hi_per_level=lams)
+    assert rr_f <= 1e-8 and it_f <= it_h + 2
