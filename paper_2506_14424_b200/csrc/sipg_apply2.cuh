@@ -29,6 +29,19 @@
 #define USE_ST 0          // keep a transposed [c][z][x][y] copy of the cell (16-byte y-lines)
 #endif
 
+// diagnostics only (upper bounds of what recomputing the metric could gain):
+// read every cell's volume / face metric from cell 0 (L1/L2-resident) instead of its own
+#ifdef DGVV_DIAG_NOVMETRIC
+#define DIAG_VC(c) 0
+#else
+#define DIAG_VC(c) (c)
+#endif
+#ifdef DGVV_DIAG_NOFMETRIC
+#define DIAG_FC(c) 0
+#else
+#define DIAG_FC(c) (c)
+#endif
+
 namespace dgvv {
 
 template <int n>
@@ -214,6 +227,7 @@ sipg_apply2_kernel(const ApplyArgsT<R> A) {
   __syncthreads();
 
   // =============================================================== volume term
+#ifndef DGVV_DIAG_NOVOL
   {
     R Da[n], Db[n];
     ld_row<n>(sD + a * RS, Da);
@@ -243,10 +257,10 @@ sipg_apply2_kernel(const ApplyArgsT<R> A) {
       if constexpr (GEO == 0) {
         w = A.nu_cell[(size_t)cell * n3 + q] * wab * R(T.w[z]) * vol;
       } else {
-        const R* vm = A.vJi + (size_t)cell * 9 * n3 + q;
+        const R* vm = A.vJi + (size_t)DIAG_VC(cell) * 9 * n3 + q;
 #pragma unroll
         for (int r = 0; r < 9; ++r) Ji[r] = __ldg(vm + r * n3);
-        w = A.nu_cell[(size_t)cell * n3 + q];                  // nu * JxW
+        w = A.nu_cell[(size_t)DIAG_VC(cell) * n3 + q];         // nu * JxW
       }
       R G[NC][3];
 #pragma unroll
@@ -288,7 +302,9 @@ sipg_apply2_kernel(const ApplyArgsT<R> A) {
     __syncthreads();
   }
 
+#endif
   // =============================================================== face terms
+#ifndef DGVV_DIAG_NOFACE
   // Faces in opposite pairs (-d,+d): one pass over each normal line gives the own traces of
   // both faces; the traces of both faces go to smem together (one barrier), then the
   // tangential coefficients of both (second barrier).  Order z, x, y: the z pair works on the
@@ -405,16 +421,16 @@ sipg_apply2_kernel(const ApplyArgsT<R> A) {
           Hp = A.Hcell[nbv];
         }
       } else if constexpr (GEO == 1) {
-        const R* fm = A.fJi + ((size_t)cell * 6 + f) * 9 * n2 + p;
+        const R* fm = A.fJi + ((size_t)DIAG_FC(cell) * 6 + f) * 9 * n2 + p;
 #pragma unroll
         for (int r = 0; r < 9; ++r) Jim[r] = __ldg(fm + r * n2);
-        wm = A.nu_face[((size_t)cell * 6 + f) * n2 + p];      // nu * dA
+        wm = A.nu_face[((size_t)DIAG_FC(cell) * 6 + f) * n2 + p];      // nu * dA
         wp = wm;
         if (inter) {
-          const R* fp = A.fJi + ((size_t)nbv * 6 + (f ^ 1)) * 9 * n2 + p;
+          const R* fp = A.fJi + ((size_t)DIAG_FC(nbv) * 6 + (f ^ 1)) * 9 * n2 + p;
 #pragma unroll
           for (int r = 0; r < 9; ++r) Jip[r] = __ldg(fp + r * n2);
-          wp = A.nu_face[((size_t)nbv * 6 + (f ^ 1)) * n2 + p];
+          wp = A.nu_face[((size_t)DIAG_FC(nbv) * 6 + (f ^ 1)) * n2 + p];
           Hp = A.Hcell[nbv];
         }
       }
@@ -615,6 +631,7 @@ sipg_apply2_kernel(const ApplyArgsT<R> A) {
     }
   }
 
+#endif
   // =============================================================== epilogue
   if constexpr (MASS) {                 // Helmholtz mass term: + mass * JxW * u (diagonal M)
 #pragma unroll
