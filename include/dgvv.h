@@ -277,6 +277,32 @@ dgvv_status dgvv_prolongate_h(dgvv_ctx* fine, int32_t op, const double* coarse_v
 dgvv_status dgvv_restrict_h(dgvv_ctx* fine, int32_t op, const double* fine_vec, double* coarse_vec,
                             double beta, dgvv_stream stream);
 
+/* c-level of the cph hierarchy ("first the conversion from
+ * a discontinuous to a continuous polynomial space is performed").  Readings C1-C3:
+ * the continuous level is Q1 — one value per mesh vertex and component, vector layout [c][vertex]
+ * — on the mesh of ctx's coarsest (degree-1) DG level; vertices are numbered topologically
+ * (corners matched across every interior/periodic face, first appearance in (cell, corner)
+ * order).  Its embedding P_c into DG_1 interpolates the trilinear corner functions at the Gauss
+ * points; its operator is the Galerkin product P_c^T A_DG P_c (matrix-free: embed, DG apply,
+ * transpose-gather; no atomics); the smoother diagonal is obtained by probing with a vertex
+ * colouring.  With the level enabled, every V-cycle on ctx continues below its coarsest DG level
+ * in the continuous space: residual restricted by P_c^T, V-cycle over the continuous levels of ctx
+ * and — nested Q1 h-transfer (reading C3), CSR on the GPU — of its coarse contexts (all of which
+ * need the level enabled), correction prolongated by P_c.  lambda_hi_per_level then lists ctx's DG
+ * levels followed by one entry per continuous level; dgvv_estimate_lambda_max with level =
+ * n_levels estimates the continuous level's; dgvv_setup_coarse_solver on the last context of the
+ * chain builds the direct solve of its continuous level (<= 4096 DoFs).  FP64 only (the FP32
+ * V-cycle returns DGVV_EUNSUPPORTED); single-GPU contexts only. */
+dgvv_status dgvv_set_continuous_level(dgvv_ctx* ctx, int32_t enable);
+dgvv_status dgvv_continuous_level_info(const dgvv_ctx* ctx, int32_t* n_vertices, int32_t* n_colors);
+/* dst = P_c^T A_DG P_c src on the continuous level (op's component count). */
+dgvv_status dgvv_apply_continuous(dgvv_ctx* ctx, int32_t op, const double* src, double* dst,
+                                  dgvv_stream stream);
+/* transpose = 0: dst (DG_1, ctx's coarsest level) = P_c src + beta dst;
+ * transpose = 1: dst (continuous) = P_c^T src + beta dst. */
+dgvv_status dgvv_embed_continuous(dgvv_ctx* ctx, int32_t op, int32_t transpose, const double* src,
+                                  double* dst, double beta, dgvv_stream stream);
+
 /* Direct coarse solver ("a direct solver if the system size falls below 2000
  * DoFs"; reading H3): assembles the operator of ctx's coarsest level (with its mass term) column
  * by column from the matrix-free apply, inverts it on the GPU by Gauss-Jordan elimination (SPD:

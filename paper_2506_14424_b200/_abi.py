@@ -64,6 +64,10 @@ _SIGS = {
     "dgvv_prolongate_h": [VP, I32, VP, VP, D, VP],
     "dgvv_restrict_h": [VP, I32, VP, VP, D, VP],
     "dgvv_setup_coarse_solver": [VP, I32, C.POINTER(I32)],
+    "dgvv_set_continuous_level": [VP, I32],
+    "dgvv_continuous_level_info": [VP, C.POINTER(I32), C.POINTER(I32)],
+    "dgvv_apply_continuous": [VP, I32, VP, VP, VP],
+    "dgvv_embed_continuous": [VP, I32, I32, VP, VP, D, VP],
     "dgvv_apply_convective": [VP, VP, VP, VP],
     "dgvv_apply_oseen": [VP, D, VP, VP, VP],
     "dgvv_gmres_solve": [VP, D, VP, VP, D, I32, I32, I32, PD, C.POINTER(I32), PD, VP],

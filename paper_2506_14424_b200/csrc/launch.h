@@ -36,6 +36,18 @@ cudaError_t launch_gauss_jordan_inverse(const double* cols, double* W, double* f
                                         cudaStream_t s);
 cudaError_t launch_dense_matvec(const double* Ainv, const double* b, double* x, int N, cudaStream_t s);
 cudaError_t launch_dense_matvec_f(const double* Ainv, const float* b, float* x, int N, cudaStream_t s);
+// f3 c-level: continuous Q1 level (embedding, transpose, CSR transfers, diagonal probing, Chebyshev)
+cudaError_t launch_cg_embed(const double* cg, double* dg, const int* vid, int n_cells, int nv, int nc, double beta,
+                            cudaStream_t s);
+cudaError_t launch_cg_embedT(const double* dg, double* cg, const int* inc_ptr, const int* inc, int nv, int nc,
+                             double beta, cudaStream_t s);
+cudaError_t launch_csr_spmv(const int* ptr, const int* col, const double* val, const double* x, double* y, int nrows,
+                            int ncols, int nc, double beta, cudaStream_t s);
+cudaError_t launch_cg_probe_set(double* sv, const int* color, int k, int comp, int nv, int nc, cudaStream_t s);
+cudaError_t launch_cg_probe_get(const double* y, double* diag, const int* color, int k, int comp, int nv,
+                                cudaStream_t s);
+cudaError_t launch_cheb_vec(const double* r, const double* dinv, double c_rho, double c_r, double* d, double* x,
+                            long n, cudaStream_t s);
 // K2: Newton-linearised viscous apply
 cudaError_t launch_newton(int n, int geo, const ApplyArgs& a, cudaStream_t s);
 // K3: Carreau viscosity at all points

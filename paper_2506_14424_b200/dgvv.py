@@ -249,12 +249,50 @@ class Context:
         return it.value, rr.value
 
     def chain_levels(self):
-        """Number of multigrid levels of the chain (own p-levels + those of the coarse contexts)."""
+        """Number of multigrid levels of the chain: own p-levels, then either the continuous levels
+        of this and every coarse context (c-level enabled) or the coarse contexts' chains."""
+        if getattr(self, "_continuous", False):
+            c, n = self, len(self.degrees)
+            while c is not None:
+                n += 1
+                c = getattr(c, "_coarse", None)
+            return n
         c, n = self, 0
         while c is not None:
+            if getattr(c, "_continuous", False):
+                return n + c.chain_levels()
             n += len(c.degrees)
             c = getattr(c, "_coarse", None)
         return n
+
+    def set_continuous_level(self, enable=True):
+        """Enable the continuous Q1 (c-) level below the coarsest (degree-1) DG level
+        (dgvv_set_continuous_level).  Returns (vertices, colours)."""
+        A.check(self._L.dgvv_set_continuous_level(self.h, int(bool(enable))))
+        self._continuous = bool(enable)
+        if not enable:
+            return None
+        nv, ncol = C.c_int32(), C.c_int32()
+        A.check(self._L.dgvv_continuous_level_info(self.h, C.byref(nv), C.byref(ncol)))
+        self.n_vertices = nv.value
+        return nv.value, ncol.value
+
+    def apply_continuous(self, op, src, dst):
+        n = (3 if op == A.OP_VISCOUS else 1) * self.n_vertices
+        A.check(self._L.dgvv_apply_continuous(self.h, op, _ptr(src, n, "src"), _ptr(dst, n, "dst"), _stream()))
+        return dst
+
+    def embed_continuous(self, op, src, dst, transpose=False, beta=0.0):
+        A.check(self._L.dgvv_embed_continuous(self.h, op, int(bool(transpose)), _ptr(src, None, "src"),
+                                              _ptr(dst, None, "dst"), float(beta), _stream()))
+        return dst
+
+    def estimate_lambda_max_continuous(self, op, v0, steps=20):
+        """lambda_max(D^-1 A) of the continuous level (dgvv_estimate_lambda_max, level = n_levels)."""
+        out = C.c_double()
+        A.check(self._L.dgvv_estimate_lambda_max(self.h, op, len(self.degrees), steps, _ptr(v0, None, "v0"),
+                                                 C.byref(out), _stream()))
+        return out.value
 
     def _lams(self, lam_hi_per_level):
         lam = [float(v) for v in lam_hi_per_level]

@@ -316,7 +316,26 @@ def run_f3(reps):
                                                         lam_hi_per_level=lams))
             report(tag, "pcg_vcycle_cph_fp32", ms, N, None, None,
                    f"{it} iterations (relres {rr:.1e}); {ms / max(it, 1):.2f} ms/it; FP32 levels, FP64 direct solve")
-            del keep, fine
+            # c-level: DG p-levels -> continuous Q1 on 64^3 -> Q1 h-levels -> direct on 4^3 (125 vertices)
+            ctxs = [fine] + keep
+            for c in ctxs:
+                c.set_continuous_level()
+            lams_c = lams[:len(degs)]
+            for c in ctxs[:-1]:
+                lams_c.append(1.2 * c.estimate_lambda_max_continuous(op, dev(uniform(2, nc * c.n_vertices)), steps=20))
+            ms_setup, nd = _timed(lambda: keep[-1].setup_coarse_solver(op))
+            lams_c.append(1.0)
+            report(tag, "setup_coarse_solver_continuous", ms_setup, nd, None, None, f"{nd} continuous DoFs")
+            x.zero_()
+            fine.cg_solve(op, b, x, rtol=1e-8, maxit=400, precond="vcycle", lam_hi_per_level=lams_c)
+            x.zero_()
+            ms, (it, rr) = _timed(lambda: fine.cg_solve(op, b, x, rtol=1e-8, maxit=400, precond="vcycle",
+                                                        lam_hi_per_level=lams_c))
+            report(tag, "pcg_vcycle_cph_c_level", ms, N, None, None,
+                   f"{it} iterations (relres {rr:.1e}); {ms / max(it, 1):.2f} ms/it; DG p -> c (Q1) -> Q1 h -> direct")
+            ms = timeit(lambda: fine.vcycle(op, b, x, lams_c), 5, reps)
+            report(tag, "vcycle_cph_c_level", ms, N, None, None, f"{fine.chain_levels()} levels")
+            del keep, fine, ctxs
             torch.cuda.empty_cache()
 
 
