@@ -60,4 +60,9 @@ for arg in sys.argv[1:]:
         traffic[tag] = o["dram_bytes"]
     res[tag] = o
 print(json.dumps(res, indent=1))
-json.dump(traffic, open("profiles/ncu_traffic.json", "w"), indent=1)
+try:                                             # merge: keep the other kernels' entries
+    old = json.load(open("profiles/ncu_traffic.json"))
+except (OSError, ValueError):
+    old = {}
+old.update(traffic)
+json.dump(old, open("profiles/ncu_traffic.json", "w"), indent=1)
