@@ -376,11 +376,14 @@ dgvv_status op_ready(dgvv_ctx* c, int op) {
 
 // launch one apply in a given mode.  Multi-GPU: interior cells run while NCCL moves the
 // ghost cells on the comm stream; cells with a ghost neighbour run after the exchange event.
-dgvv_status run_apply(dgvv_ctx* c, int op, int l, ApplyArgs a, cudaStream_t s, bool newton = false) {
+// kind: 0 plain operator, 1 Newton-linearised (K2), 2 viscous + fused convective term (f4)
+dgvv_status run_apply(dgvv_ctx* c, int op, int l, ApplyArgs a, cudaStream_t s, int kind = 0) {
   const int nc = op == DGVV_OP_VISCOUS ? 3 : 1;
   const int form = op == DGVV_OP_VISCOUS ? c->form : DGVV_FORM_LAPLACE;
   auto launch = [&](const ApplyArgs& x) -> dgvv_status {
-    cudaError_t e = newton ? launch_newton(c->L[l].n, c->geo, x, s) : launch_apply(nc, c->L[l].n, form, c->geo, x, s);
+    cudaError_t e = kind == 1 ? launch_newton(c->L[l].n, c->geo, x, s)
+                  : kind == 2 ? launch_apply_oseen(c->L[l].n, c->geo, x, s)
+                              : launch_apply(nc, c->L[l].n, form, c->geo, x, s);
     if (e == cudaErrorNotSupported) return dgvv_fail(DGVV_EUNSUPPORTED, "kernel not built for degree %d", c->L[l].k);
     if (e != cudaSuccess) return dgvv_fail(DGVV_ECUDA, "apply kernel: %s", cudaGetErrorString(e));
     return DGVV_OK;
@@ -1024,7 +1027,7 @@ dgvv_status dgvv_apply_linearized_viscous(dgvv_ctx* c, const double* src, double
   a.ulin = c->ulin;
   a.ulin_ghost = c->L[0].ulin_ghost;
   for (int i = 0; i < 4; ++i) a.law[i] = c->visc.p[i];
-  return run_apply(c, DGVV_OP_VISCOUS, 0, a, s, true);
+  return run_apply(c, DGVV_OP_VISCOUS, 0, a, s, 1);
 }
 
 static dgvv_status ensure_dinv_pen(dgvv_ctx* c, cudaStream_t s);
@@ -1651,6 +1654,12 @@ static dgvv_status apply_oseen(dgvv_ctx* c, double alpha_c, const double* src, d
   a.src = src;
   a.dst = dst;
   if (rhs) { a.b = rhs; a.mode = MODE_RESID; }
+  if (alpha_c != 0.0 && c->form == DGVV_FORM_DIVERGENCE) {   // one fused kernel (viscous + mass + convective)
+    a.wtr = c->d_wtr;
+    a.wtr_ghost = c->wtr_ghost;
+    a.alpha_c = alpha_c;
+    return run_apply(c, DGVV_OP_VISCOUS, 0, a, s, 2);
+  }
   TRY(run_apply(c, DGVV_OP_VISCOUS, 0, a, s));     // leaves the ghosts of src in L[0].ghost[0]
   if (alpha_c != 0.0) TRY(launch_conv(c, src, dst, rhs ? -alpha_c : alpha_c, 1, s));
   return DGVV_OK;

@@ -71,6 +71,10 @@ struct ApplyArgsT {  // R = double (operators) or float (FP32 multigrid levels, 
   const R* jxw;        // general geometry: JxW [n_owned][n^3]
   const R* fdA;        // general geometry: dA  [n_total][6][n^2]
   double law[4];            // eta0, eta_inf, lambda, n
+  // f4 fused convective term (CONV instantiation): + alpha_c C(w) src
+  const R* wtr;        // transport field, owned [n_owned][3][n^3]
+  const R* wtr_ghost;  // ghost [n_ghost][3][n^3]
+  double alpha_c;
 };
 using ApplyArgs = ApplyArgsT<double>;
 

@@ -75,6 +75,34 @@ static cudaError_t launch_visc_t(int n, int form, int geo, const ApplyArgsT<R>& 
   }
 }
 
+// f4: viscous apply with the convective term fused (divergence form, FP64, mass term included)
+template <int n, int GEO>
+static cudaError_t run_oseen(const ApplyArgs& a, cudaStream_t s) {
+  constexpr int CPB = cpb_visc<n, GEO>();
+  const size_t smem = (size_t)CPB * Apply2Cfg<n, 3, 0, GEO>::CS * sizeof(double);
+  auto k = sipg_apply2_kernel<double, n, 3, 0, GEO, CPB, minb_visc<n, GEO>(), true, true>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  if (a.n_proc <= 0) return cudaSuccess;
+  k<<<(a.n_proc + CPB - 1) / CPB, CPB * n * n, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_apply_oseen(int n, int geo, const ApplyArgs& a, cudaStream_t s) {
+  switch (n) {
+    case 2: return geo ? run_oseen<2, 1>(a, s) : run_oseen<2, 0>(a, s);
+    case 3: return geo ? run_oseen<3, 1>(a, s) : run_oseen<3, 0>(a, s);
+    case 4: return geo ? run_oseen<4, 1>(a, s) : run_oseen<4, 0>(a, s);
+    case 5: return geo ? run_oseen<5, 1>(a, s) : run_oseen<5, 0>(a, s);
+    case 6: return geo ? run_oseen<6, 1>(a, s) : run_oseen<6, 0>(a, s);
+    default: return cudaErrorNotSupported;
+  }
+}
+
 cudaError_t launch_apply_visc(int n, int form, int geo, const ApplyArgs& a, cudaStream_t s) {
   return launch_visc_t<double>(n, form, geo, a, s);
 }

@@ -19,6 +19,8 @@ cudaError_t launch_apply(int nc, int n, int form, int geo, const ApplyArgs& a, c
 cudaError_t launch_apply_f(int nc, int n, int form, int geo, const ApplyArgsT<float>& a, cudaStream_t s);
 // f2: divergence/continuity penalty operator (apply, or inverse diagonal when diag = true)
 cudaError_t launch_penalty(int n, int geo, const PenaltyArgs& a, bool diag, cudaStream_t s);
+// f4: viscous apply (divergence form, + mass M) with the convective term alpha_c C(w) fused in
+cudaError_t launch_apply_oseen(int n, int geo, const ApplyArgs& a, cudaStream_t s);
 // f4: dst (+)= alpha C(w) src (upwind convective term)
 cudaError_t launch_convective(int n, int geo, const ConvArgs& a, cudaStream_t s);
 // f3: h-transfer between nested refinements (octant = ox + 2 oy + 4 oz; child[p * 8 + octant])

@@ -233,7 +233,7 @@ def run_f4(reps):
         report(name + "+f4", "apply_convective", ms, N, byt, None, "upwind convective term C(w) u")
         ctx.set_mass(0, 1.0e3)
         ms = timeit(lambda: ctx.apply_oseen(src, dst, 1.0), 20, reps)
-        report(name + "+f4", "apply_oseen", ms, N, None, None, "mass M + A(nu) + C(w): viscous apply + convective kernel")
+        report(name + "+f4", "apply_oseen", ms, N, None, None, "mass M + A(nu) + C(w): one fused kernel")
         lams = [1.2 * ctx.estimate_lambda_max(0, dev(uniform(2, 3 * m.n_cells * (kk + 1) ** 3)), level=l, steps=15)
                 for l, kk in enumerate(degs)]
         for pc in ("vcycle", "vcycle_fp32"):

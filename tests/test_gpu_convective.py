@@ -243,3 +243,14 @@ def test_convective_multirank_bitwise():
         outs.append(y)
     torch.cuda.synchronize()
     assert torch.equal(torch.cat(outs), ref)
+    # the fused operator mass M + A + C (one kernel) is partition-independent too
+    for c in [ref_ctx] + ctxs:
+        c.set_mass(0, 7.0)
+    ref_ctx.apply_oseen(src, ref, alpha_c=1.0)
+    outs = []
+    for c, x in zip(ctxs, locs):
+        y = torch.empty_like(x)
+        c.apply_oseen(x, y, alpha_c=1.0)
+        outs.append(y)
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat(outs), ref)
