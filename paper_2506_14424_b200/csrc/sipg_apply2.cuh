@@ -361,10 +361,20 @@ sipg_apply2_kernel(const ApplyArgsT<R> A) {
         const double* lO = s ? T.l0 : T.l1;
         const double* dO = s ? T.d0 : T.d1;
         const int sl = lc + (nbv - cell);
+#if defined(DGVV_DIAG_LOCALNB)
+        // diagnostic only (wrong values): y (and z if DGVV_DIAG_LOCALNB > 1) neighbours read from this
+        // cell's own smem copy -- the upper bound of what cluster/DSMEM staging could gain
+        const bool in_cta = (d == 1 || (d == 2 && DGVV_DIAG_LOCALNB > 1)) ? true : (sl >= 0 && sl < CPB && sid[sl] == nbv);
+#else
         const bool in_cta = sl >= 0 && sl < CPB && sid[sl] == nbv;
+#endif
         const R* pn = nbv < A.n_owned ? A.src + (size_t)nbv * NC * n3
                                            : A.ghost + (size_t)(nbv - A.n_owned) * NC * n3;
+#if defined(DGVV_DIAG_LOCALNB)
+        const R* ns = smem + ((in_cta && d == 0) ? sl : lc) * Cf::CS;
+#else
         const R* ns = smem + (in_cta ? sl : 0) * Cf::CS;
+#endif
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
           R x[n];
