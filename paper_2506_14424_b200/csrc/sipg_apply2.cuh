@@ -25,6 +25,9 @@
 #ifndef DGVV_FACE_TMA
 #define DGVV_FACE_TMA 1   // stage the general-geometry face metric with TMA bulk copies
 #endif
+#ifndef DGVV_FACE_TMA_CART
+#define DGVV_FACE_TMA_CART 1   // stage the Cartesian face viscosities with TMA bulk copies
+#endif
 #ifndef USE_ST
 #define USE_ST 0          // keep a transposed [c][z][x][y] copy of the cell (16-byte y-lines)
 #endif
@@ -64,7 +67,13 @@ struct Apply2Cfg {
   // general geometry, n even: the face metric of one direction (own J^-1 and nu*dA of both
   // faces, the two neighbours' of their opposite faces) is staged by TMA bulk copies
   static constexpr bool TMA = (GEO == 1) && (n % 2 == 0) && (DGVV_FACE_TMA != 0);
-  static constexpr int STG = TMA ? 40 * L::n2 : 0;
+  // Cartesian divergence form, n even: the face viscosities of all six faces (own, and each
+  // neighbour's opposite face) are staged by TMA bulk copies issued at kernel start
+  // (DGVV_FACE_TMA_CART; measured: C5 3246 -> 3040 us; slower for the scalar Poisson operator and
+  // as per-direction stages)
+  static constexpr bool TMAC = (GEO == 0) && (n % 2 == 0) && (FORM == 0) && (DGVV_FACE_TMA_CART != 0);
+  static constexpr bool STAGE = TMA || TMAC;
+  static constexpr int STG = TMA ? 40 * L::n2 : (TMAC ? 12 * L::n2 : 0);
   static constexpr int CS = (1 + USE_ST) * VOL + RW + STG;         // doubles of smem per cell
 };
 
@@ -169,6 +178,18 @@ sipg_apply2_kernel(const ApplyArgsT<R> A) {
   R* stg = smem + lc * Cf::CS + (Cf::CS - Cf::STG);   // face-metric stage (TMA)
   // issue the TMA bulk copies of direction d's face metric for this cell (thread p == 0)
   auto stage_issue = [&](int d, const int (&nb)[6]) {
+    if constexpr (Cf::TMAC) {          // all six faces at once (issued at kernel start, d ignored)
+      constexpr uint32_t BN = n2 * sizeof(R);
+      uint32_t bytes = 6 * BN;
+#pragma unroll
+      for (int f = 0; f < 6; ++f) bytes += nb[f] >= 0 ? BN : 0;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(&mbar[lc], bytes);
+      tma_load_1d(stg, A.nu_face + (size_t)cell * 6 * n2, 6 * BN, &mbar[lc]);
+#pragma unroll
+      for (int f = 0; f < 6; ++f)
+        if (nb[f] >= 0) tma_load_1d(stg + (6 + f) * n2, A.nu_face + ((size_t)nb[f] * 6 + (f ^ 1)) * n2, BN, &mbar[lc]);
+    }
     if constexpr (Cf::TMA) {
       constexpr uint32_t BJ = 9 * n2 * sizeof(R), BN = n2 * sizeof(R);
       uint32_t bytes = 2 * (BJ + BN);
@@ -218,7 +239,7 @@ sipg_apply2_kernel(const ApplyArgsT<R> A) {
   int nbf[6];
 #pragma unroll
   for (int f = 0; f < 6; ++f) nbf[f] = __ldg(A.nbr + cell * 6 + f);
-  if constexpr (Cf::TMA) {
+  if constexpr (Cf::STAGE) {
     if (p == 0) {
       mbar_init(&mbar[lc], 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -256,7 +277,7 @@ sipg_apply2_kernel(const ApplyArgsT<R> A) {
       }
       R Ji[9], w;
       if constexpr (GEO == 0) {
-        w = A.nu_cell[(size_t)cell * n3 + q] * wab * R(T.w[z]) * vol;
+        w = A.nu_cell[(size_t)DIAG_VC(cell) * n3 + q] * wab * R(T.w[z]) * vol;
       } else {
         const R* vm = A.vJi + (size_t)DIAG_VC(cell) * 9 * n3 + q;
 #pragma unroll
@@ -491,13 +512,20 @@ sipg_apply2_kernel(const ApplyArgsT<R> A) {
       if constexpr (GEO == 0) {
         // ---------------- Cartesian: n = sgn e_d, J^-1 = diag(1/h)
         const R sgn = s ? R(1.0) : -R(1.0);
-        const R num = A.nu_face[((size_t)cell * 6 + f) * n2 + p];
-        R nup = num, Hp = Hm;
+        R num, nup, Hp = Hm;
+        if constexpr (Cf::TMAC) {
+          if (dd == 0 && s == 0) mbar_wait(&mbar[lc], 0);
+          num = stg[f * n2 + p];
+        } else {
+          num = A.nu_face[((size_t)DIAG_FC(cell) * 6 + f) * n2 + p];
+        }
+        nup = num;
         R ihp[3] = {ih[0], ih[1], ih[2]};
         if (inter) {
           const R* cg = A.cart + (size_t)nbv * CART_STRIDE;
           ihp[0] = cg[0]; ihp[1] = cg[1]; ihp[2] = cg[2]; Hp = cg[3];
-          nup = A.nu_face[((size_t)nbv * 6 + (f ^ 1)) * n2 + p];
+          if constexpr (Cf::TMAC) nup = stg[(6 + f) * n2 + p];
+          else nup = A.nu_face[((size_t)DIAG_FC(nbv) * 6 + (f ^ 1)) * n2 + p];
         }
         const R dA = R(T.w[a]) * R(T.w[b]) * vol * ih[d];
         const R tau = R(A.pen) * fmax(Hm, Hp) * R(0.5) * (num + nup);
