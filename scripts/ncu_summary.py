@@ -21,7 +21,11 @@ STALLS = ["long_scoreboard", "wait", "short_scoreboard", "barrier", "mio_throttl
 
 
 def raw(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    """A .ncu-rep (read with ncu) or the CSV of its raw page (exported on the GPU box)."""
+    if rep.endswith(".csv"):
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     r = list(csv.reader(io.StringIO(out)))
     return dict(zip(r[0], r[1])), dict(zip(r[0], r[2]))
 
@@ -55,6 +59,16 @@ for arg in sys.argv[1:]:
         if k in d and d[k] not in ("", None):
             st[s] = float(d[k])
     o["stall_cycles_per_issue"] = {k: round(v, 2) for k, v in sorted(st.items(), key=lambda x: -x[1])[:6]}
+    samp = {}
+    for k, v in d.items():                         # sampled stall reasons (share of all samples)
+        if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued") and v not in ("", None):
+            try:
+                samp[k.split("stalled_")[1]] = float(v.replace(",", ""))
+            except ValueError:
+                pass
+    if samp:
+        tot_s = sum(samp.values())
+        o["stall_samples_share"] = {k: round(v / tot_s, 3) for k, v in sorted(samp.items(), key=lambda x: -x[1])[:6]}
     if "dram_read" in o and "dram_write" in o:
         o["dram_bytes"] = o["dram_read"] + o["dram_write"]
         traffic[tag] = o["dram_bytes"]
