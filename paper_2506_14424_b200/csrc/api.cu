@@ -174,6 +174,9 @@ struct dgvv_ctx {
   double* d_wtr = nullptr;
   double* wtr_ghost = nullptr;
   bool has_wtr = false;
+  double* d_wref = nullptr;                  // convective point data for the fused apply (lazy)
+  double* d_wface = nullptr;
+  bool wq_stale = true;
   double* gm_work = nullptr;                 // r, w, V[0..m], Z[0..m-1]
   int gm_restart = 0;
   double* gm_H = nullptr;                    // device Hessenberg column
@@ -1635,6 +1638,8 @@ dgvv_status dgvv_set_transport(dgvv_ctx* c, const double* w, dgvv_stream stream)
   if (!std::isfinite(ww)) return dgvv_fail(DGVV_EDOMAIN, "transport field has non-finite entries");
   if (c->n_ghost) TRY(exchange_sync(c, 0, 3, c->d_wtr, c->wtr_ghost, s));
   c->has_wtr = true;
+  c->wq_stale = true;                        // point data derived at the next fused apply (after the
+                                             // caller filled external-mode transport ghosts)
   return DGVV_OK;
 }
 
@@ -1655,8 +1660,16 @@ static dgvv_status apply_oseen(dgvv_ctx* c, double alpha_c, const double* src, d
   a.dst = dst;
   if (rhs) { a.b = rhs; a.mode = MODE_RESID; }
   if (alpha_c != 0.0 && c->form == DGVV_FORM_DIVERGENCE) {   // one fused kernel (viscous + mass + convective)
-    a.wtr = c->d_wtr;
-    a.wtr_ghost = c->wtr_ghost;
+    if (c->wq_stale) {
+      const size_t n3 = (size_t)c->L[0].n * c->L[0].n * c->L[0].n, n2 = (size_t)c->L[0].n * c->L[0].n;
+      if (!c->d_wref) TRY(dalloc(c, &c->d_wref, (size_t)c->n_owned * 3 * n3));
+      if (!c->d_wface) TRY(dalloc(c, &c->d_wface, (size_t)c->n_owned * 6 * n2));
+      cudaError_t e = launch_conv_pointdata(c->L[0].n, c->geo, conv_args(c), c->d_wref, c->d_wface, s);
+      if (e != cudaSuccess) return dgvv_fail(DGVV_ECUDA, "convective point data: %s", cudaGetErrorString(e));
+      c->wq_stale = false;
+    }
+    a.wref = c->d_wref;
+    a.wface = c->d_wface;
     a.alpha_c = alpha_c;
     return run_apply(c, DGVV_OP_VISCOUS, 0, a, s, 2);
   }

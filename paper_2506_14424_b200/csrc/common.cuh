@@ -72,8 +72,8 @@ struct ApplyArgsT {  // R = double (operators) or float (FP32 multigrid levels, 
   const R* fdA;        // general geometry: dA  [n_total][6][n^2]
   double law[4];            // eta0, eta_inf, lambda, n
   // f4 fused convective term (CONV instantiation): + alpha_c C(w) src
-  const R* wtr;        // transport field, owned [n_owned][3][n^3]
-  const R* wtr_ghost;  // ghost [n_ghost][3][n^3]
+  const R* wref;       // JxW J^-1 w at cell points [n_owned][3][n^3] (convective_apply.cuh)
+  const R* wface;      // min({{w}}.n, 0) dA at own face points [n_owned][6][n^2]
   double alpha_c;
 };
 using ApplyArgs = ApplyArgsT<double>;

@@ -215,4 +215,74 @@ __global__ void __launch_bounds__(CPB * n * n) convective_apply_kernel(const Con
   }
 }
 
+// Quadrature-point data of the convective term for the fused viscous + convective apply
+// (sipg_apply2.cuh, CONV), derived once per transport field (the analogue of the stored viscosity):
+//   wref[cell][k][q]  = JxW_q sum_j Ji[k][j](q) w_j(q)     (reference transport direction times JxW)
+//   wface[cell][f][p] = min({{w}}.n, 0) dA                  (own side; 0 on boundary faces, F4b)
+// One thread per cell point / face point, plain global loads (setup-time kernel).
+template <int n, int GEO>
+__global__ void conv_pointdata_kernel(const ConvArgs A, double* wref, double* wface) {
+  constexpr int n2 = n * n, n3 = n2 * n;
+  const Tab1D& T = c_tab[n];
+  const long nvol = (long)A.n_owned * n3, nfac = (long)A.n_owned * 6 * n2;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < nvol + nfac; i += (long)gridDim.x * blockDim.x) {
+    if (i < nvol) {
+      const int cell = (int)(i / n3), q = (int)(i % n3);
+      const int a = q % n, b = (q / n) % n, z = q / n2;
+      const double* w = A.w + (size_t)cell * 3 * n3 + q;
+      const double w0 = w[0], w1 = w[n3], w2 = w[2 * n3];
+      double r[3];
+      if constexpr (GEO == 0) {
+        const double* cg = A.cart + (size_t)cell * CART_STRIDE;
+        const double jxw = T.w[a] * T.w[b] * T.w[z] * cg[4];
+        r[0] = jxw * cg[0] * w0; r[1] = jxw * cg[1] * w1; r[2] = jxw * cg[2] * w2;
+      } else {
+        const double* Ji = A.vJi + (size_t)cell * 9 * n3 + q;
+        const double jxw = A.jxw[(size_t)cell * n3 + q];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) r[k] = jxw * (Ji[(3 * k) * n3] * w0 + Ji[(3 * k + 1) * n3] * w1 + Ji[(3 * k + 2) * n3] * w2);
+      }
+#pragma unroll
+      for (int k = 0; k < 3; ++k) wref[(size_t)cell * 3 * n3 + k * n3 + q] = r[k];
+    } else {
+      const long j = i - nvol;
+      const int cell = (int)(j / (6 * n2)), f = (int)((j / n2) % 6), p = (int)(j % n2);
+      const int a = p % n, b = p / n, d = f >> 1, s = f & 1;
+      const int nbv = A.nbr[cell * 6 + f];
+      double out = 0.0;
+      if (nbv >= 0) {
+        const double* wo = A.w + (size_t)cell * 3 * n3;
+        const double* wn = nbv < A.n_owned ? A.w + (size_t)nbv * 3 * n3 : A.wghost + (size_t)(nbv - A.n_owned) * 3 * n3;
+        const double* lS = s ? T.l1 : T.l0;
+        const double* lO = s ? T.l0 : T.l1;
+        const double sgn = s ? 1.0 : -1.0;
+        auto trace = [&](const double* base, int c, const double* l) {
+          double v = 0.0;
+          for (int ii = 0; ii < n; ++ii) {
+            const int idx = (d == 2) ? ii * n2 + p : (d == 0 ? b * n2 + a * n + ii : b * n2 + ii * n + a);
+            v = fma(l[ii], base[c * n3 + idx], v);
+          }
+          return v;
+        };
+        double wnv, dA;
+        if constexpr (GEO == 0) {
+          const double* cg = A.cart + (size_t)cell * CART_STRIDE;
+          wnv = 0.5 * (trace(wo, d, lS) + trace(wn, d, lO)) * sgn;
+          dA = T.w[a] * T.w[b] * cg[4] * cg[d];
+        } else {
+          const double* fm = A.fJi + ((size_t)cell * 6 + f) * 9 * n2 + p;
+          const double v0 = fm[(3 * d) * n2], v1 = fm[(3 * d + 1) * n2], v2 = fm[(3 * d + 2) * n2];
+          const double il = sgn * rsqrt(v0 * v0 + v1 * v1 + v2 * v2);
+          const double nr[3] = {v0 * il, v1 * il, v2 * il};
+          wnv = 0.0;
+          for (int c = 0; c < 3; ++c) wnv += 0.5 * (trace(wo, c, lS) + trace(wn, c, lO)) * nr[c];
+          dA = A.fdA[((size_t)cell * 6 + f) * n2 + p];
+        }
+        out = wnv < 0.0 ? wnv * dA : 0.0;
+      }
+      wface[j] = out;
+    }
+  }
+}
+
 }  // namespace dgvv

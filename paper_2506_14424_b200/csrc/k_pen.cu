@@ -4,6 +4,8 @@
 #include "convective_apply.cuh"
 #include "launch.h"
 
+#include <algorithm>
+
 namespace dgvv {
 
 cudaError_t upload_tables_pen(const Tab1D* tabs) { return tu_upload_tables(tabs); }
@@ -58,6 +60,26 @@ static cudaError_t conv_run(const ConvArgs& a, cudaStream_t s) {
   if (a.n_proc <= 0) return cudaSuccess;
   k<<<(a.n_proc + CPB - 1) / CPB, CPB * n * n, smem, s>>>(a);
   return cudaGetLastError();
+}
+
+template <int n, int GEO>
+static cudaError_t conv_pd_run(const ConvArgs& a, double* wref, double* wface, cudaStream_t s) {
+  const long tot = (long)a.n_owned * (n * n * n + 6 * n * n);
+  if (tot <= 0) return cudaSuccess;
+  const int blocks = (int)std::min<long>(148L * 16, (tot + 255) / 256);
+  conv_pointdata_kernel<n, GEO><<<blocks, 256, 0, s>>>(a, wref, wface);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_conv_pointdata(int n, int geo, const ConvArgs& a, double* wref, double* wface, cudaStream_t s) {
+  switch (n) {
+    case 2: return geo ? conv_pd_run<2, 1>(a, wref, wface, s) : conv_pd_run<2, 0>(a, wref, wface, s);
+    case 3: return geo ? conv_pd_run<3, 1>(a, wref, wface, s) : conv_pd_run<3, 0>(a, wref, wface, s);
+    case 4: return geo ? conv_pd_run<4, 1>(a, wref, wface, s) : conv_pd_run<4, 0>(a, wref, wface, s);
+    case 5: return geo ? conv_pd_run<5, 1>(a, wref, wface, s) : conv_pd_run<5, 0>(a, wref, wface, s);
+    case 6: return geo ? conv_pd_run<6, 1>(a, wref, wface, s) : conv_pd_run<6, 0>(a, wref, wface, s);
+    default: return cudaErrorNotSupported;
+  }
 }
 
 cudaError_t launch_convective(int n, int geo, const ConvArgs& a, cudaStream_t s) {

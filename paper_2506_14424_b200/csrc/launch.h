@@ -21,6 +21,8 @@ cudaError_t launch_apply_f(int nc, int n, int form, int geo, const ApplyArgsT<fl
 cudaError_t launch_penalty(int n, int geo, const PenaltyArgs& a, bool diag, cudaStream_t s);
 // f4: viscous apply (divergence form, + mass M) with the convective term alpha_c C(w) fused in
 cudaError_t launch_apply_oseen(int n, int geo, const ApplyArgs& a, cudaStream_t s);
+// f4: quadrature-point data of the convective term for the fused apply (wref, wface)
+cudaError_t launch_conv_pointdata(int n, int geo, const ConvArgs& a, double* wref, double* wface, cudaStream_t s);
 // f4: dst (+)= alpha C(w) src (upwind convective term)
 cudaError_t launch_convective(int n, int geo, const ConvArgs& a, cudaStream_t s);
 // f3: h-transfer between nested refinements (octant = ox + 2 oy + 4 oz; child[p * 8 + octant])

@@ -286,20 +286,12 @@ sipg_apply2_kernel(const ApplyArgsT<R> A) {
       }
       if constexpr (CONV) {
         // f4 (fused): + alpha_c JxW (w.grad) u at the point (collocation: the test function is the
-        // point value); transport direction in reference coordinates wr_k = sum_j Ji[k][j] w_j
-        const R* gw = A.wtr + (size_t)cell * 3 * n3 + q;
-        const R w0 = __ldg(gw), w1 = __ldg(gw + n3), w2 = __ldg(gw + 2 * n3);
-        R wr[3], jw;
-        if constexpr (GEO == 0) {
-          wr[0] = ih[0] * w0; wr[1] = ih[1] * w1; wr[2] = ih[2] * w2;
-          jw = R(A.alpha_c) * wab * R(T.w[z]) * vol;
-        } else {
+        // point value), from the stored reference transport direction wref = JxW J^-1 w
+        const R* gw = A.wref + (size_t)cell * 3 * n3 + q;
+        const R ac = R(A.alpha_c);
+        const R wr0 = ac * __ldg(gw), wr1 = ac * __ldg(gw + n3), wr2 = ac * __ldg(gw + 2 * n3);
 #pragma unroll
-          for (int k = 0; k < 3; ++k) wr[k] = Ji[3 * k] * w0 + Ji[3 * k + 1] * w1 + Ji[3 * k + 2] * w2;
-          jw = R(A.alpha_c) * A.jxw[(size_t)cell * n3 + q];
-        }
-#pragma unroll
-        for (int c = 0; c < NC; ++c) y[c][z] = fma(jw, gxi[c][0] * wr[0] + gxi[c][1] * wr[1] + gxi[c][2] * wr[2], y[c][z]);
+        for (int c = 0; c < NC; ++c) y[c][z] = fma(gxi[c][0], wr0, fma(gxi[c][1], wr1, fma(gxi[c][2], wr2, y[c][z])));
       }
       R G[NC][3];
 #pragma unroll
@@ -637,42 +629,11 @@ sipg_apply2_kernel(const ApplyArgsT<R> A) {
       }
       if constexpr (CONV) {
         // f4 (fused): upwind flux of the convective term, a value term of this side's test
-        // functions: min({{w}}.n, 0) (u+ - u-) dA on interior/periodic faces (readings F4a/F4b)
-        if (inter) {
-          const R* wo = A.wtr + (size_t)cell * 3 * n3;
-          const R* wn_ = nbv < A.n_owned ? A.wtr + (size_t)nbv * 3 * n3 : A.wtr_ghost + (size_t)(nbv - A.n_owned) * 3 * n3;
-          const double* lS = s ? T.l1 : T.l0;
-          const double* lO = s ? T.l0 : T.l1;
-          const R sgnw = s ? R(1.0) : -R(1.0);
-          auto trace = [&](const R* base, int c, const double* l) -> R {
-            R v = R(0.0);
+        // functions: min({{w}}.n, 0) dA (u+ - u-) on interior/periodic faces (readings F4a/F4b),
+        // with the stored face factor (0 where this side is outflow and on boundary faces)
+        const R cf = R(A.alpha_c) * __ldg(A.wface + ((size_t)cell * 6 + f) * n2 + p);
 #pragma unroll
-            for (int i = 0; i < n; ++i) {
-              const int idx = (d == 2) ? i * n2 + p : (d == 0 ? b * n2 + a * n + i : b * n2 + i * n + a);
-              v = fma(R(l[i]), __ldg(base + c * n3 + idx), v);
-            }
-            return v;
-          };
-          R wnv, dAr;
-          if constexpr (GEO == 0) {
-            wnv = R(0.5) * (trace(wo, d, lS) + trace(wn_, d, lO)) * sgnw;
-            dAr = R(T.w[a]) * R(T.w[b]) * vol * ih[d];
-          } else {
-            R nr[3];
-            const R v0 = Jim[3 * d], v1 = Jim[3 * d + 1], v2 = Jim[3 * d + 2];
-            const R il = sgnw * rsqrt(v0 * v0 + v1 * v1 + v2 * v2);
-            nr[0] = v0 * il; nr[1] = v1 * il; nr[2] = v2 * il;
-            wnv = R(0.0);
-#pragma unroll
-            for (int c = 0; c < 3; ++c) wnv += R(0.5) * (trace(wo, c, lS) + trace(wn_, c, lO)) * nr[c];
-            dAr = A.fdA[((size_t)cell * 6 + f) * n2 + p];
-          }
-          if (wnv < R(0.0)) {
-            const R cf = R(A.alpha_c) * dAr * wnv;
-#pragma unroll
-            for (int c = 0; c < NC; ++c) fv[s][c] = fma(cf, up[s][c] - um[s][c], fv[s][c]);
-          }
-        }
+        for (int c = 0; c < NC; ++c) fv[s][c] = fma(cf, up[s][c] - um[s][c], fv[s][c]);
       }
       if constexpr (NT > 0) {
 #pragma unroll
