@@ -1609,6 +1609,19 @@ static ConvArgs conv_args(dgvv_ctx* c) {
   return a;
 }
 
+// quadrature-point data of w (JxW J^-1 w, min({{w}}.n, 0) dA), derived at the first use after
+// dgvv_set_transport (external-exchange mode: after the caller filled the transport ghosts)
+static dgvv_status ensure_conv_pointdata(dgvv_ctx* c, cudaStream_t s) {
+  if (!c->wq_stale) return DGVV_OK;
+  const size_t n3 = (size_t)c->L[0].n * c->L[0].n * c->L[0].n, n2 = (size_t)c->L[0].n * c->L[0].n;
+  if (!c->d_wref) TRY(dalloc(c, &c->d_wref, (size_t)c->n_owned * 3 * n3));
+  if (!c->d_wface) TRY(dalloc(c, &c->d_wface, (size_t)c->n_owned * 6 * n2));
+  cudaError_t e = launch_conv_pointdata(c->L[0].n, c->geo, conv_args(c), c->d_wref, c->d_wface, s);
+  if (e != cudaSuccess) return dgvv_fail(DGVV_ECUDA, "convective point data: %s", cudaGetErrorString(e));
+  c->wq_stale = false;
+  return DGVV_OK;
+}
+
 // dst (+)= alpha C(w) src; the ghosts of src must already be in L[0].ghost[0]
 static dgvv_status launch_conv(dgvv_ctx* c, const double* src, double* dst, double alpha, int accumulate,
                                cudaStream_t s) {
@@ -1617,7 +1630,8 @@ static dgvv_status launch_conv(dgvv_ctx* c, const double* src, double* dst, doub
   a.dst = dst;
   a.alpha = alpha;
   a.accumulate = accumulate;
-  cudaError_t e = launch_convective(c->L[0].n, c->geo, a, s);
+  TRY(ensure_conv_pointdata(c, s));
+  cudaError_t e = launch_convective_pd(c->L[0].n, a, c->d_wref, c->d_wface, s);
   if (e == cudaErrorNotSupported) return dgvv_fail(DGVV_EUNSUPPORTED, "convective kernel not built for degree %d", c->L[0].k);
   if (e != cudaSuccess) return dgvv_fail(DGVV_ECUDA, "convective kernel: %s", cudaGetErrorString(e));
   return DGVV_OK;
@@ -1660,14 +1674,7 @@ static dgvv_status apply_oseen(dgvv_ctx* c, double alpha_c, const double* src, d
   a.dst = dst;
   if (rhs) { a.b = rhs; a.mode = MODE_RESID; }
   if (alpha_c != 0.0 && c->form == DGVV_FORM_DIVERGENCE) {   // one fused kernel (viscous + mass + convective)
-    if (c->wq_stale) {
-      const size_t n3 = (size_t)c->L[0].n * c->L[0].n * c->L[0].n, n2 = (size_t)c->L[0].n * c->L[0].n;
-      if (!c->d_wref) TRY(dalloc(c, &c->d_wref, (size_t)c->n_owned * 3 * n3));
-      if (!c->d_wface) TRY(dalloc(c, &c->d_wface, (size_t)c->n_owned * 6 * n2));
-      cudaError_t e = launch_conv_pointdata(c->L[0].n, c->geo, conv_args(c), c->d_wref, c->d_wface, s);
-      if (e != cudaSuccess) return dgvv_fail(DGVV_ECUDA, "convective point data: %s", cudaGetErrorString(e));
-      c->wq_stale = false;
-    }
+    TRY(ensure_conv_pointdata(c, s));
     a.wref = c->d_wref;
     a.wface = c->d_wface;
     a.alpha_c = alpha_c;

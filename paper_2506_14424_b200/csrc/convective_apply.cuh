@@ -285,4 +285,135 @@ __global__ void conv_pointdata_kernel(const ConvArgs A, double* wref, double* wf
   }
 }
 
+// dst (+)= alpha C(w) src from the stored point data (wref, wface of conv_pointdata_kernel): no
+// geometry and no transport-field traces in the apply; the neighbour trace is read only where
+// this side is an inflow side (wface != 0).  Same team / layout as convective_apply_kernel.
+template <int n, int CPB>
+__global__ void __launch_bounds__(CPB * n * n) convective_pd_kernel(const ConvArgs A, const double* wref,
+                                                                     const double* wface) {
+  using L = Lay<n>;
+  constexpr int n2 = L::n2, n3 = L::n3, RS = L::RS, PS = L::PS, CST = L::CST, VOL = 3 * L::CST;
+  constexpr int CS = 2 * VOL;              // u | Y
+  extern __shared__ __align__(16) double csmem[];
+  __shared__ __align__(16) double sD[n * RS];
+  __shared__ int sid[CPB];
+  const Tab1D& T = c_tab[n];
+  const int lc = threadIdx.x / n2;
+  const int p = threadIdx.x - lc * n2;
+  const int a = p % n, b = p / n;
+  const int slot_raw = blockIdx.x * CPB + lc;
+  const bool active = slot_raw < A.n_proc;
+  const int cell = A.cell_base + (active ? slot_raw : A.n_proc - 1);
+  for (int i = threadIdx.x; i < n * RS; i += blockDim.x) {
+    const int r = i / RS, k = i - r * RS;
+    sD[i] = k < n ? T.D[r * DGVV_NMAX + k] : 0.0;
+  }
+  if (p == 0) sid[lc] = active ? cell : -1;
+  double* su = csmem + lc * CS;
+  double* Y = su + VOL;
+  double ucol[3][n], y[3][n];
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int z = 0; z < n; ++z) {
+      const double v = __ldg(A.src + (size_t)cell * 3 * n3 + c * n3 + z * n2 + p);
+      ucol[c][z] = v;
+      su[c * CST + z * PS + b * RS + a] = v;
+    }
+  int nbf[6];
+#pragma unroll
+  for (int f = 0; f < 6; ++f) nbf[f] = __ldg(A.nbr + cell * 6 + f);
+  __syncthreads();
+  {
+    double Da[n], Db[n];
+    ld_row<n>(sD + a * RS, Da);
+    ld_row<n>(sD + b * RS, Db);
+#pragma unroll
+    for (int z = 0; z < n; ++z) {
+      const double* gw = wref + (size_t)cell * 3 * n3 + z * n2 + p;
+      const double wr0 = A.alpha * __ldg(gw), wr1 = A.alpha * __ldg(gw + n3), wr2 = A.alpha * __ldg(gw + 2 * n3);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double gx = rowdot<n>(su + c * CST + z * PS + b * RS, Da);
+        double gy = 0.0, gz = 0.0;
+#pragma unroll
+        for (int k = 0; k < n; ++k) {
+          gy = fma(Db[k], su[c * CST + z * PS + k * RS + a], gy);
+          gz = fma(T.D[z * DGVV_NMAX + k], ucol[c][k], gz);
+        }
+        y[c][z] = gx * wr0 + gy * wr1 + gz * wr2;
+      }
+    }
+  }
+#pragma unroll
+  for (int dd = 0; dd < 3; ++dd) {
+    const int d = (dd == 0) ? 2 : dd - 1;
+    double val[2][3];
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const int f = 2 * d + s;
+      const int nbv = nbf[f];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) val[s][c] = 0.0;
+      const double cf = nbv >= 0 ? A.alpha * __ldg(wface + ((size_t)cell * 6 + f) * n2 + p) : 0.0;
+      if (cf != 0.0) {                         // inflow side of this cell: upwind from the neighbour
+        const double* lS = s ? T.l1 : T.l0;
+        const double* lO = s ? T.l0 : T.l1;
+        const int sl = lc + (nbv - cell);
+        const bool in_cta = sl >= 0 && sl < CPB && sid[sl] == nbv;
+        const double* pu = nbv < A.n_owned ? A.src + (size_t)nbv * 3 * n3 : A.ghost + (size_t)(nbv - A.n_owned) * 3 * n3;
+        const double* nsu = csmem + (in_cta ? sl : 0) * CS;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          double um = 0.0, up = 0.0;
+#pragma unroll
+          for (int i = 0; i < n; ++i) {
+            const double xm = (d == 2) ? ucol[c][i] : (d == 0 ? su[c * CST + b * PS + a * RS + i] : su[c * CST + b * PS + i * RS + a]);
+            double xp;
+            if (in_cta)
+              xp = (d == 2) ? nsu[c * CST + i * PS + b * RS + a]
+                            : (d == 0 ? nsu[c * CST + b * PS + a * RS + i] : nsu[c * CST + b * PS + i * RS + a]);
+            else
+              xp = (d == 2) ? __ldg(pu + c * n3 + i * n2 + p)
+                            : (d == 0 ? __ldg(pu + c * n3 + b * n2 + a * n + i) : __ldg(pu + c * n3 + b * n2 + i * n + a));
+            um = fma(lS[i], xm, um);
+            up = fma(lO[i], xp, up);
+          }
+          val[s][c] = cf * (up - um);
+        }
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      double add[n];
+#pragma unroll
+      for (int i = 0; i < n; ++i) add[i] = T.l0[i] * val[0][c] + T.l1[i] * val[1][c];
+      if (d == 2) {
+#pragma unroll
+        for (int i = 0; i < n; ++i) y[c][i] += add[i];
+      } else {
+        st_row<n>(Y + c * CST + b * PS + a * RS, add);
+      }
+    }
+    if (d != 2) {
+      __syncthreads();
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int z = 0; z < n; ++z) y[c][z] += (d == 0) ? Y[c * CST + z * PS + b * RS + a] : Y[c * CST + z * PS + a * RS + b];
+      __syncthreads();
+    }
+  }
+  if (active) {
+    const size_t off = (size_t)cell * 3 * n3;
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int z = 0; z < n; ++z) {
+        double* o = A.dst + off + c * n3 + z * n2 + p;
+        *o = A.accumulate ? *o + y[c][z] : y[c][z];
+      }
+  }
+}
+
 }  // namespace dgvv

@@ -82,6 +82,33 @@ cudaError_t launch_conv_pointdata(int n, int geo, const ConvArgs& a, double* wre
   }
 }
 
+template <int n>
+static cudaError_t conv_pd_apply(const ConvArgs& a, const double* wref, const double* wface, cudaStream_t s) {
+  constexpr int CPB = cpb_pen<n>();
+  const size_t smem = (size_t)CPB * 2 * 3 * Lay<n>::CST * sizeof(double);
+  auto k = convective_pd_kernel<n, CPB>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  if (a.n_proc <= 0) return cudaSuccess;
+  k<<<(a.n_proc + CPB - 1) / CPB, CPB * n * n, smem, s>>>(a, wref, wface);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_convective_pd(int n, const ConvArgs& a, const double* wref, const double* wface, cudaStream_t s) {
+  switch (n) {
+    case 2: return conv_pd_apply<2>(a, wref, wface, s);
+    case 3: return conv_pd_apply<3>(a, wref, wface, s);
+    case 4: return conv_pd_apply<4>(a, wref, wface, s);
+    case 5: return conv_pd_apply<5>(a, wref, wface, s);
+    case 6: return conv_pd_apply<6>(a, wref, wface, s);
+    default: return cudaErrorNotSupported;
+  }
+}
+
 cudaError_t launch_convective(int n, int geo, const ConvArgs& a, cudaStream_t s) {
   switch (n) {
     case 2: return geo ? conv_run<2, 1>(a, s) : conv_run<2, 0>(a, s);

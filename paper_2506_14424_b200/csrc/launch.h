@@ -23,6 +23,8 @@ cudaError_t launch_penalty(int n, int geo, const PenaltyArgs& a, bool diag, cuda
 cudaError_t launch_apply_oseen(int n, int geo, const ApplyArgs& a, cudaStream_t s);
 // f4: quadrature-point data of the convective term for the fused apply (wref, wface)
 cudaError_t launch_conv_pointdata(int n, int geo, const ConvArgs& a, double* wref, double* wface, cudaStream_t s);
+// f4: dst (+)= alpha C(w) src from the stored point data
+cudaError_t launch_convective_pd(int n, const ConvArgs& a, const double* wref, const double* wface, cudaStream_t s);
 // f4: dst (+)= alpha C(w) src (upwind convective term)
 cudaError_t launch_convective(int n, int geo, const ConvArgs& a, cudaStream_t s);
 // f3: h-transfer between nested refinements (octant = ox + 2 oy + 4 oz; child[p * 8 + octant])
