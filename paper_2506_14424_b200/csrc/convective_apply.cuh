@@ -4,216 +4,14 @@
 // (readings F4a-F4c: (w.grad)u form; Dirichlet faces carry {{w}} = 0 under the
 // mirror state, Neumann faces have no jump, so only interior/periodic faces contribute).
 // With the collocation basis (G2) the volume test functions are point values: no transposed
-// contraction, y_c(q) += alpha JxW_q (w.grad u_c)(q).  Team of n^2 threads per cell, column
-// ownership, padded smem layout of sipg_apply2.cuh; the faces need values only.
+// contraction, y_c(q) += alpha JxW_q (w.grad u_c)(q).  The transport field enters only through
+// quadrature-point data derived once per field (conv_pointdata_kernel), used by the standalone
+// apply below and by the fused viscous + convective apply (sipg_apply2.cuh, CONV).
 #pragma once
 #include "common.cuh"
 #include "sipg_apply2.cuh"
 
 namespace dgvv {
-
-template <int n>
-struct ConvCfg {
-  using L = Lay<n>;
-  static constexpr int VOL = 3 * L::CST;
-  static constexpr int CS = 3 * VOL;       // u | w | Y (x/y face accumulator)
-};
-
-template <int n, int GEO, int CPB>
-__global__ void __launch_bounds__(CPB * n * n) convective_apply_kernel(const ConvArgs A) {
-  using L = Lay<n>;
-  using Cf = ConvCfg<n>;
-  constexpr int n2 = L::n2, n3 = L::n3, RS = L::RS, PS = L::PS, CST = L::CST, VOL = Cf::VOL;
-  extern __shared__ __align__(16) double csmem[];
-  __shared__ __align__(16) double sD[n * RS];
-  __shared__ int sid[CPB];
-  const Tab1D& T = c_tab[n];
-  const int lc = threadIdx.x / n2;
-  const int p = threadIdx.x - lc * n2;
-  const int a = p % n, b = p / n;
-  const int slot_raw = blockIdx.x * CPB + lc;
-  const bool active = slot_raw < A.n_proc;
-  const int cell = A.cell_base + (active ? slot_raw : A.n_proc - 1);
-  for (int i = threadIdx.x; i < n * RS; i += blockDim.x) {
-    const int r = i / RS, k = i - r * RS;
-    sD[i] = k < n ? T.D[r * DGVV_NMAX + k] : 0.0;
-  }
-  if (p == 0) sid[lc] = active ? cell : -1;
-  double* su = csmem + lc * Cf::CS;
-  double* sw = su + VOL;
-  double* Y = sw + VOL;
-  double ucol[3][n], wcol[3][n], y[3][n];
-#pragma unroll
-  for (int c = 0; c < 3; ++c)
-#pragma unroll
-    for (int z = 0; z < n; ++z) {
-      const double v = __ldg(A.src + (size_t)cell * 3 * n3 + c * n3 + z * n2 + p);
-      const double ww = __ldg(A.w + (size_t)cell * 3 * n3 + c * n3 + z * n2 + p);
-      ucol[c][z] = v;
-      wcol[c][z] = ww;
-      su[c * CST + z * PS + b * RS + a] = v;
-      sw[c * CST + z * PS + b * RS + a] = ww;
-      y[c][z] = 0.0;
-    }
-  double ih[3] = {0, 0, 0}, vol = 0.0;
-  if constexpr (GEO == 0) {
-    const double* cg = A.cart + (size_t)cell * CART_STRIDE;
-    ih[0] = cg[0]; ih[1] = cg[1]; ih[2] = cg[2]; vol = cg[4];
-  }
-  int nbf[6];
-#pragma unroll
-  for (int f = 0; f < 6; ++f) nbf[f] = __ldg(A.nbr + cell * 6 + f);
-  __syncthreads();
-
-  // ------------------------------------------------------------ volume: JxW (w.grad) u
-  {
-    double Da[n], Db[n];
-    ld_row<n>(sD + a * RS, Da);
-    ld_row<n>(sD + b * RS, Db);
-#pragma unroll
-    for (int z = 0; z < n; ++z) {
-      const int q = z * n2 + p;
-      double jxw, Ji[9];
-      if constexpr (GEO == 0) {
-        jxw = T.w[a] * T.w[b] * T.w[z] * vol;
-      } else {
-        jxw = A.jxw[(size_t)cell * n3 + q];
-#pragma unroll
-        for (int r = 0; r < 9; ++r) Ji[r] = __ldg(A.vJi + (size_t)cell * 9 * n3 + r * n3 + q);
-      }
-      // transport direction in reference coordinates: wr_k = sum_j Ji[k][j] w_j
-      double wr[3];
-      if constexpr (GEO == 0) {
-#pragma unroll
-        for (int k = 0; k < 3; ++k) wr[k] = ih[k] * wcol[k][z];
-      } else {
-#pragma unroll
-        for (int k = 0; k < 3; ++k) wr[k] = Ji[3 * k] * wcol[0][z] + Ji[3 * k + 1] * wcol[1][z] + Ji[3 * k + 2] * wcol[2][z];
-      }
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const double gx = rowdot<n>(su + c * CST + z * PS + b * RS, Da);
-        double gy = 0.0, gz = 0.0;
-#pragma unroll
-        for (int k = 0; k < n; ++k) {
-          gy = fma(Db[k], su[c * CST + z * PS + k * RS + a], gy);
-          gz = fma(T.D[z * DGVV_NMAX + k], ucol[c][k], gz);
-        }
-        y[c][z] = A.alpha * jxw * (gx * wr[0] + gy * wr[1] + gz * wr[2]);
-      }
-    }
-  }
-
-  // ------------------------------------------------------------ faces: upwind flux
-#pragma unroll
-  for (int dd = 0; dd < 3; ++dd) {
-    const int d = (dd == 0) ? 2 : dd - 1;
-    double val[2][3];
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      const int f = 2 * d + s;
-      const int nbv = nbf[f];
-#pragma unroll
-      for (int c = 0; c < 3; ++c) val[s][c] = 0.0;
-      if (nbv >= 0) {
-        const double* lS = s ? T.l1 : T.l0;
-        const double* lO = s ? T.l0 : T.l1;
-        const double sgn = s ? 1.0 : -1.0;
-        double nrm[3] = {0.0, 0.0, 0.0}, dA;
-        if constexpr (GEO == 0) {
-          nrm[d] = sgn;
-          dA = T.w[a] * T.w[b] * vol * ih[d];
-        } else {
-          const double* fm = A.fJi + ((size_t)cell * 6 + f) * 9 * n2 + p;
-          const double v0 = __ldg(fm + (3 * d) * n2), v1 = __ldg(fm + (3 * d + 1) * n2), v2 = __ldg(fm + (3 * d + 2) * n2);
-          const double il = sgn * rsqrt(v0 * v0 + v1 * v1 + v2 * v2);
-          nrm[0] = v0 * il; nrm[1] = v1 * il; nrm[2] = v2 * il;
-          dA = A.fdA[((size_t)cell * 6 + f) * n2 + p];
-        }
-        const int sl = lc + (nbv - cell);
-        const bool in_cta = sl >= 0 && sl < CPB && sid[sl] == nbv;
-        const bool own = nbv < A.n_owned;
-        const double* pu = own ? A.src + (size_t)nbv * 3 * n3 : A.ghost + (size_t)(nbv - A.n_owned) * 3 * n3;
-        const double* pw = own ? A.w + (size_t)nbv * 3 * n3 : A.wghost + (size_t)(nbv - A.n_owned) * 3 * n3;
-        const double* nsu = csmem + (in_cta ? sl : 0) * Cf::CS;
-        auto own_line = [&](const double* base, const double (&col)[3][n], int c, double (&x)[n]) {
-#pragma unroll
-          for (int i = 0; i < n; ++i)
-            x[i] = (d == 2) ? col[c][i] : (d == 0 ? base[c * CST + b * PS + a * RS + i] : base[c * CST + b * PS + i * RS + a]);
-        };
-        auto nb_line = [&](int fld, int c, double (&x)[n]) {
-          if (in_cta) {
-            const double* base = nsu + fld * VOL;
-#pragma unroll
-            for (int i = 0; i < n; ++i)
-              x[i] = (d == 2) ? base[c * CST + i * PS + b * RS + a]
-                              : (d == 0 ? base[c * CST + b * PS + a * RS + i] : base[c * CST + b * PS + i * RS + a]);
-          } else {
-            const double* g = fld ? pw : pu;
-#pragma unroll
-            for (int i = 0; i < n; ++i)
-              x[i] = (d == 2) ? __ldg(g + c * n3 + i * n2 + p)
-                              : (d == 0 ? __ldg(g + c * n3 + b * n2 + a * n + i) : __ldg(g + c * n3 + b * n2 + i * n + a));
-          }
-        };
-        double wn = 0.0;                       // {{w}}.n
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          if (GEO == 0 && c != d) continue;
-          double xm[n], xp[n];
-          own_line(sw, wcol, c, xm);
-          nb_line(1, c, xp);
-          double wm = 0.0, wp = 0.0;
-#pragma unroll
-          for (int i = 0; i < n; ++i) { wm = fma(lS[i], xm[i], wm); wp = fma(lO[i], xp[i], wp); }
-          wn += 0.5 * (wm + wp) * nrm[c];
-        }
-        if (wn < 0.0) {                        // inflow face of this cell: upwind from the neighbour
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            double xm[n], xp[n];
-            own_line(su, ucol, c, xm);
-            nb_line(0, c, xp);
-            double um = 0.0, up = 0.0;
-#pragma unroll
-            for (int i = 0; i < n; ++i) { um = fma(lS[i], xm[i], um); up = fma(lO[i], xp[i], up); }
-            val[s][c] = A.alpha * dA * wn * (up - um);
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      double add[n];
-#pragma unroll
-      for (int i = 0; i < n; ++i) add[i] = T.l0[i] * val[0][c] + T.l1[i] * val[1][c];
-      if (d == 2) {
-#pragma unroll
-        for (int i = 0; i < n; ++i) y[c][i] += add[i];
-      } else {
-        st_row<n>(Y + c * CST + b * PS + a * RS, add);
-      }
-    }
-    if (d != 2) {
-      __syncthreads();
-#pragma unroll
-      for (int c = 0; c < 3; ++c)
-#pragma unroll
-        for (int z = 0; z < n; ++z) y[c][z] += (d == 0) ? Y[c * CST + z * PS + b * RS + a] : Y[c * CST + z * PS + a * RS + b];
-      __syncthreads();
-    }
-  }
-  if (active) {
-    const size_t off = (size_t)cell * 3 * n3;
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-#pragma unroll
-      for (int z = 0; z < n; ++z) {
-        double* o = A.dst + off + c * n3 + z * n2 + p;
-        *o = A.accumulate ? *o + y[c][z] : y[c][z];
-      }
-  }
-}
 
 // Quadrature-point data of the convective term for the fused viscous + convective apply
 // (sipg_apply2.cuh, CONV), derived once per transport field (the analogue of the stored viscosity):
@@ -287,7 +85,8 @@ __global__ void conv_pointdata_kernel(const ConvArgs A, double* wref, double* wf
 
 // dst (+)= alpha C(w) src from the stored point data (wref, wface of conv_pointdata_kernel): no
 // geometry and no transport-field traces in the apply; the neighbour trace is read only where
-// this side is an inflow side (wface != 0).  Same team / layout as convective_apply_kernel.
+// this side is an inflow side (wface != 0).  Team of n^2 threads per cell, column ownership and
+// the padded smem layout of sipg_apply2.cuh.
 template <int n, int CPB>
 __global__ void __launch_bounds__(CPB * n * n) convective_pd_kernel(const ConvArgs A, const double* wref,
                                                                      const double* wface) {

@@ -45,23 +45,7 @@ cudaError_t launch_penalty(int n, int geo, const PenaltyArgs& a, bool diag, cuda
   }
 }
 
-// f4: upwind convective term, accumulated into dst
-template <int n, int GEO>
-static cudaError_t conv_run(const ConvArgs& a, cudaStream_t s) {
-  constexpr int CPB = cpb_pen<n>();
-  const size_t smem = (size_t)CPB * ConvCfg<n>::CS * sizeof(double);
-  auto k = convective_apply_kernel<n, GEO, CPB>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  if (a.n_proc <= 0) return cudaSuccess;
-  k<<<(a.n_proc + CPB - 1) / CPB, CPB * n * n, smem, s>>>(a);
-  return cudaGetLastError();
-}
-
+// f4: upwind convective term
 template <int n, int GEO>
 static cudaError_t conv_pd_run(const ConvArgs& a, double* wref, double* wface, cudaStream_t s) {
   const long tot = (long)a.n_owned * (n * n * n + 6 * n * n);
@@ -105,17 +89,6 @@ cudaError_t launch_convective_pd(int n, const ConvArgs& a, const double* wref, c
     case 4: return conv_pd_apply<4>(a, wref, wface, s);
     case 5: return conv_pd_apply<5>(a, wref, wface, s);
     case 6: return conv_pd_apply<6>(a, wref, wface, s);
-    default: return cudaErrorNotSupported;
-  }
-}
-
-cudaError_t launch_convective(int n, int geo, const ConvArgs& a, cudaStream_t s) {
-  switch (n) {
-    case 2: return geo ? conv_run<2, 1>(a, s) : conv_run<2, 0>(a, s);
-    case 3: return geo ? conv_run<3, 1>(a, s) : conv_run<3, 0>(a, s);
-    case 4: return geo ? conv_run<4, 1>(a, s) : conv_run<4, 0>(a, s);
-    case 5: return geo ? conv_run<5, 1>(a, s) : conv_run<5, 0>(a, s);
-    case 6: return geo ? conv_run<6, 1>(a, s) : conv_run<6, 0>(a, s);
     default: return cudaErrorNotSupported;
   }
 }

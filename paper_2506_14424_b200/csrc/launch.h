@@ -25,8 +25,6 @@ cudaError_t launch_apply_oseen(int n, int geo, const ApplyArgs& a, cudaStream_t 
 cudaError_t launch_conv_pointdata(int n, int geo, const ConvArgs& a, double* wref, double* wface, cudaStream_t s);
 // f4: dst (+)= alpha C(w) src from the stored point data
 cudaError_t launch_convective_pd(int n, const ConvArgs& a, const double* wref, const double* wface, cudaStream_t s);
-// f4: dst (+)= alpha C(w) src (upwind convective term)
-cudaError_t launch_convective(int n, int geo, const ConvArgs& a, cudaStream_t s);
 // f3: h-transfer between nested refinements (octant = ox + 2 oy + 4 oz; child[p * 8 + octant])
 cudaError_t launch_hprolongate(int n, int nc, const double* coarse, double* fine, const int* parent,
                                const signed char* octant, double beta, int n_fine, cudaStream_t s);
