@@ -174,6 +174,9 @@ struct dgvv_ctx {
   double* d_wtr = nullptr;
   double* wtr_ghost = nullptr;
   bool has_wtr = false;
+  double* d_npc = nullptr;                   // Newton point data of the linearisation point (lazy)
+  double* d_npf = nullptr;
+  bool npd_stale = true;
   double* d_wref = nullptr;                  // convective point data for the fused apply (lazy)
   double* d_wface = nullptr;
   bool wq_stale = true;
@@ -893,6 +896,7 @@ dgvv_status dgvv_update_viscosity(dgvv_ctx* c, const double* u_lin, dgvv_stream 
   }
   c->ulin = u_lin;
   c->nu_ready = true;
+  c->npd_stale = true;
   ++c->coef_epoch;
   return DGVV_OK;
 }
@@ -1030,6 +1034,18 @@ dgvv_status dgvv_apply_linearized_viscous(dgvv_ctx* c, const double* src, double
   a.ulin = c->ulin;
   a.ulin_ghost = c->L[0].ulin_ghost;
   for (int i = 0; i < 4; ++i) a.law[i] = c->visc.p[i];
+  if (newton_uses_pointdata(c->geo)) {
+    if (c->npd_stale) {                       // once per linearisation (after the ghosts of u_lin arrived)
+      const size_t n = c->L[0].n, n3 = n * n * n, n2 = n * n;
+      if (!c->d_npc) TRY(dalloc(c, &c->d_npc, (size_t)c->n_owned * 7 * n3));
+      if (!c->d_npf) TRY(dalloc(c, &c->d_npf, (size_t)c->n_total * 60 * n2));
+      cudaError_t e = launch_newton_pointdata((int)n, a, c->n_total, c->d_npc, c->d_npf, s);
+      if (e != cudaSuccess) return dgvv_fail(DGVV_ECUDA, "Newton point data: %s", cudaGetErrorString(e));
+      c->npd_stale = false;
+    }
+    a.npc = c->d_npc;
+    a.npf = c->d_npf;
+  }
   return run_apply(c, DGVV_OP_VISCOUS, 0, a, s, 1);
 }
 

@@ -74,6 +74,9 @@ struct ApplyArgsT {  // R = double (operators) or float (FP32 multigrid levels, 
   // f4 fused convective term (CONV instantiation): + alpha_c C(w) src
   const R* wref;       // JxW J^-1 w at cell points [n_owned][3][n^3] (convective_apply.cuh)
   const R* wface;      // min({{w}}.n, 0) dA at own face points [n_owned][6][n^2]
+  // K2 v3 (newton_apply3.cuh): point data of the linearisation point (Cartesian)
+  const R* npc;        // [n_owned][7][n^3]  S0 (6), g at cell points
+  const R* npf;        // [n_total][6][10][n^2]  S0 (6), g, u0 trace (3) at own face points
   double alpha_c;
 };
 using ApplyArgs = ApplyArgsT<double>;

@@ -2,7 +2,10 @@
 #include "tu_tables.cuh"
 #include "newton_apply.cuh"
 #include "newton_apply2.cuh"
+#include "newton_apply3.cuh"
 #include "launch.h"
+
+#include <algorithm>
 
 namespace dgvv {
 
@@ -14,17 +17,20 @@ template <int n> constexpr int cpb_newton() { return n == 2 ? 16 : n == 3 ? 8 : 
 #define NCPB5 1
 #endif
 #ifndef NMINB5
-#define NMINB5 8
+#define NMINB5 10
 #endif
 // Cartesian cells: newton_apply2_kernel (no power evaluations, merged stresses)
 template <int n> constexpr int cpb_newton2() { return n == 2 ? 16 : n == 3 ? 6 : n == 4 ? 2 : n == 5 ? NCPB5 : 1; }
 template <int n> constexpr int minb_newton2() { return n == 5 ? NMINB5 : n == 4 ? 4 : 2; }
 
+#ifndef DGVV_NEWTON_PD
+#define DGVV_NEWTON_PD 1   // Cartesian: v3 kernel from stored point data of u0 (newton_apply3.cuh)
+#endif
 template <int n>
 static cudaError_t run2(const ApplyArgs& a, cudaStream_t s) {
   constexpr int CPB = cpb_newton2<n>();
-  const size_t smem = (size_t)CPB * Newton2Cfg<n>::CS * sizeof(double);
-  auto k = newton_apply2_kernel<n, CPB, minb_newton2<n>()>;
+  const size_t smem = (size_t)CPB * (DGVV_NEWTON_PD ? Newton3Cfg<n>::CS : Newton2Cfg<n>::CS) * sizeof(double);
+  auto k = DGVV_NEWTON_PD ? newton_apply3_kernel<n, CPB, minb_newton2<n>()> : newton_apply2_kernel<n, CPB, minb_newton2<n>()>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -51,6 +57,28 @@ static cudaError_t run(const ApplyArgs& a, cudaStream_t s) {
   if (a.n_proc <= 0) return cudaSuccess;
   k<<<(a.n_proc + CPB - 1) / CPB, CPB * n * n, smem, s>>>(a);
   return cudaGetLastError();
+}
+
+bool newton_uses_pointdata(int geo) { return geo == 0 && DGVV_NEWTON_PD; }
+
+template <int n>
+static cudaError_t npd_run(const ApplyArgs& a, int n_total, double* pc, double* pf, cudaStream_t s) {
+  const long tot = (long)a.n_owned * n * n * n + (long)n_total * 6 * n * n;
+  if (tot <= 0) return cudaSuccess;
+  const int blocks = (int)std::min<long>(148L * 16, (tot + 255) / 256);
+  newton_pointdata_kernel<n><<<blocks, 256, 0, s>>>(a, n_total, pc, pf);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_newton_pointdata(int n, const ApplyArgs& a, int n_total, double* pc, double* pf, cudaStream_t s) {
+  switch (n) {
+    case 2: return npd_run<2>(a, n_total, pc, pf, s);
+    case 3: return npd_run<3>(a, n_total, pc, pf, s);
+    case 4: return npd_run<4>(a, n_total, pc, pf, s);
+    case 5: return npd_run<5>(a, n_total, pc, pf, s);
+    case 6: return npd_run<6>(a, n_total, pc, pf, s);
+    default: return cudaErrorNotSupported;
+  }
 }
 
 cudaError_t launch_newton(int n, int geo, const ApplyArgs& a, cudaStream_t s) {

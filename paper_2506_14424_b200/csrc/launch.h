@@ -52,6 +52,9 @@ cudaError_t launch_cg_probe_get(const double* y, double* diag, const int* color,
                                 cudaStream_t s);
 cudaError_t launch_cheb_vec(const double* r, const double* dinv, double c_rho, double c_r, double* d, double* x,
                             long n, cudaStream_t s);
+// K2 v3: point data of the linearisation point (Cartesian), derived once per update_viscosity
+bool newton_uses_pointdata(int geo);
+cudaError_t launch_newton_pointdata(int n, const ApplyArgs& a, int n_total, double* pc, double* pf, cudaStream_t s);
 // K2: Newton-linearised viscous apply
 cudaError_t launch_newton(int n, int geo, const ApplyArgs& a, cudaStream_t s);
 // K3: Carreau viscosity at all points
