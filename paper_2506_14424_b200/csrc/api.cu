@@ -123,6 +123,7 @@ struct Level {
   double* wc_cell = nullptr;  // general geometry: c*JxW, c*dA
   double* wc_face = nullptr;
   double* dinv[2] = {nullptr, nullptr};
+  bool dinv_ok[2] = {false, false};          // buffer kept across coefficient changes; recomputed when false
   double* ulin = nullptr;     // u_lin interpolated to this level (levels >= 1), owned
   double* ghost[2] = {nullptr, nullptr};   // ghost src buffers (NC = 3 / 1)
   double* ulin_ghost = nullptr;
@@ -169,6 +170,7 @@ struct dgvv_ctx {
   double* d_tau_div = nullptr;
   double* d_tau_cont = nullptr;
   double* dinv_pen = nullptr;
+  bool dinv_pen_ok = false;
   bool has_pen = false;
   // f4 convective term: transport field w (level 0, owned + ghosts), GMRES work
   double* d_wtr = nullptr;
@@ -410,9 +412,9 @@ dgvv_status run_apply(dgvv_ctx* c, int op, int l, ApplyArgs a, cudaStream_t s, i
 dgvv_status ensure_dinv(dgvv_ctx* c, int op, int l, cudaStream_t s) {
   Level& L = c->L[l];
   const int oi = op == DGVV_OP_VISCOUS ? 0 : 1;
-  if (L.dinv[oi]) return DGVV_OK;
+  if (L.dinv[oi] && L.dinv_ok[oi]) return DGVV_OK;
   const int nc = op == DGVV_OP_VISCOUS ? 3 : 1;
-  TRY(dalloc(c, &L.dinv[oi], (size_t)nc * level_dofs(c, l)));
+  if (!L.dinv[oi]) TRY(dalloc(c, &L.dinv[oi], (size_t)nc * level_dofs(c, l)));
   DiagArgs d;
   d.nbr = c->d_nbr;
   d.n_owned = c->n_owned;
@@ -434,6 +436,7 @@ dgvv_status ensure_dinv(dgvv_ctx* c, int op, int l, cudaStream_t s) {
   const int form = op == DGVV_OP_VISCOUS ? c->form : DGVV_FORM_LAPLACE;
   cudaError_t e = launch_diag(nc, L.n, form, c->geo, d, s);
   if (e != cudaSuccess) return dgvv_fail(DGVV_ECUDA, "diag kernel: %s", cudaGetErrorString(e));
+  L.dinv_ok[oi] = true;
   return DGVV_OK;
 }
 
@@ -887,12 +890,7 @@ dgvv_status dgvv_update_viscosity(dgvv_ctx* c, const double* u_lin, dgvv_stream 
     TRY(check_positive(c, L.nu_cell, (long)c->n_owned * n3, s, "Carreau viscosity (cells)"));
     TRY(check_positive(c, L.nu_face, (long)c->n_total * 6 * n * n, s, "Carreau viscosity (faces)"));
     TRY(premultiply(c, (int)l, L.nu_cell, L.nu_face, L.wv_cell, L.wv_face, s));
-    for (int o = 0; o < 2; ++o)
-      if (L.dinv[o] && o == 0) { /* diagonal depends on nu: recompute lazily */
-        cudaFree(L.dinv[0]);
-        c->allocs.erase(std::remove(c->allocs.begin(), c->allocs.end(), (void*)L.dinv[0]), c->allocs.end());
-        L.dinv[0] = nullptr;
-      }
+    L.dinv_ok[0] = false;                    // the diagonal depends on nu: recomputed lazily (same buffer)
   }
   c->ulin = u_lin;
   c->nu_ready = true;
@@ -1058,12 +1056,7 @@ dgvv_status dgvv_set_mass(dgvv_ctx* c, int32_t op, double mass) {
   if (c->mass[op] == mass) return DGVV_OK;
   c->mass[op] = mass;
   ++c->coef_epoch;
-  for (auto& L : c->L)                 // the diagonal changes: recompute lazily
-    if (L.dinv[op]) {
-      cudaFree(L.dinv[op]);
-      c->allocs.erase(std::remove(c->allocs.begin(), c->allocs.end(), (void*)L.dinv[op]), c->allocs.end());
-      L.dinv[op] = nullptr;
-    }
+  for (auto& L : c->L) L.dinv_ok[op] = false;   // the diagonal changes: recomputed lazily (same buffer)
   return DGVV_OK;
 }
 
@@ -1488,12 +1481,13 @@ static dgvv_status apply_penalty_impl(dgvv_ctx* c, const double* src, double* ds
 }
 
 static dgvv_status ensure_dinv_pen(dgvv_ctx* c, cudaStream_t s) {
-  if (c->dinv_pen) return DGVV_OK;
-  TRY(dalloc(c, &c->dinv_pen, (size_t)3 * level_dofs(c, 0)));
+  if (c->dinv_pen && c->dinv_pen_ok) return DGVV_OK;
+  if (!c->dinv_pen) TRY(dalloc(c, &c->dinv_pen, (size_t)3 * level_dofs(c, 0)));
   PenaltyArgs a = penalty_args(c);
   a.dst = c->dinv_pen;
   cudaError_t e = launch_penalty(c->L[0].n, c->geo, a, true, s);
   if (e != cudaSuccess) return dgvv_fail(DGVV_ECUDA, "penalty diagonal: %s", cudaGetErrorString(e));
+  c->dinv_pen_ok = true;
   return DGVV_OK;
 }
 
@@ -1512,11 +1506,7 @@ dgvv_status dgvv_set_penalty_parameters(dgvv_ctx* c, const double* tau_div, cons
   if (!c->d_tau_cont) TRY(dalloc(c, &c->d_tau_cont, (size_t)nt));
   DGVV_CUDA_TRY(cudaMemcpy(c->d_tau_div, td.data(), nt * sizeof(double), cudaMemcpyHostToDevice));
   DGVV_CUDA_TRY(cudaMemcpy(c->d_tau_cont, tc.data(), nt * sizeof(double), cudaMemcpyHostToDevice));
-  if (c->dinv_pen) {
-    cudaFree(c->dinv_pen);
-    c->allocs.erase(std::remove(c->allocs.begin(), c->allocs.end(), (void*)c->dinv_pen), c->allocs.end());
-    c->dinv_pen = nullptr;
-  }
+  c->dinv_pen_ok = false;
   c->has_pen = true;
   return DGVV_OK;
 }

@@ -125,14 +125,17 @@ def run_c4(reps):
     ms = timeit(lambda: ctx.apply_poisson(b, x), 20, reps)
     report("C4", "apply_poisson_k5", ms, N, pb, N * (12 * n + 96 + 10 + 120 / n))
     dinv = torch.empty_like(b)
-    torch.cuda.synchronize()                           # first call: the K5 kernel (D^-1 is then cached)
+    ctx.inverse_diagonal(A.OP_POISSON, dinv)           # first call: module load + K5 kernel
+    ctx.set_mass(A.OP_POISSON, 1e-300)                 # two coefficient changes invalidate the cached
+    ctx.set_mass(A.OP_POISSON, 0.0)                    # D^-1: the next call runs K5 again (same operator)
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     ctx.inverse_diagonal(A.OP_POISSON, dinv)
     e1.record()
     e1.synchronize()
     report("C4", "inverse_diagonal_k5_kernel", e0.elapsed_time(e1), N, 8 * cells * (2 * n ** 3 + 12 * n * n) + 24 * cells,
-           None, "first call (K5 kernel + allocation of the cached D^-1), single shot")
+           None, "K5 kernel recomputing the cached D^-1 in place, single shot")
     ms = timeit(lambda: ctx.inverse_diagonal(A.OP_POISSON, dinv), 10, reps)
     report("C4", "inverse_diagonal_k5_cached", ms, N, 8 * 2 * N, None, "later calls copy the cached D^-1")
     lam = []
