@@ -185,6 +185,8 @@ struct dgvv_ctx {
   double* gm_work = nullptr;                 // r, w, V[0..m], Z[0..m-1]
   int gm_restart = 0;
   double* gm_H = nullptr;                    // device Hessenberg column
+  double* lz_buf = nullptr;                  // Lanczos work vectors (dgvv_estimate_lambda_max)
+  size_t lz_len = 0;
   // f3: h-levels (a coarser context below the coarsest p-level) and the direct coarse solver
   dgvv_ctx* coarse = nullptr;
   int* d_parent = nullptr;                   // [n_owned] coarse cell of each fine cell
@@ -2253,9 +2255,16 @@ dgvv_status dgvv_estimate_lambda_max(dgvv_ctx* c, int32_t op, int32_t level, int
     a.src = src; a.dst = dst;
     return run_apply(c, op, level, a, s);
   };
-  double* buf = nullptr;
-  DGVV_CUDA_TRY(cudaMalloc(&buf, 5 * N * sizeof(double)));
-  struct Free { double* p; ~Free() { cudaFree(p); } } fr{buf};
+  if (c->lz_len < (size_t)(5 * N)) {           // work vectors kept by the context (grow-only)
+    if (c->lz_buf) {
+      cudaFree(c->lz_buf);
+      c->allocs.erase(std::remove(c->allocs.begin(), c->allocs.end(), (void*)c->lz_buf), c->allocs.end());
+      c->lz_buf = nullptr;
+    }
+    TRY(dalloc(c, &c->lz_buf, (size_t)(5 * N)));
+    c->lz_len = (size_t)(5 * N);
+  }
+  double* buf = c->lz_buf;
   double *sq = buf, *q = buf + N, *qp = buf + 2 * N, *w = buf + 3 * N, *t = buf + 4 * N;
   double* d_alpha = c->d_scal;
   double* d_beta = c->d_scal + 1;
