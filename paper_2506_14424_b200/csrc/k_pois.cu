@@ -24,13 +24,30 @@ cudaError_t upload_tables_pois(const Tab1D* tabs) { return tu_upload_tables(tabs
 #endif
 template <int n> constexpr int cpb_pois() { return n == 2 ? 32 : n == 3 ? PCPB3 : n == 4 ? PCPB4 : n == 5 ? 5 : n == 6 ? PCPB6 : 3; }
 template <int n> constexpr int minb_pois() { return n <= 3 ? 3 : n == 6 ? PMINB6 : 4; }
+// FP32 multigrid levels (half the registers and shared memory per cell)
+#ifndef PMINB6F
+#define PMINB6F 4
+#endif
+#ifndef PMINB4F
+#define PMINB4F 4
+#endif
+#ifndef PMINB3F
+#define PMINB3F 3
+#endif
+#ifndef PMINB2F
+#define PMINB2F 3
+#endif
+template <typename R, int n> constexpr int minb_pois_t() {
+  if constexpr (sizeof(R) == 4) return n == 2 ? PMINB2F : n == 3 ? PMINB3F : n == 4 ? PMINB4F : n == 6 ? PMINB6F : minb_pois<n>();
+  else return minb_pois<n>();
+}
 
 template <typename R, int n, int GEO>
 static cudaError_t run(const ApplyArgsT<R>& a, cudaStream_t s) {
   constexpr int CPB = cpb_pois<n>();
   const size_t smem = (size_t)CPB * Apply2Cfg<n, 1, 1, GEO>::CS * sizeof(R);
-  auto k0 = sipg_apply2_kernel<R, n, 1, 1, GEO, CPB, minb_pois<n>(), false>;
-  auto k1 = sipg_apply2_kernel<R, n, 1, 1, GEO, CPB, minb_pois<n>(), true>;
+  auto k0 = sipg_apply2_kernel<R, n, 1, 1, GEO, CPB, minb_pois_t<R, n>(), false>;
+  auto k1 = sipg_apply2_kernel<R, n, 1, 1, GEO, CPB, minb_pois_t<R, n>(), true>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -34,6 +34,25 @@ template <int n, int GEO> constexpr int cpb_visc() {
 template <int n, int GEO> constexpr int minb_visc() {
   return n == 2 ? 2 : n == 3 ? 3 : n == 4 ? (GEO ? MINB4G : MINB4) : n == 5 ? MINB5 : 2;
 }
+// FP32 multigrid levels (half the registers and shared memory per cell)
+#ifndef MINB5F
+#define MINB5F 5
+#endif
+#ifndef MINB4F
+#define MINB4F 4
+#endif
+#ifndef MINB2F
+#define MINB2F 6
+#endif
+#ifndef MINB3F
+#define MINB3F 5
+#endif
+template <typename R, int n, int GEO> constexpr int minb_visc_t() {
+  if constexpr (sizeof(R) == 4 && GEO == 0)
+    return n == 2 ? MINB2F : n == 3 ? MINB3F : n == 4 ? MINB4F : n == 5 ? MINB5F : minb_visc<n, GEO>();
+  else
+    return minb_visc<n, GEO>();
+}
 
 template <typename R, int n, int FORM, int GEO>
 static cudaError_t run(const ApplyArgsT<R>& a, cudaStream_t s) {
@@ -41,8 +60,8 @@ static cudaError_t run(const ApplyArgsT<R>& a, cudaStream_t s) {
   constexpr int NC = 3;
   const size_t smem = (size_t)CPB * Apply2Cfg<n, NC, FORM, GEO>::CS * sizeof(R);
   // the Helmholtz mass term is a separate instantiation: the plain operator pays nothing for it
-  auto k0 = sipg_apply2_kernel<R, n, NC, FORM, GEO, CPB, minb_visc<n, GEO>(), false>;
-  auto k1 = sipg_apply2_kernel<R, n, NC, FORM, GEO, CPB, minb_visc<n, GEO>(), true>;
+  auto k0 = sipg_apply2_kernel<R, n, NC, FORM, GEO, CPB, minb_visc_t<R, n, GEO>(), false>;
+  auto k1 = sipg_apply2_kernel<R, n, NC, FORM, GEO, CPB, minb_visc_t<R, n, GEO>(), true>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

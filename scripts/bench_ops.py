@@ -351,6 +351,63 @@ def run_f3(reps):
             torch.cuda.empty_cache()
 
 
+def run_step(reps):
+    """One Picard-linearised viscous step of the paper's projection scheme on C3's mesh, end to end
+    on the GPU: update_viscosity(u_lin) (Carreau nu on every level), inverse diagonals and
+    lambda_max (15 Lanczos steps) of every level, then PCG to 1e-8 on gamma_0/dt M + A(nu) with the
+    FP32 cph V-cycle (p 4 -> 2 -> 1, h-levels 32^3 ... 4^3 at k = 1, direct solve on 4^3); the
+    h-levels carry the analytic C2 law (the Carreau u_lin lives on the fine mesh only).  Each phase
+    timed with CUDA events; the step = their sum."""
+    from inputs import cube_parent_map
+    m = cube(64)
+    degs = [4, 2, 1]
+    fine = Context(m, 4, visc_law=C3_LAW, degrees=degs)
+    fine.set_mass(A.OP_VISCOUS, 1.0e3)
+    ulin = dev(c3_linearization(m, 4))
+    N = 3 * fine.n_dofs(0)
+    keep, prev, Nc = [], fine, 64
+    while Nc > 4:
+        Nc //= 2
+        c = Context(cube(Nc), 1, visc_law=C2_LAW)
+        c.set_mass(A.OP_VISCOUS, 1.0e3)
+        parent, octant = cube_parent_map(2 * Nc)
+        prev.set_coarse_context(c, parent, octant)
+        keep.append(c)
+        prev = c
+    keep[-1].setup_coarse_solver(A.OP_VISCOUS)
+    lam_h = [1.2 * c.estimate_lambda_max(A.OP_VISCOUS, dev(uniform(2, 3 * c.n_dofs(0))), level=0, steps=15)
+             for c in keep[:-1]]
+    b = dev(uniform(0, N))
+    x = torch.zeros_like(b)
+    v0 = [dev(uniform(2, 3 * fine.n_dofs(l))) for l in range(len(degs))]
+
+    def step():
+        t = {}
+        def ev():
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            return e
+        e0 = ev()
+        fine.update_viscosity(ulin)
+        e1 = ev()
+        lams = [1.2 * fine.estimate_lambda_max(A.OP_VISCOUS, v0[l], level=l, steps=15) for l in range(len(degs))]
+        e2 = ev()
+        x.zero_()
+        it, rr = fine.cg_solve(A.OP_VISCOUS, b, x, rtol=1e-8, maxit=200, precond="vcycle_fp32",
+                               lam_hi_per_level=lams + lam_h + [1.0])
+        e3 = ev()
+        e3.synchronize()
+        t["update_viscosity"] = e0.elapsed_time(e1)
+        t["diagonals+lambda"] = e1.elapsed_time(e2)
+        t["pcg"] = e2.elapsed_time(e3)
+        return t, it, rr
+    step()
+    t, it, rr = step()
+    total = sum(t.values())
+    report("C3+step", "picard_viscous_step", total, N, None, None,
+           "; ".join(f"{k} {v:.1f} ms" for k, v in t.items()) + f"; PCG {it} its (relres {rr:.1e}), FP32 cph V-cycle")
+
+
 def run_c5(reps):
     m = bfs()
     ctx = Context(m, 3, visc_law=C5_LAW)
@@ -371,7 +428,7 @@ def main():
     a = ap.parse_args()
     torch.cuda.set_device(0)
     for c in a.configs.split(","):
-        {"2": run_c2, "3": run_c3, "4": run_c4, "5": run_c5, "f1": run_f1, "f2": run_f2, "f4": run_f4, "f3": run_f3}[c](a.reps)
+        {"2": run_c2, "3": run_c3, "4": run_c4, "5": run_c5, "f1": run_f1, "f2": run_f2, "f4": run_f4, "f3": run_f3, "step": run_step}[c](a.reps)
         torch.cuda.empty_cache()
 
 
