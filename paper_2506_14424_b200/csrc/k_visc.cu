@@ -31,8 +31,14 @@ cudaError_t upload_tables_visc(const Tab1D* tabs) { return tu_upload_tables(tabs
 template <int n, int GEO> constexpr int cpb_visc() {
   return n == 2 ? 32 : n == 3 ? 14 : n == 4 ? (GEO ? CPB4G : CPB4) : n == 5 ? CPB5 : 3;
 }
+#ifndef MINB2
+#define MINB2 4
+#endif
+#ifndef MINB3
+#define MINB3 4
+#endif
 template <int n, int GEO> constexpr int minb_visc() {
-  return n == 2 ? 2 : n == 3 ? 3 : n == 4 ? (GEO ? MINB4G : MINB4) : n == 5 ? MINB5 : 2;
+  return n == 2 ? MINB2 : n == 3 ? MINB3 : n == 4 ? (GEO ? MINB4G : MINB4) : n == 5 ? MINB5 : 2;
 }
 // FP32 multigrid levels (half the registers and shared memory per cell)
 #ifndef MINB5F
