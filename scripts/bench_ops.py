@@ -225,13 +225,17 @@ def run_f2(reps):
                f"{it} iterations to rtol 1e-10 (relres {rr:.2e}); {ms / max(it, 1):.3f} ms/iteration")
 
 
+F4_NU = {"kind": "const", "value": 1.0e-3}      # convection-dominated viscous step (high Re)
+
+
 def run_f4(reps):
     """f4: upwind convective term on the C2 mesh (32^3 deformed, k=3) and C3's mesh (64^3, k=4)
     with a random transport field w = rng(1); the Oseen-type viscous step mass M + A(nu) + C(w)
-    (mass = 1e3 ~ gamma_0/dt for a CFL-limited dt) and GMRES(30) with the FP64 / FP32 V-cycle of the
-    symmetric part to rtol 1e-8."""
+    (nu = 1e-3 so that convection matters, mass = 1e3 ~ gamma_0/dt for a CFL-limited dt) and
+    GMRES(30) with the FP64 / FP32 V-cycle of the symmetric part to rtol 1e-8 (p-levels only, then
+    the cph V-cycle; C3 also with a smooth transport field)."""
     for name, m, k, degs in (("C2", deformed_cube(32, 3), 3, [3, 2, 1]), ("C3", cube(64), 4, [4, 2, 1])):
-        ctx = Context(m, k, visc_law=C2_LAW, degrees=degs)
+        ctx = Context(m, k, visc_law=F4_NU, degrees=degs)
         N = 3 * ctx.n_dofs(0)
         src = dev(uniform(0, N))
         ctx.set_transport(dev(uniform(1, N)))
@@ -261,6 +265,34 @@ def run_f4(reps):
             ms = e0.elapsed_time(e1)
             report(name + "+f4", "gmres_" + pc, ms, N, None, None,
                    f"{it} iterations to rtol 1e-8 (relres {rr:.2e}); {ms / max(it, 1):.3f} ms/iteration")
+        # the cph V-cycle (h-levels down to 4^3 at k = 1, direct solve) of the symmetric part
+        from inputs import cube_parent_map
+        keep, prev, Nc = [], ctx, round(m.n_cells ** (1 / 3))
+        while Nc > 4:
+            Nc //= 2
+            cm = deformed_cube(Nc, 3) if general else cube(Nc)
+            c = Context(cm, 1, visc_law=F4_NU)
+            c.set_mass(0, 1.0e3)
+            parent, octant = cube_parent_map(2 * Nc)
+            prev.set_coarse_context(c, parent, octant)
+            keep.append(c)
+            prev = c
+        keep[-1].setup_coarse_solver(0)
+        lams_h = lams + [1.2 * c.estimate_lambda_max(0, dev(uniform(2, 3 * c.n_dofs(0))), level=0, steps=15)
+                         for c in keep[:-1]] + [1.0]
+        fields = [("random w", None)] + ([("smooth w (8-mode Fourier field)", c3_linearization(m, 4))] if not general else [])
+        for wname, wv in fields:
+            if wv is not None:
+                ctx.set_transport(dev(wv))
+            for pc in ("vcycle", "vcycle_fp32"):
+                x = torch.zeros_like(src)
+                ctx.gmres_solve(src, x, rtol=1e-8, restart=30, maxit=300, precond=pc, lam_hi_per_level=lams_h)
+                x.zero_()
+                ms, (it, rr) = _timed(lambda: ctx.gmres_solve(src, x, rtol=1e-8, restart=30, maxit=300, precond=pc,
+                                                              lam_hi_per_level=lams_h))
+                report(name + "+f4", "gmres_cph_" + pc + ("_smooth_w" if wv is not None else ""), ms, N, None, None,
+                       f"{wname}, cph V-cycle: {it} iterations (relres {rr:.2e}); {ms / max(it, 1):.3f} ms/iteration")
+        del keep
 
 
 def _timed(fn):
