@@ -254,3 +254,24 @@ def test_convective_multirank_bitwise():
         outs.append(y)
     torch.cuda.synchronize()
     assert torch.equal(torch.cat(outs), ref)
+
+
+def test_transport_point_data_follow_set_transport():
+    """The convective applies read point data derived from w: a new set_transport must be honoured
+    by both the standalone and the fused apply."""
+    m = cube(3)
+    k = 3
+    d = dg.Disc(m, k)
+    nu = dg.AnalyticNu(d, laws.C1_LAW)
+    n = m.n_cells * 3 * d.N
+    u = uniform(0, n)
+    ctx = Ctx(m, k, visc_law=laws.C1_LAW)
+    ctx.set_mass(0, 5.0)
+    y = torch.empty(n, dtype=torch.float64, device="cuda")
+    for seed in (1, 4):
+        w = uniform(seed, n)
+        ctx.set_transport(dev(w))
+        ctx.apply_oseen(dev(u), y, alpha_c=1.0)
+        assert rel(host(y), dg.helmholtz_apply(d, u, nu, 5.0) + dg.convective_apply(d, u, w)) < TOL
+        ctx.apply_convective(dev(u), y)
+        assert rel(host(y), dg.convective_apply(d, u, w)) < TOL

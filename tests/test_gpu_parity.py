@@ -396,3 +396,21 @@ def test_c5_full_size_sampled_carreau():
     cells = _sample_cells(m, 48)
     ref = dg.viscous_apply(d, u, dg.CarreauNu(d, ulin, laws.C5_CARREAU), cells=cells)
     assert rel(y[cells], ref) < TOL
+
+
+def test_newton_point_data_follow_the_linearisation():
+    """The Newton apply reads point data derived from u_lin (K2 v3): a second update_viscosity
+    with another u_lin must be honoured (no stale data)."""
+    m = cube(3)
+    k = 4
+    d = dg.Disc(m, k)
+    law = laws.C3_CARREAU
+    u0 = c3_linearization(m, k)
+    u1 = 0.5 * c3_linearization(m, k, seed=3)
+    w = uniform(0, len(u0))
+    ctx = Ctx(m, k, visc_law=law)
+    y = torch.empty(len(w), dtype=torch.float64, device="cuda")
+    for ul in (u0, u1):
+        ctx.update_viscosity(dev(ul))
+        ctx.apply_linearized_viscous(dev(w), y)
+        assert rel(host(y), dg.newton_apply(d, ul, w, law)) < TOL
