@@ -2152,14 +2152,22 @@ dgvv_status dgvv_set_coarse_context(dgvv_ctx* c, dgvv_ctx* cc, const int32_t* pa
   c->h_parent.assign(parent, parent + nf);
   c->h_octant.assign(octant, octant + nf);
   c->cg.transfer_to = nullptr;               // continuous-level transfers rebuilt on demand
-  if (c->coarse != cc) {
-    for (int o = 0; o < 2; ++o)
-      for (double** pp : {&c->hb[o], &c->hx[o]})
-        if (*pp) {
-          cudaFree(*pp);
-          c->allocs.erase(std::remove(c->allocs.begin(), c->allocs.end(), (void*)*pp), c->allocs.end());
-          *pp = nullptr;
-        }
+  if (c->coarse != cc) {                     // buffers sized by the previous coarse context
+    auto drop = [&](void** pp) {
+      if (*pp) {
+        cudaFree(*pp);
+        c->allocs.erase(std::remove(c->allocs.begin(), c->allocs.end(), *pp), c->allocs.end());
+        *pp = nullptr;
+      }
+    };
+    for (int o = 0; o < 2; ++o) {
+      drop((void**)&c->hb[o]);
+      drop((void**)&c->hx[o]);
+      drop((void**)&c->hbf[o]);
+      drop((void**)&c->hxf[o]);
+      drop((void**)&c->cg.hb[o]);
+      drop((void**)&c->cg.hx[o]);
+    }
   }
   c->coarse = cc;
   return DGVV_OK;
