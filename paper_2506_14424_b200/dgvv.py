@@ -56,7 +56,10 @@ class Context:
         L = A.lib()
         self._L = L
         n_owned = mesh.n_cells if n_owned is None else n_owned
+        self.n_ghost = int(n_ghost)
         self._nb = np.ascontiguousarray(mesh.neighbor, dtype=np.int64)
+        if self._nb.shape != (n_owned + n_ghost, 6):                  # the C ABI reads this many rows
+            raise ValueError(f"mesh.neighbor: expected ({n_owned + n_ghost}, 6), got {self._nb.shape}")
         self._nodes = np.ascontiguousarray(mesh.nodes, dtype=np.float64)
         m = A.DgvvMesh()
         m.n_cells = n_owned
@@ -208,6 +211,9 @@ class Context:
         penalty-step operator (dgvv_set_penalty_parameters)."""
         td = np.ascontiguousarray(tau_div, dtype=np.float64)
         tc = np.ascontiguousarray(tau_cont, dtype=np.float64)
+        nt = self.n_owned + self.n_ghost                             # the C ABI reads n_cells + n_ghost entries
+        if td.shape != (nt,) or tc.shape != (nt,):
+            raise ValueError(f"tau_div/tau_cont: expected {nt} entries each, got {td.shape} / {tc.shape}")
         A.check(self._L.dgvv_set_penalty_parameters(self.h, td.ctypes.data_as(C.POINTER(C.c_double)),
                                                     tc.ctypes.data_as(C.POINTER(C.c_double))))
 
@@ -305,6 +311,8 @@ class Context:
         dgvv_set_coarse_context); parent/octant per fine cell.  Keeps a reference to `coarse`."""
         par = np.ascontiguousarray(parent, dtype=np.int32)
         octa = np.ascontiguousarray(octant, dtype=np.int8)
+        if par.shape != (self.n_owned,) or octa.shape != (self.n_owned,):   # the C ABI reads n_cells entries
+            raise ValueError(f"parent/octant: expected {self.n_owned} entries each, got {par.shape} / {octa.shape}")
         A.check(self._L.dgvv_set_coarse_context(self.h, coarse.h, par.ctypes.data_as(C.POINTER(C.c_int32)),
                                                 octa.ctypes.data_as(C.POINTER(C.c_int8))))
         self._coarse = coarse
