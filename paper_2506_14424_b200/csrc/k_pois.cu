@@ -23,7 +23,20 @@ cudaError_t upload_tables_pois(const Tab1D* tabs) { return tu_upload_tables(tabs
 #define PCPB3 14
 #endif
 template <int n> constexpr int cpb_pois() { return n == 2 ? 32 : n == 3 ? PCPB3 : n == 4 ? PCPB4 : n == 5 ? 5 : n == 6 ? PCPB6 : 3; }
-template <int n> constexpr int minb_pois() { return n <= 3 ? 3 : n == 6 ? PMINB6 : 4; }
+#ifndef PCPB4F
+#define PCPB4F 16
+#endif
+template <typename R, int n> constexpr int cpb_pois_t() { return (sizeof(R) == 4 && n == 4) ? PCPB4F : cpb_pois<n>(); }
+#ifndef PMINB4
+#define PMINB4 6
+#endif
+#ifndef PMINB3
+#define PMINB3 5
+#endif
+#ifndef PMINB2
+#define PMINB2 6
+#endif
+template <int n> constexpr int minb_pois() { return n == 2 ? PMINB2 : n == 3 ? PMINB3 : n == 6 ? PMINB6 : n == 4 ? PMINB4 : 4; }
 // FP32 multigrid levels (half the registers and shared memory per cell)
 #ifndef PMINB6F
 #define PMINB6F 4
@@ -32,10 +45,10 @@ template <int n> constexpr int minb_pois() { return n <= 3 ? 3 : n == 6 ? PMINB6
 #define PMINB4F 4
 #endif
 #ifndef PMINB3F
-#define PMINB3F 3
+#define PMINB3F 4
 #endif
 #ifndef PMINB2F
-#define PMINB2F 3
+#define PMINB2F 4
 #endif
 template <typename R, int n> constexpr int minb_pois_t() {
   if constexpr (sizeof(R) == 4) return n == 2 ? PMINB2F : n == 3 ? PMINB3F : n == 4 ? PMINB4F : n == 6 ? PMINB6F : minb_pois<n>();
@@ -44,7 +57,7 @@ template <typename R, int n> constexpr int minb_pois_t() {
 
 template <typename R, int n, int GEO>
 static cudaError_t run(const ApplyArgsT<R>& a, cudaStream_t s) {
-  constexpr int CPB = cpb_pois<n>();
+  constexpr int CPB = cpb_pois_t<R, n>();
   const size_t smem = (size_t)CPB * Apply2Cfg<n, 1, 1, GEO>::CS * sizeof(R);
   auto k0 = sipg_apply2_kernel<R, n, 1, 1, GEO, CPB, minb_pois_t<R, n>(), false>;
   auto k1 = sipg_apply2_kernel<R, n, 1, 1, GEO, CPB, minb_pois_t<R, n>(), true>;
