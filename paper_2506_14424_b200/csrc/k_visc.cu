@@ -45,7 +45,7 @@ template <int n, int GEO> constexpr int minb_visc() {
 #define MINB5F 5
 #endif
 #ifndef MINB4F
-#define MINB4F 4
+#define MINB4F 6
 #endif
 #ifndef MINB2F
 #define MINB2F 6
@@ -53,6 +53,12 @@ template <int n, int GEO> constexpr int minb_visc() {
 #ifndef MINB3F
 #define MINB3F 5
 #endif
+#ifndef CPB4F
+#define CPB4F CPB4
+#endif
+template <typename R, int n, int GEO> constexpr int cpb_visc_t() {
+  return (sizeof(R) == 4 && GEO == 0 && n == 4) ? CPB4F : cpb_visc<n, GEO>();
+}
 template <typename R, int n, int GEO> constexpr int minb_visc_t() {
   if constexpr (sizeof(R) == 4 && GEO == 0)
     return n == 2 ? MINB2F : n == 3 ? MINB3F : n == 4 ? MINB4F : n == 5 ? MINB5F : minb_visc<n, GEO>();
@@ -62,7 +68,7 @@ template <typename R, int n, int GEO> constexpr int minb_visc_t() {
 
 template <typename R, int n, int FORM, int GEO>
 static cudaError_t run(const ApplyArgsT<R>& a, cudaStream_t s) {
-  constexpr int CPB = cpb_visc<n, GEO>();
+  constexpr int CPB = cpb_visc_t<R, n, GEO>();
   constexpr int NC = 3;
   const size_t smem = (size_t)CPB * Apply2Cfg<n, NC, FORM, GEO>::CS * sizeof(R);
   // the Helmholtz mass term is a separate instantiation: the plain operator pays nothing for it

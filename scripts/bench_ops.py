@@ -451,6 +451,17 @@ def run_c5(reps):
     dst = torch.empty_like(src)
     ms = timeit(lambda: ctx.apply_viscous(src, dst), 20, reps)
     report("C5", "apply_viscous", ms, N, visc_bytes(m.n_cells, 4, False), visc_flops(N, 4, False))
+    # the BFS viscous step's preconditioner: V-cycle 3 -> 2 -> 1 (FP64 and FP32 levels), mass 1e3
+    ctx2 = Context(m, 3, visc_law=C5_LAW, degrees=[3, 2, 1])
+    ctx2.set_mass(A.OP_VISCOUS, 1.0e3)
+    ctx2.update_viscosity(ulin)
+    lams = [1.2 * ctx2.estimate_lambda_max(A.OP_VISCOUS, dev(uniform(2, 3 * ctx2.n_dofs(l))), level=l, steps=15)
+            for l in range(3)]
+    x = torch.zeros_like(src)
+    ms = timeit(lambda: ctx2.vcycle(A.OP_VISCOUS, src, x, lams), 5, reps)
+    report("C5", "viscous_vcycle_3_2_1", ms, N, None, None, "Helmholtz (mass 1e3) Carreau V-cycle, FP64 levels")
+    ms = timeit(lambda: ctx2.vcycle_fp32(A.OP_VISCOUS, src, x, lams), 5, reps)
+    report("C5", "viscous_vcycle_fp32_3_2_1", ms, N, None, None, "FP32 levels")
 
 
 def main():
