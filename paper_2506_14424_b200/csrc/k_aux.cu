@@ -71,9 +71,12 @@ cudaError_t launch_diag(int nc, int n, int form, int geo, const DiagArgs& a, cud
 }
 
 // ---------------------------------------------------------------- K7
+#ifndef T3CPB
+#define T3CPB 2
+#endif
 template <typename R, int nin, int nout>
 static cudaError_t t3_run(int nc, const Mat8& M, const R* in, R* out, double beta, int ncells, cudaStream_t s) {
-  constexpr int CPB = 2;
+  constexpr int CPB = T3CPB;   // cells per CTA (64 threads each)
   constexpr int CS = nin * nin * nin + nin * nin * nout + nin * nout * nout;
   const size_t smem = (size_t)CPB * CS * sizeof(R);
   if (ncells <= 0) return cudaSuccess;

@@ -26,7 +26,12 @@ template <int n> constexpr int cpb_pois() { return n == 2 ? 32 : n == 3 ? PCPB3 
 #ifndef PCPB4F
 #define PCPB4F 16
 #endif
-template <typename R, int n> constexpr int cpb_pois_t() { return (sizeof(R) == 4 && n == 4) ? PCPB4F : cpb_pois<n>(); }
+#ifndef PCPB6F
+#define PCPB6F 8
+#endif
+template <typename R, int n> constexpr int cpb_pois_t() {
+  return sizeof(R) == 4 ? (n == 4 ? PCPB4F : n == 6 ? PCPB6F : cpb_pois<n>()) : cpb_pois<n>();
+}
 #ifndef PMINB4
 #define PMINB4 6
 #endif
