@@ -88,6 +88,7 @@ __global__ void conv_pointdata_kernel(const ConvArgs A, double* wref, double* wf
 // this side is an inflow side (wface != 0).  Team of n^2 threads per cell, column ownership and
 // the padded smem layout of sipg_apply2.cuh.
 template <int n, int CPB>
+// (no register cap: 6 / 8 resident CTAs measured slower, C3 mesh 1.26 -> 1.56 / 2.07 ms)
 __global__ void __launch_bounds__(CPB * n * n) convective_pd_kernel(const ConvArgs A, const double* wref,
                                                                      const double* wface) {
   using L = Lay<n>;

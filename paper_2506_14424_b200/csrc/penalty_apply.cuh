@@ -22,7 +22,11 @@ struct PenaltyCfg {
 };
 
 template <int n, int GEO, int CPB>
-__global__ void __launch_bounds__(CPB * n * n) penalty_apply_kernel(const PenaltyArgs A) {
+#ifndef DGVV_PEN_MINB
+#define DGVV_PEN_MINB 5   // min resident CTAs per SM (register cap), chosen by measurement:
+                          // C2 0.206 -> 0.194 ms, C3 mesh 1.70 -> 1.54 ms (6: 0.242 / 1.65)
+#endif
+__global__ void __launch_bounds__(CPB * n * n, DGVV_PEN_MINB) penalty_apply_kernel(const PenaltyArgs A) {
   using L = Lay<n>;
   using Cf = PenaltyCfg<n, GEO>;
   constexpr int n2 = L::n2, n3 = L::n3, RS = L::RS, PS = L::PS, CST = L::CST, VOL = Cf::VOL;
