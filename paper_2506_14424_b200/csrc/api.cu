@@ -888,11 +888,20 @@ dgvv_status dgvv_update_viscosity(dgvv_ctx* c, const double* u_lin, dgvv_stream 
     for (int i = 0; i < 4; ++i) a.law[i] = c->visc.p[i];
     a.nu_cell = L.nu_cell;
     a.nu_face = L.nu_face;
+    a.bad = c->d_flag;                       // domain check in the kernel: one host read at the end
+    if (l == 0) DGVV_CUDA_TRY(cudaMemsetAsync(c->d_flag, 0, sizeof(int), s));
     DGVV_CUDA_TRY(launch_carreau(n, c->geo, a, s));
-    TRY(check_positive(c, L.nu_cell, (long)c->n_owned * n3, s, "Carreau viscosity (cells)"));
-    TRY(check_positive(c, L.nu_face, (long)c->n_total * 6 * n * n, s, "Carreau viscosity (faces)"));
     TRY(premultiply(c, (int)l, L.nu_cell, L.nu_face, L.wv_cell, L.wv_face, s));
     L.dinv_ok[0] = false;                    // the diagonal depends on nu: recomputed lazily (same buffer)
+  }
+  {
+    int bad = 0;
+    DGVV_CUDA_TRY(cudaMemcpyAsync(&bad, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+    DGVV_CUDA_TRY(cudaStreamSynchronize(s));
+    if (bad) {
+      c->nu_ready = false;
+      return dgvv_fail(DGVV_EDOMAIN, "Carreau viscosity: %d quadrature points with non-positive or non-finite value", bad);
+    }
   }
   c->ulin = u_lin;
   c->nu_ready = true;

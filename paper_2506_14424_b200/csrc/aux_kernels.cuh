@@ -11,8 +11,16 @@ namespace dgvv {
 // point from the cell's own trace gradient (PAPER.md:838-866 eqn:viscosity_pointwise; G8).
 // NuArgs: see common.cuh
 
+#ifndef DGVV_K3_MINB
+#define DGVV_K3_MINB 0    // 0: compiler's register choice
+#endif
+#if DGVV_K3_MINB > 0
+#define K3_BOUNDS(t) __launch_bounds__(t, DGVV_K3_MINB)
+#else
+#define K3_BOUNDS(t) __launch_bounds__(t)
+#endif
 template <int n, int GEO, int CPB>
-__global__ void __launch_bounds__(CPB * n * n) carreau_nu_kernel(const NuArgs A) {
+__global__ void K3_BOUNDS(CPB * n * n) carreau_nu_kernel(const NuArgs A) {
   constexpr int n2 = n * n, n3 = n2 * n;
   constexpr int CS = 3 * n3 + 3 * n2;
   extern __shared__ double smem[];
@@ -76,7 +84,11 @@ __global__ void __launch_bounds__(CPB * n * n) carreau_nu_kernel(const NuArgs A)
 #pragma unroll
         for (int r = 0; r < 9; ++r) Ji[r] = vm[r * n3];
       }
-      if (active) A.nu_cell[(size_t)cell * n3 + q] = eta_of(gx, Ji);
+      if (active) {
+        const double e = eta_of(gx, Ji);
+        A.nu_cell[(size_t)cell * n3 + q] = e;
+        if (!(e > 0.0) || !isfinite(e)) atomicAdd(A.bad, 1);
+      }
     }
   }
 #pragma unroll
@@ -122,7 +134,10 @@ __global__ void __launch_bounds__(CPB * n * n) carreau_nu_kernel(const NuArgs A)
         for (int r = 0; r < 9; ++r) Ji[r] = fm[r * n2];
       }
       const double e = eta_of(gx, Ji);
-      if (active) A.nu_face[((size_t)cell * 6 + f) * n2 + p] = e;
+      if (active) {
+        A.nu_face[((size_t)cell * 6 + f) * n2 + p] = e;
+        if (!(e > 0.0) || !isfinite(e)) atomicAdd(A.bad, 1);
+      }
       __syncthreads();
     }
   }

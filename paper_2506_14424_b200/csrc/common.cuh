@@ -125,6 +125,7 @@ struct NuArgs {
   double law[4];
   double* nu_cell;          // [n_owned][n^3]
   double* nu_face;          // [n_total][6][n^2]
+  int* bad;                 // counts points with nu <= 0 or non-finite (domain check)
 };
 
 struct DiagArgs {

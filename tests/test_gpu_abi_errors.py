@@ -86,3 +86,21 @@ def test_continuous_level_requires_chain():
     fine.vcycle(A.OP_VISCOUS, b, x, [1.2 * lam, 1.2 * lamc, 1.0])
     assert torch.isfinite(x).all()
     assert status_of(lambda: fine.vcycle_fp32(A.OP_VISCOUS, b, x, [1.2 * lam, 1.2 * lamc, 1.0])) == A.EUNSUPPORTED
+
+
+def test_carreau_domain_check_in_kernel():
+    """update_viscosity checks nu > 0 and finite at every point inside the K3 kernel (one host read):
+    a non-finite u_lin gives DGVV_EDOMAIN and leaves the operator unusable until a valid update."""
+    from inputs.vectors import c3_linearization
+    m = cube(2)
+    ctx = Ctx(m, 4, visc_law=laws.C3_CARREAU)
+    u0 = c3_linearization(m, 4)
+    bad = u0.copy()
+    bad[5] = np.nan
+    w = torch.from_numpy(uniform(0, len(u0))).cuda()
+    y = torch.empty_like(w)
+    assert status_of(lambda: ctx.update_viscosity(torch.from_numpy(bad).cuda())) == A.EDOMAIN
+    assert status_of(lambda: ctx.apply_viscous(w, y)) == A.ESTATE
+    ctx.update_viscosity(torch.from_numpy(u0).cuda())
+    ctx.apply_viscous(w, y)
+    assert torch.isfinite(y).all()
