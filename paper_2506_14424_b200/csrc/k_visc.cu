@@ -59,9 +59,17 @@ template <int n, int GEO> constexpr int minb_visc() {
 template <typename R, int n, int GEO> constexpr int cpb_visc_t() {
   return (sizeof(R) == 4 && GEO == 0 && n == 4) ? CPB4F : cpb_visc<n, GEO>();
 }
+#ifndef MINB4GF
+#define MINB4GF 6
+#endif
+#ifndef MINBGF_COARSE
+#define MINBGF_COARSE 6   // 0: as FP64
+#endif
 template <typename R, int n, int GEO> constexpr int minb_visc_t() {
   if constexpr (sizeof(R) == 4 && GEO == 0)
     return n == 2 ? MINB2F : n == 3 ? MINB3F : n == 4 ? MINB4F : n == 5 ? MINB5F : minb_visc<n, GEO>();
+  else if constexpr (sizeof(R) == 4 && GEO == 1)
+    return n == 4 ? MINB4GF : ((n == 2 || n == 3) && MINBGF_COARSE > 0) ? MINBGF_COARSE : minb_visc<n, GEO>();
   else
     return minb_visc<n, GEO>();
 }
