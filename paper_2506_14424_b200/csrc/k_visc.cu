@@ -37,8 +37,12 @@ template <int n, int GEO> constexpr int cpb_visc() {
 #ifndef MINB3
 #define MINB3 4
 #endif
+#ifndef MINB23G
+#define MINB23G 3   // general geometry n = 2, 3 (0: as Cartesian); 2 / 6 measured slower
+#endif
 template <int n, int GEO> constexpr int minb_visc() {
-  return n == 2 ? MINB2 : n == 3 ? MINB3 : n == 4 ? (GEO ? MINB4G : MINB4) : n == 5 ? MINB5 : 2;
+  return (GEO && (n == 2 || n == 3) && MINB23G > 0) ? MINB23G
+         : n == 2 ? MINB2 : n == 3 ? MINB3 : n == 4 ? (GEO ? MINB4G : MINB4) : n == 5 ? MINB5 : 2;
 }
 // FP32 multigrid levels (half the registers and shared memory per cell)
 #ifndef MINB5F
