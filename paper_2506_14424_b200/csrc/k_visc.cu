@@ -8,13 +8,14 @@ namespace dgvv {
 cudaError_t upload_tables_visc(const Tab1D* tabs) { return tu_upload_tables(tabs); }
 
 // cells per CTA and min resident CTAs per SM (register cap), chosen by measurement (DESIGN.md
-// §11): n = 4 general geometry (C2) 4 cells x 4 CTAs (smem-bound by the TMA face stage);
+// §11): n = 4 general geometry (C2) 2 cells x 8 CTAs (smem-bound by the TMA face stage; 4 x 4:
+// +2 %);
 // n = 4 Cartesian (C5) 8 x 4; n = 5 Cartesian (C3) 5 x 3 (125 threads: 98 % lane use).
 #ifndef CPB4G
-#define CPB4G 4
+#define CPB4G 2
 #endif
 #ifndef MINB4G
-#define MINB4G 4
+#define MINB4G 8
 #endif
 #ifndef CPB4
 #define CPB4 8
@@ -60,8 +61,11 @@ template <int n, int GEO> constexpr int minb_visc() {
 #ifndef CPB4F
 #define CPB4F CPB4
 #endif
+#ifndef CPB4GF
+#define CPB4GF 4   // FP32 general geometry n = 4 (tuned with MINB4GF = 6)
+#endif
 template <typename R, int n, int GEO> constexpr int cpb_visc_t() {
-  return (sizeof(R) == 4 && GEO == 0 && n == 4) ? CPB4F : cpb_visc<n, GEO>();
+  return (sizeof(R) == 4 && n == 4) ? (GEO ? CPB4GF : CPB4F) : cpb_visc<n, GEO>();
 }
 #ifndef MINB4GF
 #define MINB4GF 6
