@@ -10,7 +10,7 @@ cudaError_t upload_tables_visc(const Tab1D* tabs) { return tu_upload_tables(tabs
 // cells per CTA and min resident CTAs per SM (register cap), chosen by measurement (DESIGN.md
 // §11): n = 4 general geometry (C2) 2 cells x 8 CTAs (smem-bound by the TMA face stage; 4 x 4:
 // +2 %);
-// n = 4 Cartesian (C5) 8 x 4; n = 5 Cartesian (C3) 5 x 3 (125 threads: 98 % lane use).
+// n = 4 Cartesian (C5) 4 x 8 (8 x 4: +2 %, 2 x 16: +3 %); n = 5 Cartesian (C3) 5 x 3 (125 threads: 98 % lane use).
 #ifndef CPB4G
 #define CPB4G 2
 #endif
@@ -18,10 +18,10 @@ cudaError_t upload_tables_visc(const Tab1D* tabs) { return tu_upload_tables(tabs
 #define MINB4G 8
 #endif
 #ifndef CPB4
-#define CPB4 8
+#define CPB4 4
 #endif
 #ifndef MINB4
-#define MINB4 4
+#define MINB4 8
 #endif
 #ifndef CPB5
 #define CPB5 5
@@ -59,7 +59,7 @@ template <int n, int GEO> constexpr int minb_visc() {
 #define MINB3F 5
 #endif
 #ifndef CPB4F
-#define CPB4F CPB4
+#define CPB4F 8
 #endif
 #ifndef CPB4GF
 #define CPB4GF 4   // FP32 general geometry n = 4 (tuned with MINB4GF = 6)
