@@ -29,14 +29,17 @@ cudaError_t upload_tables_visc(const Tab1D* tabs) { return tu_upload_tables(tabs
 #ifndef MINB5
 #define MINB5 3
 #endif
+#ifndef CPB3
+#define CPB3 7
+#endif
 template <int n, int GEO> constexpr int cpb_visc() {
-  return n == 2 ? 32 : n == 3 ? 14 : n == 4 ? (GEO ? CPB4G : CPB4) : n == 5 ? CPB5 : 3;
+  return n == 2 ? 32 : n == 3 ? (GEO ? 14 : CPB3) : n == 4 ? (GEO ? CPB4G : CPB4) : n == 5 ? CPB5 : 3;
 }
 #ifndef MINB2
 #define MINB2 4
 #endif
 #ifndef MINB3
-#define MINB3 4
+#define MINB3 8
 #endif
 #ifndef MINB23G
 #define MINB23G 3   // general geometry n = 2, 3 (0: as Cartesian); 2 / 6 measured slower
@@ -64,8 +67,11 @@ template <int n, int GEO> constexpr int minb_visc() {
 #ifndef CPB4GF
 #define CPB4GF 4   // FP32 general geometry n = 4 (tuned with MINB4GF = 6)
 #endif
+#ifndef CPB3F
+#define CPB3F 14
+#endif
 template <typename R, int n, int GEO> constexpr int cpb_visc_t() {
-  return (sizeof(R) == 4 && n == 4) ? (GEO ? CPB4GF : CPB4F) : cpb_visc<n, GEO>();
+  return (sizeof(R) == 4 && n == 4) ? (GEO ? CPB4GF : CPB4F) : (sizeof(R) == 4 && n == 3) ? CPB3F : cpb_visc<n, GEO>();
 }
 #ifndef MINB4GF
 #define MINB4GF 6
