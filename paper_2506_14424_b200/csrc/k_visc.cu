@@ -32,8 +32,11 @@ cudaError_t upload_tables_visc(const Tab1D* tabs) { return tu_upload_tables(tabs
 #ifndef CPB3
 #define CPB3 7
 #endif
+#ifndef CPB2
+#define CPB2 32
+#endif
 template <int n, int GEO> constexpr int cpb_visc() {
-  return n == 2 ? 32 : n == 3 ? (GEO ? 14 : CPB3) : n == 4 ? (GEO ? CPB4G : CPB4) : n == 5 ? CPB5 : 3;
+  return n == 2 ? (GEO ? 32 : CPB2) : n == 3 ? (GEO ? 14 : CPB3) : n == 4 ? (GEO ? CPB4G : CPB4) : n == 5 ? CPB5 : 3;
 }
 #ifndef MINB2
 #define MINB2 4
@@ -71,7 +74,8 @@ template <int n, int GEO> constexpr int minb_visc() {
 #define CPB3F 14
 #endif
 template <typename R, int n, int GEO> constexpr int cpb_visc_t() {
-  return (sizeof(R) == 4 && n == 4) ? (GEO ? CPB4GF : CPB4F) : (sizeof(R) == 4 && n == 3) ? CPB3F : cpb_visc<n, GEO>();
+  return (sizeof(R) == 4 && n == 4) ? (GEO ? CPB4GF : CPB4F) : (sizeof(R) == 4 && n == 3) ? CPB3F
+         : (sizeof(R) == 4 && n == 2) ? 32 : cpb_visc<n, GEO>();
 }
 #ifndef MINB4GF
 #define MINB4GF 6
