@@ -227,6 +227,23 @@ class CarreauNu:
         return self._eta(sym(grad_at(self.d, self.U[cells], self.d.dPhiF[f], Jinv)))
 
 
+def coarse_level_ulin(disc_f: Disc, disc_c: Disc, u_lin: np.ndarray) -> np.ndarray:
+    """Reading G19 (§5.3: the viscosity is stored at the integration points
+    of every multigrid level and refreshed on all levels when the linearisation changes): the
+    linearisation velocity of a coarser p-level is the fine polynomial u_lin evaluated at that
+    level's Gauss points, i.e. its coefficients in the coarse collocation basis (G2).  Full-tensor:
+    every fine basis function tabulated at every coarse volume point."""
+    Phi_fc = B.tabulate(disc_f.xi, disc_c.vol_pts)[0]                  # [N_c, N_f]
+    U = u_lin.reshape(disc_f.mesh.n_cells, 3, disc_f.N)
+    return np.einsum("pn,cin->cip", Phi_fc, U).reshape(-1)
+
+
+def coarse_level_nu(disc_f: Disc, disc_c: Disc, u_lin: np.ndarray, p: dict) -> "CarreauNu":
+    """G19: the Carreau viscosity of a coarser level, eta(gamma_dot(eps)) of the interpolated
+    linearisation velocity at that level's cell points and, per side, its face points (G8)."""
+    return CarreauNu(disc_c, coarse_level_ulin(disc_f, disc_c, u_lin), p)
+
+
 class NewtonDeltaNu:
     """delta nu[w] = 2 g(gamma_dot_0) eps(u0):eps(w), g = eta'/gamma_dot (reading G10), at every
     cell point and per side at face points from each side's own traces."""

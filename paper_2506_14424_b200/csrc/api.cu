@@ -87,12 +87,15 @@ dgvv_status nccl_load() {
   } while (0)
 
 // ------------------------------------------------------------------ tables
+// each TU's __constant__ tables live per device: uploaded once per DEVICE, not once
+// per process — a context created later on another device would otherwise read zero tables
 std::mutex g_tab_mu;
-bool g_tab_done = false;
+uint64_t g_tab_done = 0;     // bit d: tables uploaded to device d
 
 dgvv_status upload_tables() {
   std::lock_guard<std::mutex> lk(g_tab_mu);
-  if (g_tab_done) return DGVV_OK;
+  const uint64_t bit = current_device_bit();
+  if (g_tab_done & bit) return DGVV_OK;
   std::vector<Tab1D> tabs(DGVV_NMAX + 1);
   std::memset(tabs.data(), 0, sizeof(Tab1D) * tabs.size());
   for (int n = 1; n <= DGVV_NMAX; ++n) make_tab(n, &tabs[n]);
@@ -101,7 +104,7 @@ dgvv_status upload_tables() {
   DGVV_CUDA_TRY(upload_tables_aux(tabs.data()));
   DGVV_CUDA_TRY(upload_tables_newton(tabs.data()));
   DGVV_CUDA_TRY(upload_tables_pen(tabs.data()));
-  g_tab_done = true;
+  g_tab_done |= bit;
   return DGVV_OK;
 }
 }  // namespace
@@ -152,6 +155,7 @@ struct Peer {
 };
 
 struct dgvv_ctx {
+  int device = 0;               // CUDA device the context was set up on (every call must run there)
   int n_owned = 0, n_ghost = 0, n_total = 0;
   long long first = 0, n_global = 0;
   int geo = 0;                  // 0 Cartesian fast path, 1 general iso-parametric
@@ -278,8 +282,19 @@ inline long level_dofs(const dgvv_ctx* c, int l) {
   return (long)c->n_owned * n * n * n;
 }
 
-dgvv_status check_level(const dgvv_ctx* c, int level) {
+// null context, or a call made while another device is current (device memory and
+// the per-device tables / kernel attributes of the context belong to its setup device)
+dgvv_status check_ctx(const dgvv_ctx* c) {
   if (!c) return dgvv_fail(DGVV_EINVAL, "null context");
+  int d = -1;
+  cudaGetDevice(&d);
+  if (d != c->device)
+    return dgvv_fail(DGVV_ESTATE, "context was set up on device %d but device %d is current", c->device, d);
+  return DGVV_OK;
+}
+
+dgvv_status check_level(const dgvv_ctx* c, int level) {
+  TRY(check_ctx(c));
   if (level < 0 || level >= (int)c->L.size()) return dgvv_fail(DGVV_EINVAL, "level %d out of range", level);
   return DGVV_OK;
 }
@@ -371,6 +386,7 @@ ApplyArgs base_args(dgvv_ctx* c, int l, int op) {
 }
 
 dgvv_status op_ready(dgvv_ctx* c, int op) {
+  TRY(check_ctx(c));
   if (op == DGVV_OP_VISCOUS) {
     if (!c->has_visc) return dgvv_fail(DGVV_ESTATE, "no viscosity law given at setup");
     if (c->carreau && !c->nu_ready) return dgvv_fail(DGVV_ESTATE, "Carreau law: call dgvv_update_viscosity first");
@@ -567,6 +583,7 @@ static dgvv_status setup_impl(const dgvv_mesh* m, int32_t degree, const dgvv_law
   if (m->map_degree < 1 || m->map_degree > 7) return dgvv_fail(DGVV_EUNSUPPORTED, "map_degree %d not in 1..7", m->map_degree);
   if (!vl && !pl) return dgvv_fail(DGVV_EINVAL, "at least one of visc_law / poisson_law is required");
   TRY(upload_tables());
+  DGVV_CUDA_TRY(cudaGetDevice(&c->device));
 
   c->n_owned = m->n_cells;
   c->n_ghost = m->n_ghost;
@@ -851,7 +868,7 @@ dgvv_status dgvv_setup(const dgvv_mesh* m, int32_t degree, const dgvv_law* vl, c
 }
 
 dgvv_status dgvv_update_viscosity(dgvv_ctx* c, const double* u_lin, dgvv_stream stream) {
-  if (!c) return dgvv_fail(DGVV_EINVAL, "null context");
+  TRY(check_ctx(c));
   if (!c->carreau) return dgvv_fail(DGVV_EUNSUPPORTED, "update_viscosity needs the Carreau law");
   if (!u_lin) return dgvv_fail(DGVV_EINVAL, "u_lin is null");
   cudaStream_t s = (cudaStream_t)stream;
@@ -1031,7 +1048,7 @@ dgvv_status dgvv_apply_poisson(dgvv_ctx* c, int32_t level, const double* src, do
 }
 
 dgvv_status dgvv_apply_linearized_viscous(dgvv_ctx* c, const double* src, double* dst, dgvv_stream stream) {
-  if (!c) return dgvv_fail(DGVV_EINVAL, "null context");
+  TRY(check_ctx(c));
   if (!c->has_visc || !c->carreau) return dgvv_fail(DGVV_EUNSUPPORTED, "linearised apply needs the Carreau law");
   if (!c->nu_ready || !c->ulin) return dgvv_fail(DGVV_ESTATE, "call dgvv_update_viscosity first");
   if (!src || !dst || src == dst || dst == c->ulin) return dgvv_fail(DGVV_EINVAL, "bad vectors (null or aliasing)");
@@ -1061,7 +1078,7 @@ dgvv_status dgvv_apply_linearized_viscous(dgvv_ctx* c, const double* src, double
 static dgvv_status ensure_dinv_pen(dgvv_ctx* c, cudaStream_t s);
 
 dgvv_status dgvv_set_mass(dgvv_ctx* c, int32_t op, double mass) {
-  if (!c) return dgvv_fail(DGVV_EINVAL, "null context");
+  TRY(check_ctx(c));
   if (op != DGVV_OP_VISCOUS && op != DGVV_OP_POISSON) return dgvv_fail(DGVV_EINVAL, "unknown op %d", op);
   if (!std::isfinite(mass) || mass < 0.0) return dgvv_fail(DGVV_EDOMAIN, "mass coefficient %g must be finite and >= 0", mass);
   if (c->mass[op] == mass) return DGVV_OK;
@@ -1182,7 +1199,7 @@ static dgvv_status vcycle_rec(dgvv_ctx* c, int op, int l, const double* b, doubl
   const int oi = op == DGVV_OP_VISCOUS ? 0 : 1;
   auto& S = c->L[l].scratch[oi];   // [0] r, [1..2] work, (l>0: [3] b, [4] x of coarser handled by caller)
   const int last = (int)c->L.size() - 1;
-  if (l == last && !c->coarse && c->Ainv[oi]) {
+  if (l == last && !c->coarse && !c->cg.on && c->Ainv[oi]) {   // the c-level, when enabled, comes first
     if (c->direct_epoch[oi] != c->coef_epoch)
       return dgvv_fail(DGVV_ESTATE, "direct coarse solver is stale (coefficients or mass changed): call dgvv_setup_coarse_solver again");
     DGVV_CUDA_TRY(launch_dense_matvec(c->Ainv[oi], b, x, c->direct_n[oi], s));
@@ -1349,7 +1366,7 @@ static dgvv_status vcycle_rec_f(dgvv_ctx* c, int op, int l, const float* b, floa
   const int nc = op == DGVV_OP_VISCOUS ? 3 : 1;
   auto& S = c->LF[l].scratch[oi];
   const int last = (int)c->L.size() - 1;
-  if (l == last && !c->coarse && c->Ainv[oi]) {  // direct coarse solve, FP64 arithmetic
+  if (l == last && !c->coarse && !c->cg.on && c->Ainv[oi]) {   // direct coarse solve, FP64 arithmetic; the c-level, when enabled, comes first
     if (c->direct_epoch[oi] != c->coef_epoch)
       return dgvv_fail(DGVV_ESTATE, "direct coarse solver is stale (coefficients or mass changed): call dgvv_setup_coarse_solver again");
     DGVV_CUDA_TRY(launch_dense_matvec_f(c->Ainv[oi], b, x, c->direct_n[oi], s));
@@ -2012,7 +2029,13 @@ static dgvv_status cg_setup_direct(dgvv_ctx* c, int op, int32_t* n_dofs) {
   int bad = 0;
   DGVV_CUDA_TRY(cudaMemcpyAsync(&bad, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
   DGVV_CUDA_TRY(cudaStreamSynchronize(s));
-  if (bad) return dgvv_fail(DGVV_EDOMAIN, "direct coarse solver: %d non-positive pivots (operator not SPD?)", bad);
+  if (bad) {                                  // drop the inverse: later V-cycles fall back to Chebyshev
+    cudaFree(G.Ainv[oi]);
+    c->allocs.erase(std::remove(c->allocs.begin(), c->allocs.end(), (void*)G.Ainv[oi]), c->allocs.end());
+    G.Ainv[oi] = nullptr;
+    G.direct_epoch[oi] = -1;
+    return dgvv_fail(DGVV_EDOMAIN, "direct coarse solver: %d non-positive pivots (operator not SPD?)", bad);
+  }
   G.direct_n[oi] = (int)N;
   G.direct_epoch[oi] = c->coef_epoch;
   if (n_dofs) *n_dofs = (int32_t)N;
@@ -2020,7 +2043,7 @@ static dgvv_status cg_setup_direct(dgvv_ctx* c, int op, int32_t* n_dofs) {
 }
 
 dgvv_status dgvv_set_continuous_level(dgvv_ctx* c, int32_t enable) {
-  if (!c) return dgvv_fail(DGVV_EINVAL, "null context");
+  TRY(check_ctx(c));
   if (!enable) { c->cg.on = false; return DGVV_OK; }
   if (c->L.back().k != 1) return dgvv_fail(DGVV_EINVAL, "continuous level: the coarsest degree must be 1 (is %d)", c->L.back().k);
   if (c->n_ghost || c->comm) return dgvv_fail(DGVV_EUNSUPPORTED, "continuous level: single-GPU contexts only");
@@ -2087,7 +2110,7 @@ dgvv_status dgvv_set_continuous_level(dgvv_ctx* c, int32_t enable) {
 }
 
 dgvv_status dgvv_continuous_level_info(const dgvv_ctx* c, int32_t* n_vertices, int32_t* n_colors) {
-  if (!c) return dgvv_fail(DGVV_EINVAL, "null context");
+  TRY(check_ctx(c));
   if (!c->cg.on) return dgvv_fail(DGVV_ESTATE, "continuous level not enabled");
   if (n_vertices) *n_vertices = c->cg.nv;
   if (n_colors) *n_colors = c->cg.ncolors;
@@ -2183,7 +2206,7 @@ dgvv_status dgvv_set_coarse_context(dgvv_ctx* c, dgvv_ctx* cc, const int32_t* pa
 }
 
 static dgvv_status h_ready(dgvv_ctx* c, int op) {
-  if (!c) return dgvv_fail(DGVV_EINVAL, "null context");
+  TRY(check_ctx(c));
   if (!c->coarse) return dgvv_fail(DGVV_ESTATE, "no coarse context: call dgvv_set_coarse_context first");
   if (op != DGVV_OP_VISCOUS && op != DGVV_OP_POISSON) return dgvv_fail(DGVV_EINVAL, "unknown op %d", op);
   return DGVV_OK;
@@ -2204,7 +2227,7 @@ dgvv_status dgvv_restrict_h(dgvv_ctx* c, int32_t op, const double* fine, double*
 }
 
 dgvv_status dgvv_setup_coarse_solver(dgvv_ctx* c, int32_t op, int32_t* n_dofs) {
-  if (!c) return dgvv_fail(DGVV_EINVAL, "null context");
+  TRY(check_ctx(c));
   if (op != DGVV_OP_VISCOUS && op != DGVV_OP_POISSON) return dgvv_fail(DGVV_EINVAL, "unknown op %d", op);
   TRY(op_ready(c, op));
   if (c->n_ghost || c->comm) return dgvv_fail(DGVV_EUNSUPPORTED, "direct coarse solver: single-GPU contexts only");
@@ -2248,7 +2271,7 @@ dgvv_status dgvv_setup_coarse_solver(dgvv_ctx* c, int32_t op, int32_t* n_dofs) {
 
 dgvv_status dgvv_estimate_lambda_max(dgvv_ctx* c, int32_t op, int32_t level, int32_t steps, const double* v0,
                                      double* out, dgvv_stream stream) {
-  if (!c) return dgvv_fail(DGVV_EINVAL, "null context");
+  TRY(check_ctx(c));
   const bool cgl = c->cg.on && level == (int)c->L.size();      // the continuous (c-) level
   if (!cgl) TRY(check_level(c, level));
   TRY(op_ready(c, op));

@@ -4,6 +4,9 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#ifndef __CUDACC_RTC__
+#include <atomic>
+#endif
 
 #define DGVV_NMAX 8        // max points per direction (degree <= 7)
 #ifndef DGVV_MINB
@@ -152,3 +155,25 @@ struct DiagArgs {
 
 __host__ __device__ inline int face_t1(int d) { return d == 0 ? 1 : 0; }
 __host__ __device__ inline int face_t2(int d) { return d == 2 ? 1 : 2; }
+
+#ifndef __CUDACC_RTC__
+namespace dgvv {
+// Per-DEVICE one-time host setup: bit d of `done` is set once device d (the current
+// device) has the dynamic shared-memory opt-in of the kernels `ks`.  A second device in the same
+// process gets its own opt-in; concurrent first calls at worst set the attribute twice.
+inline uint64_t current_device_bit() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return 1ull << (d & 63);
+}
+template <typename... K>
+inline cudaError_t smem_optin(std::atomic<uint64_t>& done, size_t smem, K... ks) {
+  const uint64_t bit = current_device_bit();
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  cudaError_t e = cudaSuccess;
+  ((e = (e == cudaSuccess) ? cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) : e), ...);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
+}  // namespace dgvv
+#endif

@@ -20,12 +20,8 @@ static cudaError_t carreau_run(const NuArgs& a, cudaStream_t s) {
   constexpr int CPB = (128 / (n * n)) > 0 ? (128 / (n * n)) : 1;
   const size_t smem = (size_t)CPB * (3 * n * n * n + 3 * n * n) * sizeof(double);
   auto k = carreau_nu_kernel<n, GEO, CPB>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  if (cudaError_t e = smem_optin(attr, smem, k); e != cudaSuccess) return e;
   if (a.n_total <= 0) return cudaSuccess;
   k<<<(a.n_total + CPB - 1) / CPB, CPB * n * n, smem, s>>>(a);
   return cudaGetLastError();

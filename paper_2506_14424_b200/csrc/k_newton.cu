@@ -1,7 +1,6 @@
 // k_newton.cu — instantiations of the Newton-linearised viscous apply (K2).
 #include "tu_tables.cuh"
 #include "newton_apply.cuh"
-#include "newton_apply2.cuh"
 #include "newton_apply3.cuh"
 #include "launch.h"
 
@@ -19,24 +18,18 @@ template <int n> constexpr int cpb_newton() { return n == 2 ? 16 : n == 3 ? 8 : 
 #ifndef NMINB5
 #define NMINB5 10
 #endif
-// Cartesian cells: newton_apply2_kernel (no power evaluations, merged stresses)
+// Cartesian cells: newton_apply3_kernel from stored point data of u0 (the v2 kernel that
+// recomputed u0's gradients every apply was 5.21 ms vs 3.92 ms on C3; removed)
 template <int n> constexpr int cpb_newton2() { return n == 2 ? 16 : n == 3 ? 6 : n == 4 ? 2 : n == 5 ? NCPB5 : 1; }
 template <int n> constexpr int minb_newton2() { return n == 5 ? NMINB5 : n == 4 ? 4 : 2; }
 
-#ifndef DGVV_NEWTON_PD
-#define DGVV_NEWTON_PD 1   // Cartesian: v3 kernel from stored point data of u0 (newton_apply3.cuh)
-#endif
 template <int n>
 static cudaError_t run2(const ApplyArgs& a, cudaStream_t s) {
   constexpr int CPB = cpb_newton2<n>();
-  const size_t smem = (size_t)CPB * (DGVV_NEWTON_PD ? Newton3Cfg<n>::CS : Newton2Cfg<n>::CS) * sizeof(double);
-  auto k = DGVV_NEWTON_PD ? newton_apply3_kernel<n, CPB, minb_newton2<n>()> : newton_apply2_kernel<n, CPB, minb_newton2<n>()>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  const size_t smem = (size_t)CPB * Newton3Cfg<n>::CS * sizeof(double);
+  auto k = newton_apply3_kernel<n, CPB, minb_newton2<n>()>;
+  static std::atomic<uint64_t> attr{0};
+  if (cudaError_t e = smem_optin(attr, smem, k); e != cudaSuccess) return e;
   if (a.n_proc <= 0) return cudaSuccess;
   k<<<(a.n_proc + CPB - 1) / CPB, CPB * n * n, smem, s>>>(a);
   return cudaGetLastError();
@@ -48,18 +41,14 @@ static cudaError_t run(const ApplyArgs& a, cudaStream_t s) {
   constexpr int CPB = cpb_newton<n>();
   const size_t smem = (size_t)CPB * NewtonCfg<n, GEO>::CS * sizeof(double);
   auto k = newton_apply_kernel<n, GEO, CPB, 1>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  if (cudaError_t e = smem_optin(attr, smem, k); e != cudaSuccess) return e;
   if (a.n_proc <= 0) return cudaSuccess;
   k<<<(a.n_proc + CPB - 1) / CPB, CPB * n * n, smem, s>>>(a);
   return cudaGetLastError();
 }
 
-bool newton_uses_pointdata(int geo) { return geo == 0 && DGVV_NEWTON_PD; }
+bool newton_uses_pointdata(int geo) { return geo == 0; }
 
 template <int n>
 static cudaError_t npd_run(const ApplyArgs& a, int n_total, double* pc, double* pf, cudaStream_t s) {

@@ -23,12 +23,8 @@ static cudaError_t pen_run(const PenaltyArgs& a, bool diag, cudaStream_t s) {
   constexpr int CPB = cpb_pen<n>();
   const size_t smem = (size_t)CPB * PenaltyCfg<n, GEO>::CS * sizeof(double);
   auto k = penalty_apply_kernel<n, GEO, CPB>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  if (cudaError_t e = smem_optin(attr, smem, k); e != cudaSuccess) return e;
   if (a.n_proc <= 0) return cudaSuccess;
   k<<<(a.n_proc + CPB - 1) / CPB, CPB * n * n, smem, s>>>(a);
   return cudaGetLastError();
@@ -71,12 +67,8 @@ static cudaError_t conv_pd_apply(const ConvArgs& a, const double* wref, const do
   constexpr int CPB = cpb_pen<n>();
   const size_t smem = (size_t)CPB * 2 * 3 * Lay<n>::CST * sizeof(double);
   auto k = convective_pd_kernel<n, CPB>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  if (cudaError_t e = smem_optin(attr, smem, k); e != cudaSuccess) return e;
   if (a.n_proc <= 0) return cudaSuccess;
   k<<<(a.n_proc + CPB - 1) / CPB, CPB * n * n, smem, s>>>(a, wref, wface);
   return cudaGetLastError();

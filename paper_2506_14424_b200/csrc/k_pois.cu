@@ -66,13 +66,8 @@ static cudaError_t run(const ApplyArgsT<R>& a, cudaStream_t s) {
   const size_t smem = (size_t)CPB * Apply2Cfg<n, 1, 1, GEO>::CS * sizeof(R);
   auto k0 = sipg_apply2_kernel<R, n, 1, 1, GEO, CPB, minb_pois_t<R, n>(), false>;
   auto k1 = sipg_apply2_kernel<R, n, 1, 1, GEO, CPB, minb_pois_t<R, n>(), true>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  if (cudaError_t e = smem_optin(attr, smem, k0, k1); e != cudaSuccess) return e;
   if (a.n_proc <= 0) return cudaSuccess;
   const int grid = (a.n_proc + CPB - 1) / CPB;
   if (a.mass != 0.0) k1<<<grid, CPB * n * n, smem, s>>>(a);

@@ -100,13 +100,8 @@ static cudaError_t run(const ApplyArgsT<R>& a, cudaStream_t s) {
   // the Helmholtz mass term is a separate instantiation: the plain operator pays nothing for it
   auto k0 = sipg_apply2_kernel<R, n, NC, FORM, GEO, CPB, minb_visc_t<R, n, GEO>(), false>;
   auto k1 = sipg_apply2_kernel<R, n, NC, FORM, GEO, CPB, minb_visc_t<R, n, GEO>(), true>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  if (cudaError_t e = smem_optin(attr, smem, k0, k1); e != cudaSuccess) return e;
   if (a.n_proc <= 0) return cudaSuccess;
   const int grid = (a.n_proc + CPB - 1) / CPB;
   if (a.mass != 0.0) k1<<<grid, CPB * n * n, smem, s>>>(a);
@@ -138,12 +133,8 @@ static cudaError_t run_oseen(const ApplyArgs& a, cudaStream_t s) {
   constexpr int CPB = cpb_visc<n, GEO>();
   const size_t smem = (size_t)CPB * Apply2Cfg<n, 3, 0, GEO>::CS * sizeof(double);
   auto k = sipg_apply2_kernel<double, n, 3, 0, GEO, CPB, minb_visc<n, GEO>(), true, true>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  if (cudaError_t e = smem_optin(attr, smem, k); e != cudaSuccess) return e;
   if (a.n_proc <= 0) return cudaSuccess;
   k<<<(a.n_proc + CPB - 1) / CPB, CPB * n * n, smem, s>>>(a);
   return cudaGetLastError();

@@ -289,14 +289,18 @@ class Context:
         return dst
 
     def embed_continuous(self, op, src, dst, transpose=False, beta=0.0):
-        A.check(self._L.dgvv_embed_continuous(self.h, op, int(bool(transpose)), _ptr(src, None, "src"),
-                                              _ptr(dst, None, "dst"), float(beta), _stream()))
+        nc = 3 if op == A.OP_VISCOUS else 1
+        n_cg, n_dg = nc * self.n_vertices, nc * 8 * self.n_owned      # Q1 vertices / DG_1 cells
+        n_src, n_dst = (n_dg, n_cg) if transpose else (n_cg, n_dg)
+        A.check(self._L.dgvv_embed_continuous(self.h, op, int(bool(transpose)), _ptr(src, n_src, "src"),
+                                              _ptr(dst, n_dst, "dst"), float(beta), _stream()))
         return dst
 
     def estimate_lambda_max_continuous(self, op, v0, steps=20):
         """lambda_max(D^-1 A) of the continuous level (dgvv_estimate_lambda_max, level = n_levels)."""
         out = C.c_double()
-        A.check(self._L.dgvv_estimate_lambda_max(self.h, op, len(self.degrees), steps, _ptr(v0, None, "v0"),
+        n = (3 if op == A.OP_VISCOUS else 1) * self.n_vertices
+        A.check(self._L.dgvv_estimate_lambda_max(self.h, op, len(self.degrees), steps, _ptr(v0, n, "v0"),
                                                  C.byref(out), _stream()))
         return out.value
 
@@ -319,13 +323,15 @@ class Context:
 
     def prolongate_h(self, op, coarse_vec, fine_vec, beta=0.0):
         nf = self._n(op, len(self.degrees) - 1)
-        A.check(self._L.dgvv_prolongate_h(self.h, op, _ptr(coarse_vec, None, "coarse"), _ptr(fine_vec, nf, "fine"),
+        nc = self._coarse._n(op, 0) if getattr(self, "_coarse", None) is not None else None
+        A.check(self._L.dgvv_prolongate_h(self.h, op, _ptr(coarse_vec, nc, "coarse"), _ptr(fine_vec, nf, "fine"),
                                           float(beta), _stream()))
         return fine_vec
 
     def restrict_h(self, op, fine_vec, coarse_vec, beta=0.0):
         nf = self._n(op, len(self.degrees) - 1)
-        A.check(self._L.dgvv_restrict_h(self.h, op, _ptr(fine_vec, nf, "fine"), _ptr(coarse_vec, None, "coarse"),
+        nc = self._coarse._n(op, 0) if getattr(self, "_coarse", None) is not None else None
+        A.check(self._L.dgvv_restrict_h(self.h, op, _ptr(fine_vec, nf, "fine"), _ptr(coarse_vec, nc, "coarse"),
                                         float(beta), _stream()))
         return coarse_vec
 
@@ -351,7 +357,11 @@ class Context:
         return [(r[i], sc[i], rc[i]) for i in range(n.value)]
 
     def pack_ghosts(self, kind, src, sendbuf, level=0):
-        A.check(self._L.dgvv_pack_ghosts(self.h, level, kind, _ptr(src, None, "src"), _ptr(sendbuf, None, "sendbuf"),
+        k = self.degrees[level]
+        per = (1 if kind == A.GHOST_POISSON else 3) * (k + 1) ** 3
+        n_send = sum(s for _, s, _ in self.ghost_layout())
+        A.check(self._L.dgvv_pack_ghosts(self.h, level, kind, _ptr(src, per * self.n_owned, "src"),
+                                         _ptr(sendbuf, max(1, per * n_send) if n_send else None, "sendbuf"),
                                          _stream()))
         return sendbuf
 

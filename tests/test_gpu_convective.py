@@ -243,6 +243,9 @@ def test_convective_multirank_bitwise():
         outs.append(y)
     torch.cuda.synchronize()
     assert torch.equal(torch.cat(outs), ref)
+    from test_gpu_multirank import oracle_close
+    d = dg.Disc(m, k)
+    oracle_close(torch.cat(outs), dg.convective_apply(d, u, w))
     # the fused operator mass M + A + C (one kernel) is partition-independent too
     for c in [ref_ctx] + ctxs:
         c.set_mass(0, 7.0)
@@ -254,6 +257,8 @@ def test_convective_multirank_bitwise():
         outs.append(y)
     torch.cuda.synchronize()
     assert torch.equal(torch.cat(outs), ref)
+    oracle_close(torch.cat(outs), dg.helmholtz_apply(d, u, dg.AnalyticNu(d, laws.C2_LAW), 7.0)
+                 + dg.convective_apply(d, u, w))
 
 
 def test_transport_point_data_follow_set_transport():

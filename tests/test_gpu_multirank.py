@@ -2,7 +2,9 @@
 whose ghost buffers are filled from the peers' packed send buffers (the library's own pack
 kernel and ghost ordering; NCCL only moves those same buffers).  The gathered result must be
 BITWISE equal to the single-context apply: each cell's output is a fixed-order sum of its
-own volume and face terms, independent of the partition."""
+own volume and face terms, independent of the partition.  Every
+gathered result is also compared with the CPU oracle (relative L2 <= 1e-12, reading G25), so
+the multi-rank path is held to the same bar as the one-context path, not only to itself."""
 import numpy as np
 import pytest
 
@@ -11,7 +13,7 @@ pytestmark = pytest.mark.gpu
 
 from inputs import bfs, cube, deformed_cube, uniform                       # noqa: E402
 from inputs.vectors import c3_linearization                               # noqa: E402
-from oracle import laws                                                    # noqa: E402
+from oracle import dg, laws                                                # noqa: E402
 from paper_2506_14424_b200 import _abi as A                               # noqa: E402
 from paper_2506_14424_b200.partition import slab_partition                # noqa: E402
 
@@ -20,6 +22,16 @@ from paper_2506_14424_b200.partition import slab_partition                # noqa
 def _need_gpu():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
+
+
+TOL = 1e-12
+
+
+def oracle_close(y, ref):
+    """Gathered multi-rank result vs the oracle: relative L2 <= 1e-12 (G25)."""
+    y = y.cpu().numpy()
+    err = np.linalg.norm(y - ref) / np.linalg.norm(ref)
+    assert err < TOL, err
 
 
 def make_ranks(m, R, k, **kw):
@@ -85,6 +97,8 @@ def test_viscous_multirank_bitwise(name, mk, k, R):
         outs.append(y)
     torch.cuda.synchronize()
     assert torch.equal(torch.cat(outs), ref)
+    d = dg.Disc(m, k)
+    oracle_close(torch.cat(outs), dg.viscous_apply(d, u, dg.AnalyticNu(d, laws.C2_LAW)))
 
 
 def test_poisson_and_carreau_multirank_bitwise():
@@ -106,6 +120,8 @@ def test_poisson_and_carreau_multirank_bitwise():
         outs.append(y)
     torch.cuda.synchronize()
     assert torch.equal(torch.cat(outs), ref)
+    dp = dg.Disc(m, 5)
+    oracle_close(torch.cat(outs), dg.poisson_apply(dp, p_, dg.AnalyticNu(dp, laws.C4_LAW)))
     # Carreau (ghost u_lin) + Picard and Newton applies, k=4
     k, per = 4, 3 * 125
     ul = torch.from_numpy(c3_linearization(m, k)).cuda()
@@ -132,3 +148,7 @@ def test_poisson_and_carreau_multirank_bitwise():
     torch.cuda.synchronize()
     assert torch.equal(torch.cat(op), refp)
     assert torch.equal(torch.cat(on), refn)
+    d = dg.Disc(m, k)
+    ul_h, w_h = ul.cpu().numpy(), w.cpu().numpy()
+    oracle_close(torch.cat(op), dg.viscous_apply(d, w_h, dg.CarreauNu(d, ul_h, laws.C3_CARREAU)))
+    oracle_close(torch.cat(on), dg.newton_apply(d, ul_h, w_h, laws.C3_CARREAU))

@@ -143,3 +143,5 @@ def test_penalty_multirank_bitwise():
         outs.append(y)
     torch.cuda.synchronize()
     assert torch.equal(torch.cat(outs), ref)
+    from test_gpu_multirank import oracle_close
+    oracle_close(torch.cat(outs), dg.penalty_apply(dg.Disc(m, k), u, td, tc))

@@ -206,3 +206,67 @@ def test_diagonal_and_lanczos():
     ev_s = np.linalg.eigvalsh(small * np.sqrt(np.outer(Ds, Ds)))
     lam_s = mg.lanczos_lambda_max(lambda x: small @ x, Ds, uniform(2, 16), 20)
     assert abs(lam_s - ev_s.max()) < 1e-10 * ev_s.max()
+
+
+# ----------------------------------------------------------------- G19 coarse-level viscosity
+def _nodal(disc, fn):
+    """Nodal (collocation) coefficients of a physical vector field fn(x [...,3]) -> [...,3]."""
+    x, _, _ = disc.vol_geom(np.arange(disc.mesh.n_cells))
+    return np.ascontiguousarray(np.transpose(fn(x), (0, 2, 1))).reshape(-1)
+
+
+@pytest.mark.parametrize("mk,kf,kc", [(lambda: cube(3), 4, 2), (lambda: deformed_cube(2, 2), 4, 2),
+                                      (lambda: cube(2), 3, 1)])
+def test_coarse_level_nu_g19_linear_field_is_exact(mk, kf, kc):
+    """G19 pin (closed form): for u = A x the strain is sym(A) everywhere.  x(xi) is Q_{map
+    degree} per cell, so u_lin's fine nodal interpolant and its coarse interpolation are both
+    exact when the map degree <= k_c: the coarse nu must equal eta(gamma_dot(sym A)) at every
+    coarse cell point and every face point of every side."""
+    m = mk()
+    df, dc = dg.Disc(m, kf), dg.Disc(m, kc)
+    Amat = np.array([[0.3, -1.2, 0.5], [0.7, 0.1, -0.4], [-0.2, 0.9, -0.4]])
+    ulin = _nodal(df, lambda x: x @ Amat.T)
+    nu = dg.coarse_level_nu(df, dc, ulin, laws.C3_CARREAU)
+    p = laws.C3_CARREAU
+    eps = 0.5 * (Amat + Amat.T)
+    expect = laws.carreau(np.sqrt(2.0 * np.sum(eps * eps)), p["eta0"], p["eta_inf"], p["lam"], p["n"])
+    cells = np.arange(m.n_cells)
+    assert np.allclose(nu.vol(cells), expect, rtol=1e-12, atol=0)
+    for f in range(6):
+        assert np.allclose(nu.face(cells, f), expect, rtol=1e-12, atol=0)
+    # and the interpolated coefficients are the field's values at the coarse Gauss points
+    assert np.allclose(dg.coarse_level_ulin(df, dc, ulin), _nodal(dc, lambda x: x @ Amat.T), rtol=0, atol=1e-13)
+
+
+def test_coarse_level_nu_g19_quadratic_field():
+    """G19 pin: a quadratic field is reproduced exactly by the k=2 level on box cells, so the
+    coarse-level nu equals eta of the analytic strain at the coarse physical points (cell and
+    face points); a transposed or wrongly ordered interpolation fails it."""
+    m = cube(3)
+    df, dc = dg.Disc(m, 4), dg.Disc(m, 2)
+
+    def u(x):
+        X, Y, Z = x[..., 0], x[..., 1], x[..., 2]
+        return np.stack([X * Y + 0.3 * Z * Z, -0.5 * X * X + Y * Z, 0.2 * X * Z - Y * Y], axis=-1)
+
+    def grad(x):
+        X, Y, Z = x[..., 0], x[..., 1], x[..., 2]
+        G = np.zeros(x.shape[:-1] + (3, 3))
+        G[..., 0, 0], G[..., 0, 1], G[..., 0, 2] = Y, X, 0.6 * Z
+        G[..., 1, 0], G[..., 1, 1], G[..., 1, 2] = -X, Z, Y
+        G[..., 2, 0], G[..., 2, 1], G[..., 2, 2] = 0.2 * Z, -2.0 * Y, 0.2 * X
+        return G
+
+    p = laws.C3_CARREAU
+    nu = dg.coarse_level_nu(df, dc, _nodal(df, u), p)
+
+    def eta(x):
+        e = 0.5 * (grad(x) + np.swapaxes(grad(x), -1, -2))
+        return laws.carreau(np.sqrt(2.0 * np.einsum("...ij,...ij->...", e, e)), p["eta0"], p["eta_inf"], p["lam"], p["n"])
+
+    cells = np.arange(m.n_cells)
+    xq, _, _ = dc.vol_geom(cells)
+    assert np.allclose(nu.vol(cells), eta(xq), rtol=1e-12, atol=0)
+    for f in range(6):
+        xf = dc.face_geom(cells, f)[0]
+        assert np.allclose(nu.face(cells, f), eta(xf), rtol=1e-12, atol=0)
