@@ -1,6 +1,8 @@
 """Summarise ncu reports (raw page) into one JSON per kernel + profiles/ncu_traffic.json.
 usage: python scripts/ncu_summary.py <tag>=<report.ncu-rep> ...  > profiles/rNN_ncu_summary.json"""
-import csv, io, json, subprocess, sys
+import csv, io, json, os, subprocess, sys
+
+TRAFFIC = os.environ.get("NCU_TRAFFIC", "profiles/r02_ncu_traffic.json")   # per-config DRAM bytes per launch (bench.py roofline.traffic)
 
 KEYS = {
     "gpu__time_duration.sum": "duration_us",
@@ -75,8 +77,8 @@ for arg in sys.argv[1:]:
     res[tag] = o
 print(json.dumps(res, indent=1))
 try:                                             # merge: keep the other kernels' entries
-    old = json.load(open("profiles/ncu_traffic.json"))
+    old = json.load(open(TRAFFIC))
 except (OSError, ValueError):
     old = {}
 old.update(traffic)
-json.dump(old, open("profiles/ncu_traffic.json", "w"), indent=1)
+json.dump(old, open(TRAFFIC, "w"), indent=1)
