@@ -155,10 +155,21 @@ enum { DGVV_PRECOND_NONE = 0, DGVV_PRECOND_JACOBI = 1, DGVV_PRECOND_VCYCLE = 2, 
  * side), no term on Neumann faces.  The paper takes tau_div, tau_cont from Fehn2018b without
  * formulas: they are inputs here, one value per cell (host arrays of n_cells + n_ghost
  * entries, owned cells then ghosts in the dgvv_mesh ghost order; copied).  DGVV_EDOMAIN for
- * negative or non-finite values.  Usable with dgvv_inverse_diagonal (level 0) and
- * dgvv_cg_solve (preconditioner none or Jacobi) as op = DGVV_OP_PENALTY. */
+ * negative or non-finite values.
+ * Multigrid for the penalty step ("a multigrid preconditioner is necessary
+ * for the penalty step"): the operator is defined on every p-level of the context (the level's
+ * degree and geometry, the same per-cell tau), so op = DGVV_OP_PENALTY works with
+ * dgvv_inverse_diagonal, dgvv_estimate_lambda_max and dgvv_chebyshev_smooth on any level, with
+ * dgvv_vcycle (p-levels of this context only: Chebyshev(5) pre/post smoothing with the
+ * unfused smoother r = b - A x, d = c_rho d + c_r D^-1 r, x += d; R = P^T of the velocity
+ * p-transfer; coarsest p-level Chebyshev(5) from zero; h-levels / the c-level are not used) and
+ * dgvv_cg_solve with preconditioner none, Jacobi or the FP64 V-cycle (lambda_hi_per_level: one
+ * value per p-level).  DGVV_ESTATE before dgvv_set_penalty_parameters.
+ * dgvv_apply_penalty: level 0; dgvv_apply_penalty_level: any p-level (same semantics). */
 dgvv_status dgvv_set_penalty_parameters(dgvv_ctx* ctx, const double* tau_div, const double* tau_cont);
 dgvv_status dgvv_apply_penalty(dgvv_ctx* ctx, const double* src, double* dst, dgvv_stream stream);
+dgvv_status dgvv_apply_penalty_level(dgvv_ctx* ctx, int32_t level, const double* src, double* dst,
+                                     dgvv_stream stream);
 
 /* Preconditioned conjugate gradients on (mass M +) A_op, level 0 (the Krylov solver of the
  * symmetric viscous and pressure steps):

@@ -58,6 +58,7 @@ _SIGS = {
     "dgvv_vcycle_fp32": [VP, I32, VP, VP, PD, VP],
     "dgvv_set_penalty_parameters": [VP, PD, PD],
     "dgvv_apply_penalty": [VP, VP, VP, VP],
+    "dgvv_apply_penalty_level": [VP, I32, VP, VP, VP],
     "dgvv_cg_solve": [VP, I32, VP, VP, D, I32, I32, PD, C.POINTER(I32), PD, VP],
     "dgvv_set_transport": [VP, VP, VP],
     "dgvv_set_coarse_context": [VP, VP, C.POINTER(I32), C.POINTER(C.c_int8)],

@@ -131,6 +131,11 @@ struct Level {
   double* ghost[2] = {nullptr, nullptr};   // ghost src buffers (NC = 3 / 1)
   double* ulin_ghost = nullptr;
   std::vector<double*> scratch[2];         // V-cycle scratch per op
+  // f2 penalty-step operator on this level (same per-cell tau on every level): inverse diagonal
+  // and V-cycle scratch [0] r, [1] Chebyshev work (r | d), [3] b, [4] x (levels >= 1)
+  double* dinv_pen = nullptr;
+  bool dinv_pen_ok = false;
+  std::vector<double*> scratch_pen;
 };
 
 // FP32 mirror of a level for the single-precision multigrid preconditioner (PAPER.md:1546-1551,
@@ -173,8 +178,6 @@ struct dgvv_ctx {
   // f2 penalty-step operator: per-cell parameters (owned then ghosts, internal order)
   double* d_tau_div = nullptr;
   double* d_tau_cont = nullptr;
-  double* dinv_pen = nullptr;
-  bool dinv_pen_ok = false;
   bool has_pen = false;
   // f4 convective term: transport field w (level 0, owned + ghosts), GMRES work
   double* d_wtr = nullptr;
@@ -1075,7 +1078,13 @@ dgvv_status dgvv_apply_linearized_viscous(dgvv_ctx* c, const double* src, double
   return run_apply(c, DGVV_OP_VISCOUS, 0, a, s, 1);
 }
 
-static dgvv_status ensure_dinv_pen(dgvv_ctx* c, cudaStream_t s);
+static dgvv_status ensure_dinv_pen(dgvv_ctx* c, int l, cudaStream_t s);
+static dgvv_status apply_penalty_impl(dgvv_ctx* c, int l, const double* src, double* dst, cudaStream_t s);
+static dgvv_status cheb_pen(dgvv_ctx* c, int l, double* x, const double* b, int degree, double lo, double hi,
+                            int x_is_zero, double* work, cudaStream_t s);
+static dgvv_status ensure_pen_scratch(dgvv_ctx* c);
+static dgvv_status vcycle_pen_rec(dgvv_ctx* c, int l, const double* b, double* x, const double* his,
+                                  cudaStream_t s);
 
 dgvv_status dgvv_set_mass(dgvv_ctx* c, int32_t op, double mass) {
   TRY(check_ctx(c));
@@ -1094,9 +1103,8 @@ dgvv_status dgvv_inverse_diagonal(dgvv_ctx* c, int32_t op, int32_t level, double
   if (!dst) return dgvv_fail(DGVV_EINVAL, "null dst");
   cudaStream_t s = (cudaStream_t)stream;
   if (op == DGVV_OP_PENALTY) {
-    if (level != 0) return dgvv_fail(DGVV_EINVAL, "penalty operator: level 0 only");
-    TRY(ensure_dinv_pen(c, s));
-    DGVV_CUDA_TRY(cudaMemcpyAsync(dst, c->dinv_pen, (size_t)3 * level_dofs(c, 0) * sizeof(double),
+    TRY(ensure_dinv_pen(c, level, s));
+    DGVV_CUDA_TRY(cudaMemcpyAsync(dst, c->L[level].dinv_pen, (size_t)3 * level_dofs(c, level) * sizeof(double),
                                   cudaMemcpyDeviceToDevice, s));
     return DGVV_OK;
   }
@@ -1149,6 +1157,8 @@ dgvv_status dgvv_chebyshev_smooth(dgvv_ctx* c, int32_t op, int32_t level, double
   if (!x || !b || !work) return dgvv_fail(DGVV_EINVAL, "null vector");
   if (degree < 1) return dgvv_fail(DGVV_EINVAL, "degree %d < 1", degree);
   if (!(lambda_hi > lambda_lo) || !(lambda_lo > 0.0)) return dgvv_fail(DGVV_EDOMAIN, "need 0 < lambda_lo < lambda_hi");
+  if (op == DGVV_OP_PENALTY)
+    return cheb_pen(c, level, x, b, degree, lambda_lo, lambda_hi, x_is_zero, work, (cudaStream_t)stream);
   return cheb_impl(c, op, level, x, b, degree, lambda_lo, lambda_hi, x_is_zero, work, (cudaStream_t)stream);
 }
 
@@ -1420,6 +1430,10 @@ dgvv_status dgvv_vcycle(dgvv_ctx* c, int32_t op, const double* b, double* x, con
                         dgvv_stream stream) {
   if (!c || !b || !x || !his) return dgvv_fail(DGVV_EINVAL, "null argument");
   TRY(op_ready(c, op));
+  if (op == DGVV_OP_PENALTY) {                 // f2: p-levels of this context
+    TRY(ensure_pen_scratch(c));
+    return vcycle_pen_rec(c, 0, b, x, his, (cudaStream_t)stream);
+  }
   TRY(ensure_vcycle_scratch(c, op));
   return vcycle_rec(c, op, 0, b, x, his, (cudaStream_t)stream);
 }
@@ -1475,10 +1489,10 @@ static dgvv_status dot_host(dgvv_ctx* c, const double* a, const double* b, long 
 }
 
 // ------------------------------------------------------------------ f2: penalty-step operator
-static PenaltyArgs penalty_args(dgvv_ctx* c) {
+static PenaltyArgs penalty_args(dgvv_ctx* c, int l) {
   PenaltyArgs a;
   std::memset(&a, 0, sizeof(a));
-  Level& L = c->L[0];
+  Level& L = c->L[l];
   a.nbr = c->d_nbr;
   a.n_proc = c->n_owned;
   a.n_owned = c->n_owned;
@@ -1493,29 +1507,95 @@ static PenaltyArgs penalty_args(dgvv_ctx* c) {
   return a;
 }
 
-static dgvv_status apply_penalty_impl(dgvv_ctx* c, const double* src, double* dst, cudaStream_t s) {
-  PenaltyArgs a = penalty_args(c);
+// the penalty-step operator on level l (the level's degree and geometry, the same per-cell tau)
+static dgvv_status apply_penalty_impl(dgvv_ctx* c, int l, const double* src, double* dst, cudaStream_t s) {
+  PenaltyArgs a = penalty_args(c, l);
   a.src = src;
   a.dst = dst;
+  Level& L = c->L[l];
   if (c->n_ghost) {
-    if (!c->L[0].ghost[0]) TRY(dalloc(c, &c->L[0].ghost[0], (size_t)c->n_ghost * 3 * c->L[0].n * c->L[0].n * c->L[0].n));
-    a.ghost = c->L[0].ghost[0];
-    TRY(exchange_sync(c, 0, 3, src, c->L[0].ghost[0], s));
+    if (!L.ghost[0]) TRY(dalloc(c, &L.ghost[0], (size_t)c->n_ghost * 3 * L.n * L.n * L.n));
+    a.ghost = L.ghost[0];
+    TRY(exchange_sync(c, l, 3, src, L.ghost[0], s));
   }
-  cudaError_t e = launch_penalty(c->L[0].n, c->geo, a, false, s);
-  if (e == cudaErrorNotSupported) return dgvv_fail(DGVV_EUNSUPPORTED, "penalty kernel not built for degree %d", c->L[0].k);
+  cudaError_t e = launch_penalty(L.n, c->geo, a, false, s);
+  if (e == cudaErrorNotSupported) return dgvv_fail(DGVV_EUNSUPPORTED, "penalty kernel not built for degree %d", L.k);
   if (e != cudaSuccess) return dgvv_fail(DGVV_ECUDA, "penalty kernel: %s", cudaGetErrorString(e));
   return DGVV_OK;
 }
 
-static dgvv_status ensure_dinv_pen(dgvv_ctx* c, cudaStream_t s) {
-  if (c->dinv_pen && c->dinv_pen_ok) return DGVV_OK;
-  if (!c->dinv_pen) TRY(dalloc(c, &c->dinv_pen, (size_t)3 * level_dofs(c, 0)));
-  PenaltyArgs a = penalty_args(c);
-  a.dst = c->dinv_pen;
-  cudaError_t e = launch_penalty(c->L[0].n, c->geo, a, true, s);
+static dgvv_status ensure_dinv_pen(dgvv_ctx* c, int l, cudaStream_t s) {
+  Level& L = c->L[l];
+  if (L.dinv_pen && L.dinv_pen_ok) return DGVV_OK;
+  if (!L.dinv_pen) TRY(dalloc(c, &L.dinv_pen, (size_t)3 * level_dofs(c, l)));
+  PenaltyArgs a = penalty_args(c, l);
+  a.dst = L.dinv_pen;
+  cudaError_t e = launch_penalty(L.n, c->geo, a, true, s);
   if (e != cudaSuccess) return dgvv_fail(DGVV_ECUDA, "penalty diagonal: %s", cudaGetErrorString(e));
-  c->dinv_pen_ok = true;
+  L.dinv_pen_ok = true;
+  return DGVV_OK;
+}
+
+// Chebyshev-Jacobi smoother of SURVEY §8(c) c1.6 for the penalty operator on level l:
+// r = b - A x by the penalty kernel, then d = c_rho d + c_r D^-1 r, x += d (cheb_vec kernel).
+// work holds 2 N doubles (r | d).
+static dgvv_status cheb_pen(dgvv_ctx* c, int l, double* x, const double* b, int degree, double lo, double hi,
+                            int x_is_zero, double* work, cudaStream_t s) {
+  const long N = 3L * level_dofs(c, l);
+  TRY(ensure_dinv_pen(c, l, s));
+  const double* dinv = c->L[l].dinv_pen;
+  const double theta = 0.5 * (hi + lo), delta = 0.5 * (hi - lo), sigma = theta / delta;
+  double rho = 1.0 / sigma;
+  double *r = work, *d = work + N;
+  if (x_is_zero) {
+    DGVV_CUDA_TRY(launch_cheb_first(b, dinv, 1.0 / theta, d, x, N, s));
+  } else {
+    TRY(apply_penalty_impl(c, l, x, r, s));
+    DGVV_CUDA_TRY(launch_axpby(1.0, b, -1.0, r, N, s));          // r = b - A x
+    DGVV_CUDA_TRY(launch_cheb_vec(r, dinv, 0.0, 1.0 / theta, d, x, N, s));
+  }
+  for (int j = 1; j < degree; ++j) {
+    const double rho_new = 1.0 / (2.0 * sigma - rho);
+    TRY(apply_penalty_impl(c, l, x, r, s));
+    DGVV_CUDA_TRY(launch_axpby(1.0, b, -1.0, r, N, s));
+    DGVV_CUDA_TRY(launch_cheb_vec(r, dinv, rho_new * rho, 2.0 * rho_new / delta, d, x, N, s));
+    rho = rho_new;
+  }
+  return DGVV_OK;
+}
+
+static dgvv_status ensure_pen_scratch(dgvv_ctx* c) {
+  for (size_t l = 0; l < c->L.size(); ++l) {
+    auto& S = c->L[l].scratch_pen;
+    if (!S.empty()) continue;
+    const size_t Nl = 3 * (size_t)level_dofs(c, (int)l);
+    S.resize(5, nullptr);
+    TRY(dalloc(c, &S[0], Nl));
+    TRY(dalloc(c, &S[1], 2 * Nl));
+    if (l > 0) { TRY(dalloc(c, &S[3], Nl)); TRY(dalloc(c, &S[4], Nl)); }
+  }
+  return DGVV_OK;
+}
+
+// f2 ("a multigrid preconditioner is necessary for the penalty step"): the
+// V-cycle of SURVEY §8(c) c1.7 over the context's p-levels for the penalty operator — Chebyshev(5)
+// pre/post smoothing, residual, p-restriction R = P^T, recursion, prolongation; coarsest level
+// Chebyshev(5) from zero (G15).  h-levels / the c-level of the viscous hierarchy are not used.
+static dgvv_status vcycle_pen_rec(dgvv_ctx* c, int l, const double* b, double* x, const double* his,
+                                  cudaStream_t s) {
+  auto& S = c->L[l].scratch_pen;
+  const int last = (int)c->L.size() - 1;
+  const long N = 3L * level_dofs(c, l);
+  const double hi = his[l], lo = hi / 20.0;
+  TRY(cheb_pen(c, l, x, b, 5, lo, hi, 1, S[1], s));
+  if (l == last) return DGVV_OK;
+  TRY(apply_penalty_impl(c, l, x, S[0], s));
+  DGVV_CUDA_TRY(launch_axpby(1.0, b, -1.0, S[0], N, s));         // r = b - A x
+  auto& C = c->L[l + 1].scratch_pen;
+  TRY(transfer(c, DGVV_OP_VISCOUS, l, S[0], C[3], 0.0, false, s));
+  TRY(vcycle_pen_rec(c, l + 1, C[3], C[4], his, s));
+  TRY(transfer(c, DGVV_OP_VISCOUS, l, C[4], x, 1.0, true, s));
+  TRY(cheb_pen(c, l, x, b, 5, lo, hi, 0, S[1], s));
   return DGVV_OK;
 }
 
@@ -1534,7 +1614,7 @@ dgvv_status dgvv_set_penalty_parameters(dgvv_ctx* c, const double* tau_div, cons
   if (!c->d_tau_cont) TRY(dalloc(c, &c->d_tau_cont, (size_t)nt));
   DGVV_CUDA_TRY(cudaMemcpy(c->d_tau_div, td.data(), nt * sizeof(double), cudaMemcpyHostToDevice));
   DGVV_CUDA_TRY(cudaMemcpy(c->d_tau_cont, tc.data(), nt * sizeof(double), cudaMemcpyHostToDevice));
-  c->dinv_pen_ok = false;
+  for (auto& L : c->L) L.dinv_pen_ok = false;   // recomputed lazily in the same buffers
   c->has_pen = true;
   return DGVV_OK;
 }
@@ -1543,7 +1623,16 @@ dgvv_status dgvv_apply_penalty(dgvv_ctx* c, const double* src, double* dst, dgvv
   if (!c || !src || !dst) return dgvv_fail(DGVV_EINVAL, "null argument");
   if (src == dst) return dgvv_fail(DGVV_EINVAL, "src and dst alias");
   TRY(op_ready(c, DGVV_OP_PENALTY));
-  return apply_penalty_impl(c, src, dst, (cudaStream_t)stream);
+  return apply_penalty_impl(c, 0, src, dst, (cudaStream_t)stream);
+}
+
+dgvv_status dgvv_apply_penalty_level(dgvv_ctx* c, int32_t level, const double* src, double* dst,
+                                     dgvv_stream stream) {
+  TRY(check_level(c, level));
+  if (!src || !dst) return dgvv_fail(DGVV_EINVAL, "null argument");
+  if (src == dst) return dgvv_fail(DGVV_EINVAL, "src and dst alias");
+  TRY(op_ready(c, DGVV_OP_PENALTY));
+  return apply_penalty_impl(c, level, src, dst, (cudaStream_t)stream);
 }
 
 dgvv_status dgvv_cg_solve(dgvv_ctx* c, int32_t op, const double* b, double* x, double rtol, int32_t maxit,
@@ -1559,19 +1648,19 @@ dgvv_status dgvv_cg_solve(dgvv_ctx* c, int32_t op, const double* b, double* x, d
     return dgvv_fail(DGVV_EINVAL, "V-cycle preconditioner needs lambda_hi_per_level");
   cudaStream_t s = (cudaStream_t)stream;
   const bool pen = op == DGVV_OP_PENALTY;
-  if (pen && (precond == DGVV_PRECOND_VCYCLE || precond == DGVV_PRECOND_VCYCLE_FP32))
-    return dgvv_fail(DGVV_EUNSUPPORTED, "penalty operator: no multigrid hierarchy (use none or Jacobi)");
+  if (pen && precond == DGVV_PRECOND_VCYCLE_FP32)
+    return dgvv_fail(DGVV_EUNSUPPORTED, "penalty operator: FP64 V-cycle, Jacobi or none");
   const int oi = op == DGVV_OP_VISCOUS ? 0 : 1;
   const int nc = op == DGVV_OP_POISSON ? 1 : 3;
   const long N = (long)nc * level_dofs(c, 0);
   auto& W = c->cg_work[pen ? 2 : oi];
   if (!W) TRY(dalloc(c, &W, (size_t)4 * N));
   double *r = W, *z = W + N, *pv = W + 2 * N, *q = W + 3 * N;
-  if (precond == DGVV_PRECOND_JACOBI) TRY(pen ? ensure_dinv_pen(c, s) : ensure_dinv(c, op, 0, s));
-  if (precond == DGVV_PRECOND_VCYCLE) TRY(ensure_vcycle_scratch(c, op));
+  if (precond == DGVV_PRECOND_JACOBI) TRY(pen ? ensure_dinv_pen(c, 0, s) : ensure_dinv(c, op, 0, s));
+  if (precond == DGVV_PRECOND_VCYCLE) TRY(pen ? ensure_pen_scratch(c) : ensure_vcycle_scratch(c, op));
   auto apply_A = [&](const double* src, double* dst, const double* rhs) -> dgvv_status {
     if (pen) {
-      TRY(apply_penalty_impl(c, src, dst, s));
+      TRY(apply_penalty_impl(c, 0, src, dst, s));
       if (rhs) DGVV_CUDA_TRY(launch_axpby(1.0, rhs, -1.0, dst, N, s));   // dst = rhs - A src
       return DGVV_OK;
     }
@@ -1582,9 +1671,9 @@ dgvv_status dgvv_cg_solve(dgvv_ctx* c, int32_t op, const double* b, double* x, d
   };
   auto prec = [&](const double* rr, double* zz) -> dgvv_status {
     if (precond == DGVV_PRECOND_JACOBI) {
-      DGVV_CUDA_TRY(launch_ew_mul(pen ? c->dinv_pen : c->L[0].dinv[oi], rr, zz, N, s));
+      DGVV_CUDA_TRY(launch_ew_mul(pen ? c->L[0].dinv_pen : c->L[0].dinv[oi], rr, zz, N, s));
     } else if (precond == DGVV_PRECOND_VCYCLE) {
-      TRY(vcycle_rec(c, op, 0, rr, zz, lambda_hi_per_level, s));
+      TRY(pen ? vcycle_pen_rec(c, 0, rr, zz, lambda_hi_per_level, s) : vcycle_rec(c, op, 0, rr, zz, lambda_hi_per_level, s));
     } else if (precond == DGVV_PRECOND_VCYCLE_FP32) {
       TRY(vcycle_fp32_d(c, op, rr, zz, lambda_hi_per_level, s));
     } else {
@@ -2278,10 +2367,14 @@ dgvv_status dgvv_estimate_lambda_max(dgvv_ctx* c, int32_t op, int32_t level, int
   if (cgl && op != DGVV_OP_VISCOUS && op != DGVV_OP_POISSON) return dgvv_fail(DGVV_EINVAL, "unknown op %d", op);
   if (!v0 || !out || steps < 1) return dgvv_fail(DGVV_EINVAL, "bad argument");
   cudaStream_t s = (cudaStream_t)stream;
-  const int nc = op == DGVV_OP_VISCOUS ? 3 : 1;
+  const bool pen = op == DGVV_OP_PENALTY;
+  const int nc = op == DGVV_OP_POISSON ? 1 : 3;
   const long N = cgl ? (long)nc * c->cg.nv : (long)nc * level_dofs(c, level);
   const double* dinv;
-  if (cgl) {
+  if (pen) {
+    TRY(ensure_dinv_pen(c, level, s));
+    dinv = c->L[level].dinv_pen;
+  } else if (cgl) {
     TRY(ensure_vcycle_scratch(c, op));
     TRY(cg_ensure_dinv(c, op, s));
     dinv = c->cg.dinv[op == DGVV_OP_VISCOUS ? 0 : 1];
@@ -2291,6 +2384,7 @@ dgvv_status dgvv_estimate_lambda_max(dgvv_ctx* c, int32_t op, int32_t level, int
   }
   auto apply_op = [&](const double* src, double* dst) -> dgvv_status {
     if (cgl) return cg_apply(c, op, src, dst, s);
+    if (pen) return apply_penalty_impl(c, level, src, dst, s);
     ApplyArgs a = base_args(c, level, op);
     a.src = src; a.dst = dst;
     return run_apply(c, op, level, a, s);

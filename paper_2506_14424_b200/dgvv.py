@@ -217,9 +217,13 @@ class Context:
         A.check(self._L.dgvv_set_penalty_parameters(self.h, td.ctypes.data_as(C.POINTER(C.c_double)),
                                                     tc.ctypes.data_as(C.POINTER(C.c_double))))
 
-    def apply_penalty(self, src, dst):
-        n = 3 * self.n_dofs(0)
-        A.check(self._L.dgvv_apply_penalty(self.h, _ptr(src, n, "src"), _ptr(dst, n, "dst"), _stream()))
+    def apply_penalty(self, src, dst, level=0):
+        n = 3 * self.n_dofs(level)
+        if level == 0:
+            A.check(self._L.dgvv_apply_penalty(self.h, _ptr(src, n, "src"), _ptr(dst, n, "dst"), _stream()))
+        else:
+            A.check(self._L.dgvv_apply_penalty_level(self.h, level, _ptr(src, n, "src"), _ptr(dst, n, "dst"),
+                                                     _stream()))
         return dst
 
     def set_transport(self, w):

@@ -223,6 +223,21 @@ def run_f2(reps):
         ms = e0.elapsed_time(e1)
         report(name + "+f2", "penalty_pcg_jacobi", ms, N, None, None,
                f"{it} iterations to rtol 1e-10 (relres {rr:.2e}); {ms / max(it, 1):.3f} ms/iteration")
+        # f2 multigrid: V-cycle-PCG over the p-levels k -> 2 -> 1
+        degs = [k, 2, 1]
+        cm = Context(m, k, visc_law=C2_LAW, degrees=degs)
+        cm.set_penalty_parameters(speed * h * 1e-3, speed * 1e-3)
+        t_l, lams = _timed(lambda: [1.2 * cm.estimate_lambda_max(A.OP_PENALTY, dev(uniform(2, 3 * cm.n_dofs(l))),
+                                                                 level=l, steps=20) for l in range(3)])
+        x = torch.zeros_like(src)
+        cm.cg_solve(A.OP_PENALTY, src, x, rtol=1e-10, maxit=500, precond="vcycle", lam_hi_per_level=lams)
+        x.zero_()
+        ms, (it, rr) = _timed(lambda: cm.cg_solve(A.OP_PENALTY, src, x, rtol=1e-10, maxit=500, precond="vcycle",
+                                                  lam_hi_per_level=lams))
+        report(name + "+f2", "penalty_pcg_vcycle", ms, N, None, None,
+               f"{it} iterations to rtol 1e-10 (relres {rr:.2e}); {ms / max(it, 1):.3f} ms/iteration; "
+               f"p-levels {degs}; lambda setup (20 Lanczos steps per level) {t_l:.1f} ms")
+        del cm
 
 
 F4_NU = {"kind": "const", "value": 1.0e-3}      # convection-dominated viscous step (high Re)
