@@ -10,7 +10,7 @@ cudaError_t upload_tables_visc(const Tab1D* tabs) { return tu_upload_tables(tabs
 // cells per CTA and min resident CTAs per SM (register cap), chosen by measurement (DESIGN.md
 // §11): n = 4 general geometry (C2) 2 cells x 8 CTAs (smem-bound by the TMA face stage; 4 x 4:
 // +2 %);
-// n = 4 Cartesian (C5) 4 x 8 (8 x 4: +2 %, 2 x 16: +3 %); n = 5 Cartesian (C3) 5 x 3 (125 threads: 98 % lane use).
+// n = 4 Cartesian (C5) 4 x 6 (r02; r01: 4 x 8, 8 x 4: +2 %, 2 x 16: +3 %); n = 5 Cartesian (C3) 5 x 3 (125 threads: 98 % lane use).
 #ifndef CPB4G
 #define CPB4G 2
 #endif
@@ -21,7 +21,7 @@ cudaError_t upload_tables_visc(const Tab1D* tabs) { return tu_upload_tables(tabs
 #define CPB4 4
 #endif
 #ifndef MINB4
-#define MINB4 8
+#define MINB4 6   // with the 2x2 lane-quad swizzle and early coefficient loads (r02): 6 > 7 = 8 (C5 2848 / 2897 / 2897 us)
 #endif
 #ifndef CPB5
 #define CPB5 5

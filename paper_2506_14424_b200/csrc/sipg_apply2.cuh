@@ -31,6 +31,12 @@
 #ifndef USE_ST
 #define USE_ST 0          // keep a transposed [c][z][x][y] copy of the cell (16-byte y-lines)
 #endif
+#ifndef DGVV_NU_EARLY
+#define DGVV_NU_EARLY 1       // Cartesian: load the column's cell-point coefficients with the column
+#endif
+#ifndef DGVV_QUAD_SWIZZLE
+#define DGVV_QUAD_SWIZZLE 1   // n = 4: lane quads cover 2 x 2 blocks of columns (see the kernel)
+#endif
 
 // diagnostics only (upper bounds of what recomputing the metric could gain):
 // read every cell's volume / face metric from cell 0 (L1/L2-resident) instead of its own
@@ -161,8 +167,16 @@ sipg_apply2_kernel(const ApplyArgsT<R> A) {
   const Tab1D& T = c_tab[n];
 
   const int lc = threadIdx.x / n2;
-  const int p = threadIdx.x - lc * n2;
-  const int a = p % n, b = p / n;
+  const int pr = threadIdx.x - lc * n2;
+  // Lane -> column (a, b).  Shared-memory cost on B200 (measured, scripts/lds_patterns.cu, DESIGN.md
+  // §6): a 64-bit load costs one wavefront per 128 B of distinct data summed over the warp's lane
+  // quads (4 consecutive lanes share one read port), a 128-bit load at least two.  With a fastest
+  // (p = a + n b) a quad shares its row (x-direction loads: 1 wavefront) but reads 4 different
+  // columns (y-direction loads: 2).  For n = 4 the quad covers a 2 x 2 block of (a, b) instead:
+  // 2 distinct rows and 2 distinct columns per quad, one wavefront per 64-bit load either way.
+  const int a = (n == 4 && DGVV_QUAD_SWIZZLE) ? ((pr & 1) | ((pr >> 1) & 2)) : pr % n;
+  const int b = (n == 4 && DGVV_QUAD_SWIZZLE) ? (((pr >> 1) & 1) | ((pr >> 2) & 2)) : pr / n;
+  const int p = a + n * b;                          // the column's point index in the cell block
   const int slot_raw = blockIdx.x * CPB + lc;
   const bool active = slot_raw < A.n_proc;
   const int slot = active ? slot_raw : (A.n_proc - 1);
@@ -229,6 +243,13 @@ sipg_apply2_kernel(const ApplyArgsT<R> A) {
         if (USE_ST) sT[c * CST + z * PS + a * RS + b] = v;
       }
   }
+  // the cell-point coefficient of the column, loaded with the column (its latency overlaps the
+  // column loads instead of stalling the volume term)
+  R nuq[(GEO == 0 && DGVV_NU_EARLY) ? n : 1];
+  if constexpr (GEO == 0 && DGVV_NU_EARLY) {
+#pragma unroll
+    for (int z = 0; z < n; ++z) nuq[z] = A.nu_cell[(size_t)cell * n3 + z * n2 + p];
+  }
   R ih[3] = {0, 0, 0}, vol = R(0.0), Hm;
   if constexpr (GEO == 0) {
     const R* cg = A.cart + (size_t)cell * CART_STRIDE;
@@ -277,7 +298,8 @@ sipg_apply2_kernel(const ApplyArgsT<R> A) {
       }
       R Ji[9], w;
       if constexpr (GEO == 0) {
-        w = A.nu_cell[(size_t)DIAG_VC(cell) * n3 + q] * wab * R(T.w[z]) * vol;
+        if constexpr (DGVV_NU_EARLY) w = nuq[z] * wab * R(T.w[z]) * vol;
+        else w = A.nu_cell[(size_t)DIAG_VC(cell) * n3 + q] * wab * R(T.w[z]) * vol;
       } else {
         const R* vm = A.vJi + (size_t)DIAG_VC(cell) * 9 * n3 + q;
 #pragma unroll
