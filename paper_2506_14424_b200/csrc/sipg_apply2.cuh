@@ -38,18 +38,6 @@
 #define DGVV_QUAD_SWIZZLE 1   // n = 4: lane quads cover 2 x 2 blocks of columns (see the kernel)
 #endif
 
-// diagnostics only (upper bounds of what recomputing the metric could gain):
-// read every cell's volume / face metric from cell 0 (L1/L2-resident) instead of its own
-#ifdef DGVV_DIAG_NOVMETRIC
-#define DIAG_VC(c) 0
-#else
-#define DIAG_VC(c) (c)
-#endif
-#ifdef DGVV_DIAG_NOFMETRIC
-#define DIAG_FC(c) 0
-#else
-#define DIAG_FC(c) (c)
-#endif
 
 namespace dgvv {
 
@@ -270,7 +258,6 @@ sipg_apply2_kernel(const ApplyArgsT<R> A) {
   __syncthreads();
 
   // =============================================================== volume term
-#ifndef DGVV_DIAG_NOVOL
   {
     R Da[n], Db[n];
     ld_row<n>(sD + a * RS, Da);
@@ -299,12 +286,12 @@ sipg_apply2_kernel(const ApplyArgsT<R> A) {
       R Ji[9], w;
       if constexpr (GEO == 0) {
         if constexpr (DGVV_NU_EARLY) w = nuq[z] * wab * R(T.w[z]) * vol;
-        else w = A.nu_cell[(size_t)DIAG_VC(cell) * n3 + q] * wab * R(T.w[z]) * vol;
+        else w = A.nu_cell[(size_t)cell * n3 + q] * wab * R(T.w[z]) * vol;
       } else {
-        const R* vm = A.vJi + (size_t)DIAG_VC(cell) * 9 * n3 + q;
+        const R* vm = A.vJi + (size_t)cell * 9 * n3 + q;
 #pragma unroll
         for (int r = 0; r < 9; ++r) Ji[r] = __ldg(vm + r * n3);
-        w = A.nu_cell[(size_t)DIAG_VC(cell) * n3 + q];         // nu * JxW
+        w = A.nu_cell[(size_t)cell * n3 + q];         // nu * JxW
       }
       if constexpr (CONV) {
         // f4 (fused): + alpha_c JxW (w.grad) u at the point (collocation: the test function is the
@@ -355,9 +342,7 @@ sipg_apply2_kernel(const ApplyArgsT<R> A) {
     __syncthreads();
   }
 
-#endif
   // =============================================================== face terms
-#ifndef DGVV_DIAG_NOFACE
   // Faces in opposite pairs (-d,+d): one pass over each normal line gives the own traces of
   // both faces; the traces of both faces go to smem together (one barrier), then the
   // tangential coefficients of both (second barrier).  Order z, x, y: the z pair works on the
@@ -396,20 +381,10 @@ sipg_apply2_kernel(const ApplyArgsT<R> A) {
         const double* lO = s ? T.l0 : T.l1;
         const double* dO = s ? T.d0 : T.d1;
         const int sl = lc + (nbv - cell);
-#if defined(DGVV_DIAG_LOCALNB)
-        // diagnostic only (wrong values): y (and z if DGVV_DIAG_LOCALNB > 1) neighbours read from this
-        // cell's own smem copy -- the upper bound of what cluster/DSMEM staging could gain
-        const bool in_cta = (d == 1 || (d == 2 && DGVV_DIAG_LOCALNB > 1)) ? true : (sl >= 0 && sl < CPB && sid[sl] == nbv);
-#else
         const bool in_cta = sl >= 0 && sl < CPB && sid[sl] == nbv;
-#endif
         const R* pn = nbv < A.n_owned ? A.src + (size_t)nbv * NC * n3
                                            : A.ghost + (size_t)(nbv - A.n_owned) * NC * n3;
-#if defined(DGVV_DIAG_LOCALNB)
-        const R* ns = smem + ((in_cta && d == 0) ? sl : lc) * Cf::CS;
-#else
         const R* ns = smem + (in_cta ? sl : 0) * Cf::CS;
-#endif
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
           R x[n];
@@ -484,16 +459,16 @@ sipg_apply2_kernel(const ApplyArgsT<R> A) {
           Hp = A.Hcell[nbv];
         }
       } else if constexpr (GEO == 1) {
-        const R* fm = A.fJi + ((size_t)DIAG_FC(cell) * 6 + f) * 9 * n2 + p;
+        const R* fm = A.fJi + ((size_t)cell * 6 + f) * 9 * n2 + p;
 #pragma unroll
         for (int r = 0; r < 9; ++r) Jim[r] = __ldg(fm + r * n2);
-        wm = A.nu_face[((size_t)DIAG_FC(cell) * 6 + f) * n2 + p];      // nu * dA
+        wm = A.nu_face[((size_t)cell * 6 + f) * n2 + p];      // nu * dA
         wp = wm;
         if (inter) {
-          const R* fp = A.fJi + ((size_t)DIAG_FC(nbv) * 6 + (f ^ 1)) * 9 * n2 + p;
+          const R* fp = A.fJi + ((size_t)nbv * 6 + (f ^ 1)) * 9 * n2 + p;
 #pragma unroll
           for (int r = 0; r < 9; ++r) Jip[r] = __ldg(fp + r * n2);
-          wp = A.nu_face[((size_t)DIAG_FC(nbv) * 6 + (f ^ 1)) * n2 + p];
+          wp = A.nu_face[((size_t)nbv * 6 + (f ^ 1)) * n2 + p];
           Hp = A.Hcell[nbv];
         }
       }
@@ -531,7 +506,7 @@ sipg_apply2_kernel(const ApplyArgsT<R> A) {
           if (dd == 0 && s == 0) mbar_wait(&mbar[lc], 0);
           num = stg[f * n2 + p];
         } else {
-          num = A.nu_face[((size_t)DIAG_FC(cell) * 6 + f) * n2 + p];
+          num = A.nu_face[((size_t)cell * 6 + f) * n2 + p];
         }
         nup = num;
         R ihp[3] = {ih[0], ih[1], ih[2]};
@@ -539,7 +514,7 @@ sipg_apply2_kernel(const ApplyArgsT<R> A) {
           const R* cg = A.cart + (size_t)nbv * CART_STRIDE;
           ihp[0] = cg[0]; ihp[1] = cg[1]; ihp[2] = cg[2]; Hp = cg[3];
           if constexpr (Cf::TMAC) nup = stg[(6 + f) * n2 + p];
-          else nup = A.nu_face[((size_t)DIAG_FC(nbv) * 6 + (f ^ 1)) * n2 + p];
+          else nup = A.nu_face[((size_t)nbv * 6 + (f ^ 1)) * n2 + p];
         }
         const R dA = R(T.w[a]) * R(T.w[b]) * vol * ih[d];
         const R tau = R(A.pen) * fmax(Hm, Hp) * R(0.5) * (num + nup);
@@ -709,7 +684,6 @@ sipg_apply2_kernel(const ApplyArgsT<R> A) {
     }
   }
 
-#endif
   // =============================================================== epilogue
   if constexpr (MASS) {                 // Helmholtz mass term: + mass * JxW * u (diagonal M)
 #pragma unroll
