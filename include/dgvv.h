@@ -226,8 +226,9 @@ dgvv_status dgvv_inverse_diagonal(dgvv_ctx* ctx, int32_t op, int32_t level, doub
  * coefficients, inverse diagonals) in single precision — the paper's choice for the
  * preconditioner; b and x are FP64 and converted at
  * entry and exit.  Same algorithm as dgvv_vcycle; FP32 mirrors of the level data are built on
- * first use and refreshed after dgvv_update_viscosity / dgvv_set_mass.  Single-GPU contexts
- * only in this build (DGVV_EUNSUPPORTED with ghosts). */
+ * first use and refreshed after dgvv_update_viscosity / dgvv_set_mass.  Multi-rank: every FP32
+ * apply exchanges its ghost cells in single precision (half the bytes of the FP64 exchange),
+ * overlapped with the interior cells; collective (all ranks call it).  Not with the c-level. */
 dgvv_status dgvv_vcycle_fp32(dgvv_ctx* ctx, int32_t op, const double* b, double* x,
                              const double* lambda_hi_per_level, dgvv_stream stream);
 
@@ -360,6 +361,18 @@ dgvv_status dgvv_ghost_buffer(dgvv_ctx* ctx, int32_t level, int32_t kind, double
 dgvv_status dgvv_nccl_get_unique_id(char out_id[128]);
 dgvv_status dgvv_nccl_comm_init(const char id[128], int32_t nranks, int32_t rank, void** comm);
 dgvv_status dgvv_nccl_comm_destroy(void* comm);
+
+/* In-process communicator for R ranks driven by R host threads in ONE process (one GPU is
+ * enough): dgvv_thread_group_create makes the group, dgvv_thread_group_comm returns rank r's
+ * communicator, to be passed as dgvv_options.nccl_comm exactly like an NCCL one.  Every
+ * collective of the library (setup handshake, ghost exchange, allreduced dots) then runs as
+ * device-to-device copies / a rank-ordered sum on the ranks' own streams, ordered by CUDA events
+ * recorded before a host barrier: no kernel waits on another rank's kernel.  Each rank must run
+ * on its own (non-legacy) stream and every rank must make the same sequence of collective calls
+ * (as with NCCL).  The group owns the per-rank communicators; destroy it after the contexts. */
+dgvv_status dgvv_thread_group_create(int32_t nranks, void** group);
+dgvv_status dgvv_thread_group_comm(void* group, int32_t rank, void** comm);
+dgvv_status dgvv_thread_group_destroy(void* group);
 
 const char* dgvv_last_error(void);   /* thread-local message of the last failure          */
 const char* dgvv_version(void);

@@ -89,6 +89,9 @@ _SIGS = {
     "dgvv_nccl_get_unique_id": [C.c_char_p],
     "dgvv_nccl_comm_init": [C.c_char_p, I32, I32, C.POINTER(VP)],
     "dgvv_nccl_comm_destroy": [VP],
+    "dgvv_thread_group_create": [I32, C.POINTER(VP)],
+    "dgvv_thread_group_comm": [VP, I32, C.POINTER(VP)],
+    "dgvv_thread_group_destroy": [VP],
 }
 
 

@@ -10,6 +10,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <condition_variable>
 #include <mutex>
 #include <string>
 #include <unordered_map>
@@ -86,6 +87,48 @@ dgvv_status nccl_load() {
     if (r_ != ncclSuccess) return dgvv_fail(DGVV_ENCCL, "%s: %s", #expr, g_nccl.errStr(r_)); \
   } while (0)
 
+// ------------------------------------------------------------------ communicators
+// A dgvv communicator (the void* of dgvv_options.nccl_comm) is either an NCCL communicator (one
+// process per GPU, the production transport) or one rank of an in-process thread group: R host
+// threads, each driving its own context and CUDA stream, exchanging through device-to-device copies
+// ordered by CUDA events (no kernel ever waits on another rank's kernel: the dependencies are
+// stream/event edges recorded before a host barrier).  The thread group runs the whole multi-rank
+// library path — grouped ghost exchange overlapped with the interior cells, allreduced dots,
+// multi-rank V-cycles and Krylov solvers — on one GPU, so it can be tested where NCCL cannot run
+// (NCCL refuses two ranks on one device).
+enum { COMM_NCCL = 1, COMM_THREADS = 2 };
+struct ThreadGroup;
+struct DgvvComm {
+  int kind = 0;
+  ncclComm_t nccl = nullptr;
+  ThreadGroup* tg = nullptr;
+  int rank = 0;
+};
+struct ThreadGroup {
+  int R = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  unsigned long gen = 0;
+  std::vector<std::vector<const void*>> sptr;   // [from][to] send segment
+  std::vector<std::vector<size_t>> sbytes;
+  std::vector<cudaEvent_t> ev_a, ev_b;          // per rank events of the current collective
+  std::vector<const double*> red;               // per rank allreduce staging
+  std::vector<long long> hval;                  // per rank host values
+  std::vector<DgvvComm> comms;
+};
+void tg_barrier(ThreadGroup* g) {
+  std::unique_lock<std::mutex> lk(g->mu);
+  const unsigned long my = g->gen;
+  if (++g->arrived == g->R) {
+    g->arrived = 0;
+    ++g->gen;
+    g->cv.notify_all();
+  } else {
+    g->cv.wait(lk, [&] { return g->gen != my; });
+  }
+}
+
 // ------------------------------------------------------------------ tables
 // each TU's __constant__ tables live per device: uploaded once per DEVICE, not once
 // per process — a context created later on another device would otherwise read zero tables
@@ -149,6 +192,7 @@ struct LevelF {
   float* fJi = nullptr;
   float* Hc = nullptr;
   float* jxw = nullptr;
+  float* ghost[2] = {nullptr, nullptr};     // FP32 ghost cells per op (multi-rank)
   std::vector<float*> scratch[2];           // [0] r, [1] work (2N), [3] b, [4] x
 };
 
@@ -234,8 +278,10 @@ struct dgvv_ctx {
   const double* ulin = nullptr;
   // comm: peers exist whenever there are ghosts; NCCL transport only with a communicator
   // (without one the caller fills the ghost buffers: external-exchange mode, used by tests)
-  void* comm = nullptr;
+  void* comm = nullptr;                      // DgvvComm*
   std::vector<Peer> peers;
+  double* tg_red = nullptr;                  // thread group: allreduce staging (8 doubles)
+  cudaEvent_t ev_red = nullptr, ev_red2 = nullptr;
   double* d_sendbuf = nullptr;
   size_t sendbuf_len = 0;
   cudaStream_t comm_stream = nullptr;
@@ -334,24 +380,127 @@ dgvv_status pack(dgvv_ctx* c, int l, int nc, const double* src, double* sendbuf,
 // ghost exchange of a level vector (NC components): pack on s, grouped ncclSend/ncclRecv on
 // the comm stream into `ghost`; ev_comm marks completion (the caller's stream must wait on it
 // before reading ghosts).  No-op without ghosts or without a communicator.
+// grouped point-to-point exchange of packed cells (len elements of esz bytes per cell) with every
+// peer, on the comm stream after ev_pack; ev_comm marks completion
+dgvv_status comm_sendrecv(dgvv_ctx* c, const void* sendbuf, void* ghost, int len, size_t esz, cudaStream_t s) {
+  DgvvComm* cm = (DgvvComm*)c->comm;
+  DGVV_CUDA_TRY(cudaEventRecord(c->ev_pack, s));
+  if (cm->kind == COMM_NCCL) {
+    DGVV_CUDA_TRY(cudaStreamWaitEvent(c->comm_stream, c->ev_pack, 0));
+    const ncclDataType_t dt = esz == 8 ? ncclDouble : ncclFloat;
+    NCCL_TRY(g_nccl.groupStart());
+    size_t off = 0;
+    for (auto& P : c->peers) {
+      if (P.n_send) NCCL_TRY(g_nccl.send((const char*)sendbuf + off * esz, (size_t)P.n_send * len, dt, P.rank, cm->nccl, c->comm_stream));
+      if (P.n_recv) NCCL_TRY(g_nccl.recv((char*)ghost + (size_t)P.recv_off * len * esz, (size_t)P.n_recv * len, dt, P.rank, cm->nccl, c->comm_stream));
+      off += (size_t)P.n_send * len;
+    }
+    NCCL_TRY(g_nccl.groupEnd());
+    DGVV_CUDA_TRY(cudaEventRecord(c->ev_comm, c->comm_stream));
+    return DGVV_OK;
+  }
+  ThreadGroup* g = cm->tg;
+  const int r = cm->rank;
+  {
+    std::lock_guard<std::mutex> lk(g->mu);
+    size_t off = 0;
+    for (int q = 0; q < g->R; ++q) { g->sptr[r][q] = nullptr; g->sbytes[r][q] = 0; }
+    for (auto& P : c->peers) {
+      g->sptr[r][P.rank] = (const char*)sendbuf + off * esz;
+      g->sbytes[r][P.rank] = (size_t)P.n_send * len * esz;
+      off += (size_t)P.n_send * len;
+    }
+    g->ev_a[r] = c->ev_pack;
+  }
+  tg_barrier(g);
+  // our ghost buffer is rewritten only after our own earlier kernels that read it (ordered before
+  // ev_pack on s), and after each peer has packed
+  DGVV_CUDA_TRY(cudaStreamWaitEvent(c->comm_stream, c->ev_pack, 0));
+  for (auto& P : c->peers) {
+    const size_t want = (size_t)P.n_recv * len * esz;
+    if (g->sbytes[P.rank][r] != want)
+      return dgvv_fail(DGVV_EINVAL, "thread group: rank %d sends %zu bytes, rank %d expects %zu", P.rank, g->sbytes[P.rank][r], r, want);
+    if (!want) continue;
+    DGVV_CUDA_TRY(cudaStreamWaitEvent(c->comm_stream, g->ev_a[P.rank], 0));
+    DGVV_CUDA_TRY(cudaMemcpyAsync((char*)ghost + (size_t)P.recv_off * len * esz, g->sptr[P.rank][r], want,
+                                  cudaMemcpyDeviceToDevice, c->comm_stream));
+  }
+  DGVV_CUDA_TRY(cudaEventRecord(c->ev_comm, c->comm_stream));
+  {
+    std::lock_guard<std::mutex> lk(g->mu);
+    g->ev_b[r] = c->ev_comm;
+  }
+  tg_barrier(g);
+  // the peers copy from our send buffer: later work on s (the next pack) waits for their copies
+  for (auto& P : c->peers) DGVV_CUDA_TRY(cudaStreamWaitEvent(s, g->ev_b[P.rank], 0));
+  tg_barrier(g);                               // ev_b is not re-recorded before every rank has waited
+  return DGVV_OK;
+}
+
+// sum-allreduce of `count` doubles in place (device pointer, stream-ordered on s)
+dgvv_status comm_allreduce(dgvv_ctx* c, double* ptr, int count, cudaStream_t s) {
+  DgvvComm* cm = (DgvvComm*)c->comm;
+  if (!cm) return DGVV_OK;
+  if (cm->kind == COMM_NCCL) {
+    NCCL_TRY(g_nccl.allReduce(ptr, ptr, count, ncclDouble, ncclSum, cm->nccl, s));
+    return DGVV_OK;
+  }
+  ThreadGroup* g = cm->tg;
+  const int r = cm->rank;
+  if (count > 8) return dgvv_fail(DGVV_EINVAL, "thread group allreduce: count %d > 8", count);
+  DGVV_CUDA_TRY(cudaMemcpyAsync(c->tg_red, ptr, count * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  DGVV_CUDA_TRY(cudaEventRecord(c->ev_red, s));
+  {
+    std::lock_guard<std::mutex> lk(g->mu);
+    g->red[r] = c->tg_red;
+    g->ev_a[r] = c->ev_red;
+  }
+  tg_barrier(g);
+  for (int q = 0; q < g->R; ++q) DGVV_CUDA_TRY(cudaStreamWaitEvent(s, g->ev_a[q], 0));
+  DGVV_CUDA_TRY(launch_sum_ranks(g->red.data(), g->R, count, ptr, s));   // ranks summed in rank order
+  DGVV_CUDA_TRY(cudaEventRecord(c->ev_red2, s));
+  {
+    std::lock_guard<std::mutex> lk(g->mu);
+    g->ev_b[r] = c->ev_red2;
+  }
+  tg_barrier(g);
+  for (int q = 0; q < g->R; ++q) DGVV_CUDA_TRY(cudaStreamWaitEvent(s, g->ev_b[q], 0));   // staging reusable
+  tg_barrier(g);
+  return DGVV_OK;
+}
+
+// host-side sum over the ranks (setup: global sizes)
+dgvv_status comm_host_sum(dgvv_ctx* c, long long* v, cudaStream_t s) {
+  DgvvComm* cm = (DgvvComm*)c->comm;
+  if (!cm) return DGVV_OK;
+  if (cm->kind == COMM_NCCL) {
+    long long* d = nullptr;
+    TRY(dalloc(c, &d, 1));
+    DGVV_CUDA_TRY(cudaMemcpy(d, v, sizeof(long long), cudaMemcpyHostToDevice));
+    NCCL_TRY(g_nccl.allReduce(d, d, 1, ncclInt64, ncclSum, cm->nccl, s));
+    DGVV_CUDA_TRY(cudaMemcpyAsync(v, d, sizeof(long long), cudaMemcpyDeviceToHost, s));
+    DGVV_CUDA_TRY(cudaStreamSynchronize(s));
+    return DGVV_OK;
+  }
+  ThreadGroup* g = cm->tg;
+  {
+    std::lock_guard<std::mutex> lk(g->mu);
+    g->hval[cm->rank] = *v;
+  }
+  tg_barrier(g);
+  long long t = 0;
+  for (int q = 0; q < g->R; ++q) t += g->hval[q];
+  tg_barrier(g);
+  *v = t;
+  return DGVV_OK;
+}
+
 dgvv_status exchange(dgvv_ctx* c, int l, int nc, const double* src, double* ghost, cudaStream_t s) {
   if (!c->comm || c->peers.empty()) return DGVV_OK;
   const int n = c->L[l].n;
   const int len = nc * n * n * n;
   TRY(pack(c, l, nc, src, c->d_sendbuf, s));
-  DGVV_CUDA_TRY(cudaEventRecord(c->ev_pack, s));
-  DGVV_CUDA_TRY(cudaStreamWaitEvent(c->comm_stream, c->ev_pack, 0));
-  ncclComm_t comm = (ncclComm_t)c->comm;
-  NCCL_TRY(g_nccl.groupStart());
-  size_t off = 0;
-  for (auto& P : c->peers) {
-    if (P.n_send) NCCL_TRY(g_nccl.send(c->d_sendbuf + off, (size_t)P.n_send * len, ncclDouble, P.rank, comm, c->comm_stream));
-    if (P.n_recv) NCCL_TRY(g_nccl.recv(ghost + (size_t)P.recv_off * len, (size_t)P.n_recv * len, ncclDouble, P.rank, comm, c->comm_stream));
-    off += (size_t)P.n_send * len;
-  }
-  NCCL_TRY(g_nccl.groupEnd());
-  DGVV_CUDA_TRY(cudaEventRecord(c->ev_comm, c->comm_stream));
-  return DGVV_OK;
+  return comm_sendrecv(c, c->d_sendbuf, ghost, len, sizeof(double), s);
 }
 
 dgvv_status exchange_sync(dgvv_ctx* c, int l, int nc, const double* src, double* ghost, cudaStream_t s) {
@@ -464,7 +613,7 @@ dgvv_status ensure_dinv(dgvv_ctx* c, int op, int l, cudaStream_t s) {
 dgvv_status dot_dev(dgvv_ctx* c, const double* a, const double* b, long n, double* dout, cudaStream_t s) {
   const int nb = (int)std::max(1L, std::min((long)kPartials, (n + 255) / 256));
   DGVV_CUDA_TRY(launch_dot(a, b, n, c->d_part, nb, dout, s));
-  if (c->comm) NCCL_TRY(g_nccl.allReduce(dout, dout, 1, ncclDouble, ncclSum, (ncclComm_t)c->comm, s));
+  if (c->comm) TRY(comm_allreduce(c, dout, 1, s));
   return DGVV_OK;
 }
 
@@ -547,16 +696,55 @@ dgvv_status dgvv_nccl_comm_init(const char id_bytes[128], int32_t nranks, int32_
   TRY(nccl_load());
   ncclUniqueId id;
   std::memcpy(id.internal, id_bytes, 128);
-  ncclComm_t cm;
-  NCCL_TRY(g_nccl.commInitRank(&cm, nranks, id, rank));
+  ncclComm_t nc;
+  NCCL_TRY(g_nccl.commInitRank(&nc, nranks, id, rank));
+  DgvvComm* cm = new DgvvComm;
+  cm->kind = COMM_NCCL;
+  cm->nccl = nc;
+  cm->rank = rank;
   *comm = (void*)cm;
   return DGVV_OK;
 }
 
 dgvv_status dgvv_nccl_comm_destroy(void* comm) {
   if (!comm) return DGVV_OK;
+  DgvvComm* cm = (DgvvComm*)comm;
+  if (cm->kind != COMM_NCCL) return dgvv_fail(DGVV_EINVAL, "not an NCCL communicator");
   TRY(nccl_load());
-  NCCL_TRY(g_nccl.commDestroy((ncclComm_t)comm));
+  NCCL_TRY(g_nccl.commDestroy(cm->nccl));
+  delete cm;
+  return DGVV_OK;
+}
+
+dgvv_status dgvv_thread_group_create(int32_t nranks, void** group) {
+  if (nranks < 1 || nranks > 64 || !group) return dgvv_fail(DGVV_EINVAL, "thread group: 1 <= nranks <= 64");
+  ThreadGroup* g = new ThreadGroup;
+  g->R = nranks;
+  g->sptr.assign(nranks, std::vector<const void*>(nranks, nullptr));
+  g->sbytes.assign(nranks, std::vector<size_t>(nranks, 0));
+  g->ev_a.assign(nranks, nullptr);
+  g->ev_b.assign(nranks, nullptr);
+  g->red.assign(nranks, nullptr);
+  g->hval.assign(nranks, 0);
+  g->comms.resize(nranks);
+  for (int r = 0; r < nranks; ++r) {
+    g->comms[r].kind = COMM_THREADS;
+    g->comms[r].tg = g;
+    g->comms[r].rank = r;
+  }
+  *group = (void*)g;
+  return DGVV_OK;
+}
+
+dgvv_status dgvv_thread_group_comm(void* group, int32_t rank, void** comm) {
+  ThreadGroup* g = (ThreadGroup*)group;
+  if (!g || !comm || rank < 0 || rank >= g->R) return dgvv_fail(DGVV_EINVAL, "thread group: bad rank %d", rank);
+  *comm = (void*)&g->comms[rank];
+  return DGVV_OK;
+}
+
+dgvv_status dgvv_thread_group_destroy(void* group) {
+  delete (ThreadGroup*)group;
   return DGVV_OK;
 }
 
@@ -573,6 +761,8 @@ void dgvv_destroy(dgvv_ctx* c) {
     if (c->hp.cs[i]) cudaStreamDestroy(c->hp.cs[i]);
   if (c->ev_pack) cudaEventDestroy(c->ev_pack);
   if (c->ev_comm) cudaEventDestroy(c->ev_comm);
+  if (c->ev_red) cudaEventDestroy(c->ev_red);
+  if (c->ev_red2) cudaEventDestroy(c->ev_red2);
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
   delete c;
 }
@@ -810,12 +1000,30 @@ static dgvv_status setup_impl(const dgvv_mesh* m, int32_t degree, const dgvv_law
     DGVV_CUDA_TRY(cudaMemcpy(c->d_boundary, bnd.data(), bnd.size() * sizeof(int), cudaMemcpyHostToDevice));
   }
   if (opt && opt->nccl_comm) {
-    TRY(nccl_load());
+    DgvvComm* cm = (DgvvComm*)opt->nccl_comm;
+    if (cm->kind != COMM_NCCL && cm->kind != COMM_THREADS) return dgvv_fail(DGVV_EINVAL, "not a dgvv communicator");
+    if (cm->kind == COMM_NCCL) TRY(nccl_load());
     c->comm = opt->nccl_comm;
     DGVV_CUDA_TRY(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
     DGVV_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_pack, cudaEventDisableTiming));
     DGVV_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_comm, cudaEventDisableTiming));
-    if (!c->peers.empty()) {
+    DGVV_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_red, cudaEventDisableTiming));
+    DGVV_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_red2, cudaEventDisableTiming));
+    TRY(dalloc(c, &c->tg_red, 8));
+    if (cm->kind == COMM_THREADS) {               // handshake: send counts vs listed ghosts
+      ThreadGroup* g = cm->tg;
+      {
+        std::lock_guard<std::mutex> lk(g->mu);
+        for (int q = 0; q < g->R; ++q) g->sbytes[cm->rank][q] = 0;
+        for (auto& P : c->peers) g->sbytes[cm->rank][P.rank] = (size_t)P.n_send;
+      }
+      tg_barrier(g);
+      std::string bad;
+      for (auto& P : c->peers)
+        if (g->sbytes[P.rank][cm->rank] != (size_t)P.n_recv) bad = "peer count mismatch";
+      tg_barrier(g);
+      if (!bad.empty()) return dgvv_fail(DGVV_EINVAL, "thread group: a peer sends a different number of cells than the ghosts listed");
+    } else if (!c->peers.empty()) {
       // handshake: every peer's send count must equal the ghosts listed here
       int* d_cnt = nullptr;
       TRY(dalloc(c, &d_cnt, 2 * c->peers.size()));
@@ -824,8 +1032,8 @@ static dgvv_status setup_impl(const dgvv_mesh* m, int32_t degree, const dgvv_law
       DGVV_CUDA_TRY(cudaMemcpy(d_cnt, hs.data(), hs.size() * sizeof(int), cudaMemcpyHostToDevice));
       NCCL_TRY(g_nccl.groupStart());
       for (size_t i = 0; i < c->peers.size(); ++i) {
-        NCCL_TRY(g_nccl.send(d_cnt + i, 1, ncclInt32, c->peers[i].rank, (ncclComm_t)c->comm, s));
-        NCCL_TRY(g_nccl.recv(d_cnt + c->peers.size() + i, 1, ncclInt32, c->peers[i].rank, (ncclComm_t)c->comm, s));
+        NCCL_TRY(g_nccl.send(d_cnt + i, 1, ncclInt32, c->peers[i].rank, cm->nccl, s));
+        NCCL_TRY(g_nccl.recv(d_cnt + c->peers.size() + i, 1, ncclInt32, c->peers[i].rank, cm->nccl, s));
       }
       NCCL_TRY(g_nccl.groupEnd());
       std::vector<int> got(c->peers.size());
@@ -839,13 +1047,8 @@ static dgvv_status setup_impl(const dgvv_mesh* m, int32_t degree, const dgvv_law
   // global DoF count
   c->n_global = c->n_owned;   // multi-rank: caller sums (dgvv_sizes reports local/global via comm)
   if (c->comm) {
-    long long* d_ng = nullptr;
-    TRY(dalloc(c, &d_ng, 1));
     long long v = c->n_owned;
-    DGVV_CUDA_TRY(cudaMemcpy(d_ng, &v, sizeof(v), cudaMemcpyHostToDevice));
-    NCCL_TRY(g_nccl.allReduce(d_ng, d_ng, 1, ncclInt64, ncclSum, (ncclComm_t)c->comm, s));
-    DGVV_CUDA_TRY(cudaMemcpyAsync(&v, d_ng, sizeof(v), cudaMemcpyDeviceToHost, s));
-    DGVV_CUDA_TRY(cudaStreamSynchronize(s));
+    TRY(comm_host_sum(c, &v, s));
     c->n_global = v;
   }
   DGVV_CUDA_TRY(cudaStreamSynchronize(s));
@@ -1245,7 +1448,6 @@ static dgvv_status d2f_alloc(dgvv_ctx* c, float** dst, const double* src, long n
 }
 
 static dgvv_status ensure_fp32(dgvv_ctx* c, int op, cudaStream_t s) {
-  if (!c->peers.empty()) return dgvv_fail(DGVV_EUNSUPPORTED, "FP32 multigrid: single-GPU contexts only (this build)");
   const int oi = op == DGVV_OP_VISCOUS ? 0 : 1;
   const int nc = op == DGVV_OP_VISCOUS ? 3 : 1;
   if (c->LF.size() != c->L.size()) c->LF.resize(c->L.size());
@@ -1269,6 +1471,7 @@ static dgvv_status ensure_fp32(dgvv_ctx* c, int op, cudaStream_t s) {
       TRY(d2f_alloc(c, &F.dinv[oi], L.dinv[oi], (long)nc * c->n_owned * n3, s));
       F.epoch[oi] = c->coef_epoch;
     }
+    if (c->n_ghost && !F.ghost[oi]) TRY(dalloc(c, &F.ghost[oi], (size_t)nc * c->n_ghost * n3));
     auto& S = F.scratch[oi];
     if (S.empty()) {
       const size_t N = (size_t)nc * c->n_owned * n3;
@@ -1307,16 +1510,41 @@ static ApplyArgsT<float> base_args_f(dgvv_ctx* c, int l, int op) {
   a.Hcell = F.Hc;
   a.pen = c->ip * (double)(c->L[l].k + 1) * (double)(c->L[l].k + 1);
   a.mass = c->mass[oi];
+  a.ghost = F.ghost[oi];
   a.mode = MODE_APPLY;
   return a;
 }
 
+// FP32 levels across ranks: the ghost cells travel in single precision (half the bytes), packed by
+// the float gather kernel and moved by the same collective as the FP64 exchange; interior cells
+// run while they move
 static dgvv_status run_apply_f(dgvv_ctx* c, int op, int l, const ApplyArgsT<float>& a, cudaStream_t s) {
   const int nc = op == DGVV_OP_VISCOUS ? 3 : 1;
   const int form = op == DGVV_OP_VISCOUS ? c->form : DGVV_FORM_LAPLACE;
-  cudaError_t e = launch_apply_f(nc, c->L[l].n, form, c->geo, a, s);
-  if (e != cudaSuccess) return dgvv_fail(DGVV_ECUDA, "FP32 apply kernel: %s", cudaGetErrorString(e));
-  return DGVV_OK;
+  auto launch = [&](const ApplyArgsT<float>& x) -> dgvv_status {
+    cudaError_t e = launch_apply_f(nc, c->L[l].n, form, c->geo, x, s);
+    if (e != cudaSuccess) return dgvv_fail(DGVV_ECUDA, "FP32 apply kernel: %s", cudaGetErrorString(e));
+    return DGVV_OK;
+  };
+  if (!c->comm || c->peers.empty()) return launch(a);
+  const int n = c->L[l].n;
+  const int len = nc * n * n * n;
+  float* sb = reinterpret_cast<float*>(c->d_sendbuf);
+  size_t off = 0;
+  for (auto& P : c->peers) {
+    DGVV_CUDA_TRY(launch_gather_cells_f(a.src, P.d_send, P.n_send, len, sb + off, s));
+    off += (size_t)P.n_send * len;
+  }
+  TRY(comm_sendrecv(c, sb, const_cast<float*>(a.ghost), len, sizeof(float), s));
+  ApplyArgsT<float> ai = a;
+  ai.cell_list = c->d_interior;
+  ai.n_proc = c->n_interior;
+  TRY(launch(ai));
+  DGVV_CUDA_TRY(cudaStreamWaitEvent(s, c->ev_comm, 0));
+  ApplyArgsT<float> ab = a;
+  ab.cell_list = c->d_boundary;
+  ab.n_proc = c->n_boundary;
+  return launch(ab);
 }
 
 static dgvv_status cheb_impl_f(dgvv_ctx* c, int op, int l, float* x, const float* b, int degree, double lo,

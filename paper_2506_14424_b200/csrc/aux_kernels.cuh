@@ -386,7 +386,8 @@ __global__ void scale_by_inv_kernel(const double* w, const double* s2, double* q
 }
 
 // gather cells (ghost exchange pack): out[k] = src[list[k]] (blocks of len doubles)
-__global__ void gather_cells_kernel(const double* src, const int* list, int ncells, int len, double* out) {
+template <typename R>
+__global__ void gather_cells_kernel(const R* src, const int* list, int ncells, int len, R* out) {
   const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (long)ncells * len) return;
   const int k = i / len, r = i % len;

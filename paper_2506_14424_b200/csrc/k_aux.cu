@@ -169,6 +169,23 @@ cudaError_t launch_range(const double* v, long n, double* bmin, double* bmax, in
 }
 
 // ---------------------------------------------------------------- vectors
+// thread-group allreduce: out[i] = sum over ranks (in rank order) of ranks[r][i] — every rank sums
+// the same operands in the same order, so every rank holds the same bits
+struct RankPtrs { const double* p[64]; };
+__global__ void sum_ranks_kernel(RankPtrs P, int R, int count, double* out) {
+  const int i = threadIdx.x;
+  if (i >= count) return;
+  double s = 0.0;
+  for (int r = 0; r < R; ++r) s += P.p[r][i];
+  out[i] = s;
+}
+cudaError_t launch_sum_ranks(const double* const* ranks, int R, int count, double* out, cudaStream_t s) {
+  RankPtrs P;
+  for (int r = 0; r < R && r < 64; ++r) P.p[r] = ranks[r];
+  sum_ranks_kernel<<<1, 32, 0, s>>>(P, R, count, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_dot(const double* a, const double* b, long n, double* part, int nblocks, double* out,
                        cudaStream_t s) {
   dot_partial_kernel<<<nblocks, 256, 0, s>>>(a, b, n, part);
@@ -225,8 +242,14 @@ cudaError_t launch_scale_by_inv(const double* w, const double* s2, double* q, lo
 }
 cudaError_t launch_gather_cells(const double* src, const int* list, int ncells, int len, double* out,
                                 cudaStream_t s) {
-  if (ncells <= 0) return cudaSuccess;
-  gather_cells_kernel<<<nblk((long)ncells * len), 256, 0, s>>>(src, list, ncells, len, out);
+  if ((long)ncells * len <= 0) return cudaSuccess;
+  gather_cells_kernel<double><<<nblk((long)ncells * len), 256, 0, s>>>(src, list, ncells, len, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_gather_cells_f(const float* src, const int* list, int ncells, int len, float* out,
+                                  cudaStream_t s) {
+  if ((long)ncells * len <= 0) return cudaSuccess;
+  gather_cells_kernel<float><<<nblk((long)ncells * len), 256, 0, s>>>(src, list, ncells, len, out);
   return cudaGetLastError();
 }
 

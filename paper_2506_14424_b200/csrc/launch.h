@@ -82,6 +82,7 @@ cudaError_t launch_range(const double* v, long n, double* bmin, double* bmax, in
                          cudaStream_t s);
 
 // vector kernels
+cudaError_t launch_sum_ranks(const double* const* ranks, int R, int count, double* out, cudaStream_t s);
 cudaError_t launch_dot(const double* a, const double* b, long n, double* part, int nblocks, double* out,
                        cudaStream_t s);
 cudaError_t launch_cheb_first(const double* b, const double* dinv, double c_r, double* d, double* x, long n,
@@ -98,6 +99,8 @@ cudaError_t launch_lanczos_update(double* w, const double* q, const double* qpre
                                   const double* beta_prev, long n, cudaStream_t s);
 cudaError_t launch_axpy_dev(const double* coef, double sgn, const double* x, double* y, long n, cudaStream_t s);
 cudaError_t launch_scale_by_inv(const double* w, const double* s2, double* q, long n, cudaStream_t s);
+cudaError_t launch_gather_cells_f(const float* src, const int* list, int ncells, int len, float* out,
+                                  cudaStream_t s);
 cudaError_t launch_gather_cells(const double* src, const int* list, int ncells, int len, double* out,
                                 cudaStream_t s);
 

@@ -401,3 +401,24 @@ def nccl_comm_init(uid: bytes, nranks: int, rank: int):
     comm = C.c_void_p()
     A.check(A.lib().dgvv_nccl_comm_init(uid, nranks, rank, C.byref(comm)))
     return comm
+
+
+class ThreadGroup:
+    """In-process communicator group of R ranks (dgvv_thread_group_create): rank r's communicator
+    (comm(r)) is passed to Context(nccl_comm=...) like an NCCL one; each rank is driven by its own
+    host thread on its own CUDA stream (see include/dgvv.h)."""
+
+    def __init__(self, nranks: int):
+        g = C.c_void_p()
+        A.check(A.lib().dgvv_thread_group_create(int(nranks), C.byref(g)))
+        self.h, self.nranks = g, int(nranks)
+
+    def comm(self, rank: int):
+        cm = C.c_void_p()
+        A.check(A.lib().dgvv_thread_group_comm(self.h, int(rank), C.byref(cm)))
+        return cm
+
+    def close(self):
+        if self.h:
+            A.lib().dgvv_thread_group_destroy(self.h)
+            self.h = None

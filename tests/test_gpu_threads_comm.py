@@ -1,0 +1,192 @@
+"""The multi-rank library path executed end to end on ONE GPU: R ranks, each a host
+thread with its own context and CUDA stream, joined by the library's in-process communicator
+(dgvv_thread_group_*).  Unlike the external-exchange tests this runs the library's own collective
+path — setup handshake, grouped ghost exchange on the comm stream overlapped with the interior
+cells, allreduced dots, and therefore the multi-rank Lanczos, Chebyshev, V-cycle and CG.
+Results: applies bitwise equal to one context (each cell's sum is partition-independent) and
+within 1e-12 of the CPU oracle; solvers match the one-context run (dots are summed rank-wise, so
+only to rounding)."""
+import threading
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from inputs import bfs, cube, uniform                                      # noqa: E402
+from inputs.vectors import c3_linearization                               # noqa: E402
+from oracle import dg, laws                                               # noqa: E402
+from paper_2506_14424_b200 import _abi as A                               # noqa: E402
+from paper_2506_14424_b200.partition import slab_partition                # noqa: E402
+
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def run_ranks(m, R, k, body, **kw):
+    """body(rank, ctx, part) in R threads (each on its own stream); returns the per-rank results."""
+    from paper_2506_14424_b200.dgvv import Context, ThreadGroup
+    g = ThreadGroup(R)
+    parts = [slab_partition(m, R, r) for r in range(R)]
+    out, err = [None] * R, [None] * R
+
+    def worker(r):
+        try:
+            torch.cuda.set_device(0)
+            with torch.cuda.stream(torch.cuda.Stream()):
+                p = parts[r]
+                ctx = Context(p, k, n_owned=p.n_owned, n_ghost=p.n_ghost, ghost_global_id=p.ghost_global_id,
+                              ghost_owner=p.ghost_owner, first_global_cell=p.first, nccl_comm=g.comm(r), **kw)
+                out[r] = body(r, ctx, p)
+                torch.cuda.current_stream().synchronize()
+                ctx.close()
+        except BaseException as e:          # noqa: BLE001 - re-raised in the main thread
+            err[r] = e
+
+    ts = [threading.Thread(target=worker, args=(r,)) for r in range(R)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=600)
+    g.close()
+    for e in err:
+        if e is not None:
+            raise e
+    return parts, out
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+@pytest.mark.parametrize("name,mk,k,R", [("cube4 k4 R2", lambda: cube(4), 4, 2), ("cube5 k3 R3", lambda: cube(5), 3, 3),
+                                         ("bfs small k3 R3", lambda: bfs(nx_in=4, ny_in=2, nx_out=8, nz=3), 3, 3)])
+def test_thread_group_viscous_and_poisson_apply(name, mk, k, R):
+    from paper_2506_14424_b200.dgvv import Context
+    m = mk()
+    per = 3 * (k + 1) ** 3
+    u = uniform(0, m.n_cells * per)
+    ref_ctx = Context(m, k, visc_law=laws.C2_LAW, poisson_law=laws.C4_LAW)
+    ref = torch.empty(len(u), dtype=torch.float64, device="cuda")
+    ref_ctx.apply_viscous(torch.from_numpy(u).cuda(), ref)
+    ps = uniform(1, m.n_cells * (k + 1) ** 3)
+    refp = torch.empty(len(ps), dtype=torch.float64, device="cuda")
+    ref_ctx.apply_poisson(torch.from_numpy(ps).cuda(), refp)
+
+    def body(r, ctx, p):
+        x = torch.from_numpy(u[p.first * per:(p.first + p.n_owned) * per].copy()).cuda()
+        y = torch.empty_like(x)
+        for _ in range(3):                     # repeated exchanges reuse the buffers
+            ctx.apply_viscous(x, y)
+        n1 = (k + 1) ** 3
+        xp = torch.from_numpy(ps[p.first * n1:(p.first + p.n_owned) * n1].copy()).cuda()
+        yp = torch.empty_like(xp)
+        ctx.apply_poisson(xp, yp)
+        d = ctx.dot(x, x, 3)                   # allreduced
+        return y.cpu(), yp.cpu(), d
+
+    parts, out = run_ranks(m, R, k, body, visc_law=laws.C2_LAW, poisson_law=laws.C4_LAW)
+    y = torch.cat([o[0] for o in out])
+    assert torch.equal(y, ref.cpu())
+    assert torch.equal(torch.cat([o[1] for o in out]), refp.cpu())
+    assert all(abs(o[2] - float(u @ u)) <= 1e-13 * float(u @ u) for o in out)
+    assert len({o[2] for o in out}) == 1      # every rank holds the same allreduced bits
+    d = dg.Disc(m, k)
+    assert rel(y.numpy(), dg.viscous_apply(d, u, dg.AnalyticNu(d, laws.C2_LAW))) < TOL
+
+
+def test_thread_group_carreau_newton():
+    """Carreau update (ghost u_lin exchange, coarse-level nu), Picard and Newton applies on 2 ranks."""
+    from paper_2506_14424_b200.dgvv import Context
+    m = cube(4)
+    k, R = 4, 2
+    per = 3 * 125
+    ul = c3_linearization(m, k)
+    w = uniform(0, m.n_cells * per)
+    rc = Context(m, k, visc_law=laws.C3_CARREAU, degrees=[4, 2])
+    rc.update_viscosity(torch.from_numpy(ul).cuda())
+    refp, refn = torch.empty(len(w), dtype=torch.float64, device="cuda"), torch.empty(len(w), dtype=torch.float64, device="cuda")
+    rc.apply_viscous(torch.from_numpy(w).cuda(), refp)
+    rc.apply_linearized_viscous(torch.from_numpy(w).cuda(), refn)
+
+    def body(r, ctx, p):
+        sl = slice(p.first * per, (p.first + p.n_owned) * per)
+        ctx.update_viscosity(torch.from_numpy(ul[sl].copy()).cuda())
+        x = torch.from_numpy(w[sl].copy()).cuda()
+        y1, y2 = torch.empty_like(x), torch.empty_like(x)
+        ctx.apply_viscous(x, y1)
+        ctx.apply_linearized_viscous(x, y2)
+        return y1.cpu(), y2.cpu()
+
+    _, out = run_ranks(m, R, k, body, visc_law=laws.C3_CARREAU, degrees=[4, 2])
+    assert torch.equal(torch.cat([o[0] for o in out]), refp.cpu())
+    assert torch.equal(torch.cat([o[1] for o in out]), refn.cpu())
+    d = dg.Disc(m, k)
+    assert rel(torch.cat([o[1] for o in out]).numpy(), dg.newton_apply(d, ul, w, laws.C3_CARREAU)) < TOL
+
+
+@pytest.mark.parametrize("op,precond", [(0, "vcycle"), (1, "vcycle"), (0, "jacobi"), (2, "vcycle"),
+                                        (0, "vcycle_fp32"), (1, "vcycle_fp32")])
+def test_thread_group_pcg_matches_one_context(op, precond):
+    """Multi-rank Lanczos, V-cycle and PCG on 3 ranks vs one context: lambda_max to rounding (the
+    Lanczos dots are allreduced rank-wise); with the same bounds one V-cycle (FP64 or FP32 levels, no
+    dot inside) is bitwise the one-context V-cycle; PCG to rtol 1e-9 then differs only through the
+    rounding of its dots: iteration counts within one, solutions within 1e-6."""
+    from paper_2506_14424_b200.dgvv import Context
+    m = cube(6)
+    R = 3
+    degs = [3, 2, 1]
+    kw = dict(visc_law=laws.C2_LAW, poisson_law=laws.C4_LAW, degrees=degs)
+    nc = 1 if op == 1 else 3
+    per = nc * 64
+    rng = np.random.default_rng(3)
+    td, tc = rng.uniform(1e-3, 1e-2, m.n_cells), rng.uniform(1e-3, 1e-2, m.n_cells)   # Fehn2018b-sized (DESIGN P1)
+    b = uniform(0, m.n_cells * per)
+    one = Context(m, 3, **kw)
+    if op == 0:
+        one.set_mass(0, 10.0)
+    if op == 2:
+        one.set_penalty_parameters(td, tc)
+    v0s = [uniform(2, m.n_cells * nc * (kk + 1) ** 3) for kk in degs]
+    lams = [1.2 * one.estimate_lambda_max(op, torch.from_numpy(v0s[l]).cuda(), level=l, steps=15)
+            for l in range(len(degs))]
+    bd = torch.from_numpy(b).cuda()
+    v1 = torch.zeros(len(b), dtype=torch.float64, device="cuda")
+    if precond != "jacobi":
+        (one.vcycle_fp32 if precond == "vcycle_fp32" else one.vcycle)(op, bd, v1, lams)
+    x1 = torch.zeros(len(b), dtype=torch.float64, device="cuda")
+    it1, rr1 = one.cg_solve(op, bd, x1, rtol=1e-9, maxit=2000, precond=precond, lam_hi_per_level=lams)
+
+    def body(r, ctx, p):
+        if op == 0:
+            ctx.set_mass(0, 10.0)
+        if op == 2:
+            rows = np.concatenate([np.arange(p.first, p.first + p.n_owned), np.asarray(p.ghost_global_id, dtype=np.int64)])
+            ctx.set_penalty_parameters(td[rows], tc[rows])
+        lam = []
+        for l, kk in enumerate(degs):
+            q = nc * (kk + 1) ** 3
+            lam.append(1.2 * ctx.estimate_lambda_max(op, torch.from_numpy(v0s[l][p.first * q:(p.first + p.n_owned) * q].copy()).cuda(),
+                                                     level=l, steps=15))
+        bb = torch.from_numpy(b[p.first * per:(p.first + p.n_owned) * per].copy()).cuda()
+        v = torch.zeros(p.n_owned * per, dtype=torch.float64, device="cuda")
+        if precond != "jacobi":
+            (ctx.vcycle_fp32 if precond == "vcycle_fp32" else ctx.vcycle)(op, bb, v, lams)
+        x = torch.zeros(p.n_owned * per, dtype=torch.float64, device="cuda")
+        it, rr = ctx.cg_solve(op, bb, x, rtol=1e-9, maxit=2000, precond=precond, lam_hi_per_level=lams)
+        return x.cpu(), it, rr, lam, v.cpu()
+
+    _, out = run_ranks(m, R, 3, body, **kw)
+    for o in out:
+        assert np.allclose(o[3], lams, rtol=1e-10, atol=0), (o[3], lams)
+        assert abs(o[1] - it1) <= 1, (o[1], it1)
+    assert torch.equal(torch.cat([o[4] for o in out]), v1.cpu())
+    x = torch.cat([o[0] for o in out]).numpy()
+    assert rel(x, x1.cpu().numpy()) < 1e-6
+    assert rr1 <= 1e-9 and max(o[2] for o in out) <= 1e-9
