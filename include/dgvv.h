@@ -278,8 +278,11 @@ dgvv_status dgvv_vcycle(dgvv_ctx* ctx, int32_t op, const double* b, double* x,
  * lambda_hi_per_level lists every level of that chain in order.  `coarse` is borrowed: keep it
  * alive while `fine` is used; its coefficients/mass are its own (set them consistently).
  * The FP32 V-cycle (dgvv_vcycle_fp32, DGVV_PRECOND_VCYCLE_FP32) follows the chain as well, with
- * the direct coarse solve in FP64 arithmetic.  Single-GPU contexts only
- * (DGVV_EUNSUPPORTED with ghosts). */
+ * the direct coarse solve in FP64 arithmetic.  Across ranks: both contexts
+ * carry the communicator and the partitions are nested (every owned fine cell's parent is an owned
+ * coarse cell: parent[] holds local coarse ids < coarse n_cells), so the h-transfers stay
+ * rank-local and every coarse level exchanges its own ghosts (DGVV_EUNSUPPORTED if only one of the
+ * two has a communicator).  The direct coarse solver and the c-level are single-rank only. */
 dgvv_status dgvv_set_coarse_context(dgvv_ctx* fine, dgvv_ctx* coarse, const int32_t* parent,
                                     const int8_t* octant);
 /* fine = P coarse + beta fine (fine's coarsest level <- coarse's level 0), op selects 3 or 1

@@ -2479,8 +2479,11 @@ dgvv_status dgvv_set_coarse_context(dgvv_ctx* c, dgvv_ctx* cc, const int32_t* pa
   if (c == cc) return dgvv_fail(DGVV_EINVAL, "a context cannot be its own coarse level");
   for (dgvv_ctx* q = cc; q; q = q->coarse)
     if (q == c) return dgvv_fail(DGVV_EINVAL, "coarse-context chain would form a cycle");
-  if (c->n_ghost || cc->n_ghost || c->comm || cc->comm)
-    return dgvv_fail(DGVV_EUNSUPPORTED, "h-levels: single-GPU contexts only in this build");
+  // across ranks: both contexts on the communicator, partitions nested (every owned fine cell's
+  // parent is an owned coarse cell, checked below), so the h-transfers stay rank-local and the
+  // coarse levels exchange their own ghosts
+  if ((c->comm == nullptr) != (cc->comm == nullptr) || (c->n_ghost && !c->comm) || (cc->n_ghost && !cc->comm))
+    return dgvv_fail(DGVV_EUNSUPPORTED, "h-levels across ranks need a communicator on both contexts");
   if (cc->L[0].k != c->L.back().k)
     return dgvv_fail(DGVV_EINVAL, "coarse context degree %d != coarsest level degree %d", cc->L[0].k, c->L.back().k);
   const int nf = c->n_owned, ncs = cc->n_owned;

@@ -162,8 +162,11 @@ sipg_apply2_kernel(const ApplyArgsT<R> A) {
   // (p = a + n b) a quad shares its row (x-direction loads: 1 wavefront) but reads 4 different
   // columns (y-direction loads: 2).  For n = 4 the quad covers a 2 x 2 block of (a, b) instead:
   // 2 distinct rows and 2 distinct columns per quad, one wavefront per 64-bit load either way.
-  const int a = (n == 4 && DGVV_QUAD_SWIZZLE) ? ((pr & 1) | ((pr >> 1) & 2)) : pr % n;
-  const int b = (n == 4 && DGVV_QUAD_SWIZZLE) ? (((pr >> 1) & 1) | ((pr >> 2) & 2)) : pr / n;
+  // n = 6 likewise: quad q = pr / 4 (9 per team; a team of 36 starts on a quad boundary) covers the
+  // 2 x 2 block (2 (q % 3), 2 (q / 3)).  n = 5 teams (25 lanes) straddle quads: natural order.
+  constexpr bool SWZ = DGVV_QUAD_SWIZZLE && (n == 4 || n == 6);
+  const int a = !SWZ ? pr % n : (n == 4 ? ((pr & 1) | ((pr >> 1) & 2)) : 2 * ((pr >> 2) % 3) + (pr & 1));
+  const int b = !SWZ ? pr / n : (n == 4 ? (((pr >> 1) & 1) | ((pr >> 2) & 2)) : 2 * ((pr >> 2) / 3) + ((pr >> 1) & 1));
   const int p = a + n * b;                          // the column's point index in the cell block
   const int slot_raw = blockIdx.x * CPB + lc;
   const bool active = slot_raw < A.n_proc;

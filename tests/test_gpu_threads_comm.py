@@ -190,3 +190,92 @@ def test_thread_group_pcg_matches_one_context(op, precond):
     x = torch.cat([o[0] for o in out]).numpy()
     assert rel(x, x1.cpu().numpy()) < 1e-6
     assert rr1 <= 1e-9 and max(o[2] for o in out) <= 1e-9
+
+
+def test_thread_group_cph_vcycle_h_levels():
+    """h-levels across ranks (nested z-slabs): the cph V-cycle 8^3 k=2 -> k=1 -> 4^3 k=1 -> 2^3 k=1
+    (coarsest: Chebyshev) on 2 ranks is bitwise the one-context V-cycle; PCG with it matches."""
+    from inputs import cube_parent_map
+    from paper_2506_14424_b200.dgvv import Context, ThreadGroup
+    R = 2
+    law = laws.C2_LAW
+    meshes = [cube(8), cube(4), cube(2)]
+    degs0 = [2, 1]
+    b = uniform(0, meshes[0].n_cells * 3 * 27)
+
+    def chain(ctxs, parts):
+        for lvl in range(len(ctxs) - 1):
+            par, octa = cube_parent_map(meshes[lvl].n_cells and round(meshes[lvl].n_cells ** (1 / 3)))
+            pf, pc = parts[lvl], parts[lvl + 1]
+            sl = slice(pf.first, pf.first + pf.n_owned)
+            ctxs[lvl].set_coarse_context(ctxs[lvl + 1], par[sl] - pc.first, octa[sl])
+
+    # one context
+    one = [Context(meshes[0], 2, visc_law=law, degrees=degs0), Context(meshes[1], 1, visc_law=law),
+           Context(meshes[2], 1, visc_law=law)]
+    for c in one:
+        c.set_mass(0, 10.0)
+
+    class _P:
+        first, n_owned = 0, None
+    full = []
+    for m in meshes:
+        p = _P()
+        p.n_owned = m.n_cells
+        full.append(p)
+    chain(one, full)
+    nlev = 4
+    v0 = [uniform(2, 3 * meshes[0].n_cells * 27), uniform(2, 3 * meshes[0].n_cells * 8),
+          uniform(3, 3 * meshes[1].n_cells * 8), uniform(4, 3 * meshes[2].n_cells * 8)]
+    lams = [1.2 * one[0].estimate_lambda_max(0, torch.from_numpy(v0[0]).cuda(), level=0, steps=15),
+            1.2 * one[0].estimate_lambda_max(0, torch.from_numpy(v0[1]).cuda(), level=1, steps=15),
+            1.2 * one[1].estimate_lambda_max(0, torch.from_numpy(v0[2]).cuda(), level=0, steps=15),
+            1.2 * one[2].estimate_lambda_max(0, torch.from_numpy(v0[3]).cuda(), level=0, steps=15)]
+    assert one[0].chain_levels() == nlev
+    v1 = torch.zeros(len(b), dtype=torch.float64, device="cuda")
+    one[0].vcycle(0, torch.from_numpy(b).cuda(), v1, lams)
+    x1 = torch.zeros(len(b), dtype=torch.float64, device="cuda")
+    it1, _ = one[0].cg_solve(0, torch.from_numpy(b).cuda(), x1, rtol=1e-9, maxit=200, precond="vcycle", lam_hi_per_level=lams)
+
+    g = ThreadGroup(R)
+    parts = [[slab_partition(m, R, r) for m in meshes] for r in range(R)]
+    out, err = [None] * R, [None] * R
+
+    def worker(r):
+        try:
+            torch.cuda.set_device(0)
+            with torch.cuda.stream(torch.cuda.Stream()):
+                ps = parts[r]
+                kws = [dict(degrees=degs0), {}, {}]
+                ks = [2, 1, 1]
+                ctxs = [Context(p, k, visc_law=law, n_owned=p.n_owned, n_ghost=p.n_ghost, ghost_global_id=p.ghost_global_id,
+                                ghost_owner=p.ghost_owner, first_global_cell=p.first, nccl_comm=g.comm(r), **kw)
+                        for p, k, kw in zip(ps, ks, kws)]
+                for c in ctxs:
+                    c.set_mass(0, 10.0)
+                chain(ctxs, ps)
+                per = 3 * 27
+                bb = torch.from_numpy(b[ps[0].first * per:(ps[0].first + ps[0].n_owned) * per].copy()).cuda()
+                v = torch.zeros_like(bb)
+                ctxs[0].vcycle(0, bb, v, lams)
+                x = torch.zeros_like(bb)
+                it, rr = ctxs[0].cg_solve(0, bb, x, rtol=1e-9, maxit=200, precond="vcycle", lam_hi_per_level=lams)
+                torch.cuda.current_stream().synchronize()
+                out[r] = (v.cpu(), x.cpu(), it, rr)
+                for c in ctxs:
+                    c.close()
+        except BaseException as e:          # noqa: BLE001
+            err[r] = e
+
+    ts = [threading.Thread(target=worker, args=(r,)) for r in range(R)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=600)
+    g.close()
+    for e in err:
+        if e is not None:
+            raise e
+    assert torch.equal(torch.cat([o[0] for o in out]), v1.cpu())
+    assert all(abs(o[2] - it1) <= 1 for o in out)
+    assert rel(torch.cat([o[1] for o in out]).numpy(), x1.cpu().numpy()) < 1e-6
