@@ -211,6 +211,15 @@ def run_reference(args, rank, world):
 
 
 # ---------------------------------------------------------------------- GPU arm
+def _nccl_version():
+    try:
+        import torch
+        v = torch.cuda.nccl.version()
+        return ".".join(str(x) for x in v) if isinstance(v, tuple) else str(v)
+    except Exception:
+        return None
+
+
 def _dist_setup(world, rank):
     """torch.distributed (NCCL) for barriers/timing reductions; the library's own NCCL
     communicator for the ghost exchange (unique id broadcast through torch.distributed)."""
@@ -424,6 +433,17 @@ def run_ours(args, rank, world):
              "algorithmic_bytes_per_launch": bytes_alg,
              "counting": f"SURVEY §8(d): src + dst + stored nu = {visc_bytes_per_dof(n):.2f} B/DoF x {N} DoFs"}
     launches = args.steps * (1 if world == 1 else 2 + len(ctx.ghost_layout()))
+    exch = None
+    if world > 1:                              # per-rank face-trace exchange bytes of one apply
+        sent, recv = ctx.exchange_bytes(0)
+        t = torch.tensor([float(sent), float(recv)], dtype=torch.float64, device=dev)
+        allt = [torch.zeros_like(t) for _ in range(world)]
+        torch.distributed.all_gather(allt, t)
+        exch = {"kind": "face traces (value + d/dxi_n per component and face point), NCCL grouped send/recv on a "
+                        "comm stream overlapped with the interior cells",
+                "bytes_sent_per_apply": [int(x[0].item()) for x in allt],
+                "bytes_received_per_apply": [int(x[1].item()) for x in allt],
+                "nccl_version": _nccl_version()}
     line = {"metric": METRIC, "value": value, "unit": "DoFs/s", "n_gpus": world, "steps": args.steps,
             "warmup": W, "ms_per_step": t_ms, "ms_per_step_median": t_med, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -438,6 +458,8 @@ def run_ours(args, rank, world):
                     "d2h_bytes_per_step": N_glob * 8, "ms_per_step": e_ms,
                     "call": "dgvv_apply_viscous_host (pinned host src/dst, copies inside the timed region)"},
             "clocks": clk.result()}
+    if exch is not None:
+        line["exchange"] = exch
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = time_cpu_oracle(cfg, seconds=args.cpu_seconds, mesh=mg, ulin=ulin)
         cb.pop("seconds")

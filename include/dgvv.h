@@ -349,6 +349,15 @@ dgvv_status dgvv_coefficient_range(dgvv_ctx* ctx, int32_t op, int32_t level, dou
  * run after the exchange.  Without a communicator (external-exchange mode) the caller fills
  * the ghost buffers itself, using dgvv_pack_ghosts on the peer's context. */
 enum { DGVV_GHOST_VISCOUS = 0, DGVV_GHOST_POISSON = 1, DGVV_GHOST_ULIN = 2, DGVV_GHOST_TRANSPORT = 3 };
+/* Bytes one apply of `op` on `level` sends / receives in communicator mode (a5): the face traces
+ * (value and reference normal derivative of every component at the n^2 points of every cut face,
+ * FP64) of the owned cells next to each peer — 2 NC n^2 doubles per cut face instead of the
+ * NC n^3 of a whole ghost cell.  The Newton apply (K2), the penalty and the standalone convective
+ * operator still exchange whole ghost cells; the external-exchange mode (no communicator; tests)
+ * fills whole ghost cells for every operator. */
+dgvv_status dgvv_exchange_bytes(const dgvv_ctx* ctx, int32_t level, int32_t op, int64_t* sent,
+                                int64_t* received);
+
 /* Peers in ascending rank; arrays (may be NULL) sized by a first call that only reads n_peers. */
 dgvv_status dgvv_ghost_layout(const dgvv_ctx* ctx, int32_t* n_peers, int32_t* peer_ranks,
                               int32_t* send_counts, int32_t* recv_counts);

@@ -92,6 +92,7 @@ _SIGS = {
     "dgvv_thread_group_create": [I32, C.POINTER(VP)],
     "dgvv_thread_group_comm": [VP, I32, C.POINTER(VP)],
     "dgvv_thread_group_destroy": [VP],
+    "dgvv_exchange_bytes": [VP, I32, I32, C.POINTER(I64), C.POINTER(I64)],
 }
 
 

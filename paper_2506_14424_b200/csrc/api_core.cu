@@ -287,7 +287,7 @@ DGVV_INTERNAL dgvv_status setup_impl(const dgvv_mesh* m, int32_t degree, const d
     std::vector<int> uniq = owners;
     std::sort(uniq.begin(), uniq.end());
     uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
-    size_t total_send = 0;
+    size_t total_send = 0, total_send_f = 0;
     for (int r : uniq) {
       Peer P;
       P.rank = r;
@@ -303,11 +303,39 @@ DGVV_INTERNAL dgvv_status setup_impl(const dgvv_mesh* m, int32_t degree, const d
       TRY(dalloc(c, &P.d_send, send.size()));
       DGVV_CUDA_TRY(cudaMemcpy(P.d_send, send.data(), send.size() * sizeof(int), cudaMemcpyHostToDevice));
       total_send += send.size();
+      // face-trace items: (owned cell, face) with the neighbour owned by r, ascending
+      std::vector<int> fc, ff;
+      for (int lc = 0; lc < c->n_owned; ++lc)
+        for (int f = 0; f < 6; ++f) {
+          const int v = nbr[(size_t)lc * 6 + f];
+          if (v >= c->n_owned && owners[v - c->n_owned] == r) { fc.push_back(lc); ff.push_back(f); }
+        }
+      P.n_send_f = (int)fc.size();
+      TRY(dalloc(c, &P.d_fcell, fc.size()));
+      TRY(dalloc(c, &P.d_fface, ff.size()));
+      DGVV_CUDA_TRY(cudaMemcpy(P.d_fcell, fc.data(), fc.size() * sizeof(int), cudaMemcpyHostToDevice));
+      DGVV_CUDA_TRY(cudaMemcpy(P.d_fface, ff.data(), ff.size() * sizeof(int), cudaMemcpyHostToDevice));
+      total_send_f += fc.size();
       c->peers.push_back(P);
     }
+    // received items: the faces of each peer's ghosts that touch an owned cell, in ghost order
+    std::vector<int> gslot((size_t)c->n_ghost * 6, -1);
+    int item = 0;
+    for (auto& P : c->peers) {
+      P.recv_off_f = item;
+      for (int g = P.recv_off; g < P.recv_off + P.n_recv; ++g)
+        for (int f = 0; f < 6; ++f) {
+          const int v = nbr[(size_t)(c->n_owned + g) * 6 + f];
+          if (v >= 0 && v < c->n_owned) gslot[(size_t)g * 6 + f] = item++;
+        }
+      P.n_recv_f = item - P.recv_off_f;
+    }
+    c->n_recv_f = item;
+    TRY(dalloc(c, &c->d_gslot, gslot.size()));
+    DGVV_CUDA_TRY(cudaMemcpy(c->d_gslot, gslot.data(), gslot.size() * sizeof(int), cudaMemcpyHostToDevice));
     int nmax = 0;
     for (auto& L : c->L) nmax = std::max(nmax, L.n);
-    c->sendbuf_len = total_send * 3 * nmax * nmax * nmax;
+    c->sendbuf_len = std::max(total_send * 3 * nmax * nmax * nmax, total_send_f * 2 * 3 * nmax * nmax);
     TRY(dalloc(c, &c->d_sendbuf, c->sendbuf_len));
     std::vector<int> inner, bnd;
     for (int lc = 0; lc < c->n_owned; ++lc) {
@@ -338,33 +366,35 @@ DGVV_INTERNAL dgvv_status setup_impl(const dgvv_mesh* m, int32_t degree, const d
       {
         std::lock_guard<std::mutex> lk(g->mu);
         for (int q = 0; q < g->R; ++q) g->sbytes[cm->rank][q] = 0;
-        for (auto& P : c->peers) g->sbytes[cm->rank][P.rank] = (size_t)P.n_send;
+        for (auto& P : c->peers) g->sbytes[cm->rank][P.rank] = (size_t)P.n_send + ((size_t)P.n_send_f << 32);
       }
       tg_barrier(g);
       std::string bad;
       for (auto& P : c->peers)
-        if (g->sbytes[P.rank][cm->rank] != (size_t)P.n_recv) bad = "peer count mismatch";
+        if (g->sbytes[P.rank][cm->rank] != (size_t)P.n_recv + ((size_t)P.n_recv_f << 32)) bad = "peer count mismatch";
       tg_barrier(g);
       if (!bad.empty()) return dgvv_fail(DGVV_EINVAL, "thread group: a peer sends a different number of cells than the ghosts listed");
     } else if (!c->peers.empty()) {
-      // handshake: every peer's send count must equal the ghosts listed here
+      // handshake: every peer's send counts (cells, trace items) must equal what is listed here
+      const size_t np = c->peers.size();
       int* d_cnt = nullptr;
-      TRY(dalloc(c, &d_cnt, 2 * c->peers.size()));
-      std::vector<int> hs(c->peers.size());
-      for (size_t i = 0; i < c->peers.size(); ++i) hs[i] = c->peers[i].n_send;
+      TRY(dalloc(c, &d_cnt, 4 * np));
+      std::vector<int> hs(2 * np);
+      for (size_t i = 0; i < np; ++i) { hs[2 * i] = c->peers[i].n_send; hs[2 * i + 1] = c->peers[i].n_send_f; }
       DGVV_CUDA_TRY(cudaMemcpy(d_cnt, hs.data(), hs.size() * sizeof(int), cudaMemcpyHostToDevice));
       NCCL_TRY(g_nccl.groupStart());
-      for (size_t i = 0; i < c->peers.size(); ++i) {
-        NCCL_TRY(g_nccl.send(d_cnt + i, 1, ncclInt32, c->peers[i].rank, cm->nccl, s));
-        NCCL_TRY(g_nccl.recv(d_cnt + c->peers.size() + i, 1, ncclInt32, c->peers[i].rank, cm->nccl, s));
+      for (size_t i = 0; i < np; ++i) {
+        NCCL_TRY(g_nccl.send(d_cnt + 2 * i, 2, ncclInt32, c->peers[i].rank, cm->nccl, s));
+        NCCL_TRY(g_nccl.recv(d_cnt + 2 * np + 2 * i, 2, ncclInt32, c->peers[i].rank, cm->nccl, s));
       }
       NCCL_TRY(g_nccl.groupEnd());
-      std::vector<int> got(c->peers.size());
-      DGVV_CUDA_TRY(cudaMemcpyAsync(got.data(), d_cnt + c->peers.size(), got.size() * sizeof(int), cudaMemcpyDeviceToHost, s));
+      std::vector<int> got(2 * np);
+      DGVV_CUDA_TRY(cudaMemcpyAsync(got.data(), d_cnt + 2 * np, got.size() * sizeof(int), cudaMemcpyDeviceToHost, s));
       DGVV_CUDA_TRY(cudaStreamSynchronize(s));
-      for (size_t i = 0; i < c->peers.size(); ++i)
-        if (got[i] != c->peers[i].n_recv)
-          return dgvv_fail(DGVV_EINVAL, "peer %d sends %d cells but %d ghosts are listed", c->peers[i].rank, got[i], c->peers[i].n_recv);
+      for (size_t i = 0; i < np; ++i)
+        if (got[2 * i] != c->peers[i].n_recv || got[2 * i + 1] != c->peers[i].n_recv_f)
+          return dgvv_fail(DGVV_EINVAL, "peer %d sends %d cells / %d faces but %d ghosts / %d faces are listed",
+                           c->peers[i].rank, got[2 * i], got[2 * i + 1], c->peers[i].n_recv, c->peers[i].n_recv_f);
     }
   }
   // global DoF count
@@ -651,6 +681,18 @@ dgvv_status dgvv_coefficient_range(dgvv_ctx* c, int32_t op, int32_t level, doubl
   TRY(array_range(c, vf, (long)c->n_owned * 6 * n * n, s, &a2, &b2, &bad));
   *lo = std::min(a1, a2);
   *hi = std::max(b1, b2);
+  return DGVV_OK;
+}
+
+dgvv_status dgvv_exchange_bytes(const dgvv_ctx* c, int32_t level, int32_t op, int64_t* sent, int64_t* received) {
+  TRY(check_level(c, level));
+  if (!sent || !received) return dgvv_fail(DGVV_EINVAL, "null output");
+  const int nc = op == DGVV_OP_POISSON ? 1 : 3;
+  const long long per = 2LL * nc * c->L[level].n * c->L[level].n * 8;   // value + d/dxi_n, FP64
+  long long snd = 0, rcv = 0;
+  for (auto& P : c->peers) { snd += P.n_send_f * per; rcv += P.n_recv_f * per; }
+  *sent = snd;
+  *received = rcv;
   return DGVV_OK;
 }
 

@@ -180,6 +180,7 @@ struct Level {
   bool dinv_ok[2] = {false, false};          // buffer kept across coefficient changes; recomputed when false
   double* ulin = nullptr;     // u_lin interpolated to this level (levels >= 1), owned
   double* ghost[2] = {nullptr, nullptr};   // ghost src buffers (NC = 3 / 1)
+  double* gtr[2] = {nullptr, nullptr};     // received ghost face traces (communicator mode)
   double* ulin_ghost = nullptr;
   std::vector<double*> scratch[2];         // V-cycle scratch per op
   // f2 penalty-step operator on this level (same per-cell tau on every level): inverse diagonal
@@ -201,6 +202,7 @@ struct LevelF {
   float* Hc = nullptr;
   float* jxw = nullptr;
   float* ghost[2] = {nullptr, nullptr};     // FP32 ghost cells per op (multi-rank)
+  float* gtr[2] = {nullptr, nullptr};       // FP32 ghost face traces per op (communicator mode)
   std::vector<float*> scratch[2];           // [0] r, [1] work (2N), [3] b, [4] x
 };
 
@@ -209,6 +211,12 @@ struct Peer {
   int* d_send = nullptr;      // owned local cells to send (sorted by global id)
   int n_send = 0;
   int recv_off = 0, n_recv = 0;   // ghost index range received from this peer
+  // face-trace exchange (communicator mode): (owned cell, face) items whose neighbour the peer
+  // owns, ascending (cell, face); the peer receives them in the same order for its ghosts
+  int* d_fcell = nullptr;
+  int* d_fface = nullptr;
+  int n_send_f = 0;
+  int recv_off_f = 0, n_recv_f = 0;   // trace item range received from this peer
 };
 
 struct dgvv_ctx {
@@ -288,6 +296,8 @@ struct dgvv_ctx {
   // (without one the caller fills the ghost buffers: external-exchange mode, used by tests)
   void* comm = nullptr;                      // DgvvComm*
   std::vector<Peer> peers;
+  int* d_gslot = nullptr;                    // [n_ghost][6] trace item of ghost g's face f (-1: none)
+  int n_recv_f = 0;                          // trace items received in total
   double* tg_red = nullptr;                  // thread group: allreduce staging (8 doubles)
   cudaEvent_t ev_red = nullptr, ev_red2 = nullptr;
   double* d_sendbuf = nullptr;
@@ -390,7 +400,11 @@ dgvv_status pack(dgvv_ctx* c, int l, int nc, const double* src, double* sendbuf,
 // before reading ghosts).  No-op without ghosts or without a communicator.
 // grouped point-to-point exchange of packed cells (len elements of esz bytes per cell) with every
 // peer, on the comm stream after ev_pack; ev_comm marks completion
-dgvv_status comm_sendrecv(dgvv_ctx* c, const void* sendbuf, void* ghost, int len, size_t esz, cudaStream_t s) {
+dgvv_status comm_sendrecv(dgvv_ctx* c, const void* sendbuf, void* ghost, int len, size_t esz, cudaStream_t s,
+                          bool faces = false) {
+  auto nsend = [&](const Peer& P) { return faces ? P.n_send_f : P.n_send; };
+  auto nrecv = [&](const Peer& P) { return faces ? P.n_recv_f : P.n_recv; };
+  auto roff = [&](const Peer& P) { return faces ? P.recv_off_f : P.recv_off; };
   DgvvComm* cm = (DgvvComm*)c->comm;
   DGVV_CUDA_TRY(cudaEventRecord(c->ev_pack, s));
   if (cm->kind == COMM_NCCL) {
@@ -399,9 +413,9 @@ dgvv_status comm_sendrecv(dgvv_ctx* c, const void* sendbuf, void* ghost, int len
     NCCL_TRY(g_nccl.groupStart());
     size_t off = 0;
     for (auto& P : c->peers) {
-      if (P.n_send) NCCL_TRY(g_nccl.send((const char*)sendbuf + off * esz, (size_t)P.n_send * len, dt, P.rank, cm->nccl, c->comm_stream));
-      if (P.n_recv) NCCL_TRY(g_nccl.recv((char*)ghost + (size_t)P.recv_off * len * esz, (size_t)P.n_recv * len, dt, P.rank, cm->nccl, c->comm_stream));
-      off += (size_t)P.n_send * len;
+      if (nsend(P)) NCCL_TRY(g_nccl.send((const char*)sendbuf + off * esz, (size_t)nsend(P) * len, dt, P.rank, cm->nccl, c->comm_stream));
+      if (nrecv(P)) NCCL_TRY(g_nccl.recv((char*)ghost + (size_t)roff(P) * len * esz, (size_t)nrecv(P) * len, dt, P.rank, cm->nccl, c->comm_stream));
+      off += (size_t)nsend(P) * len;
     }
     NCCL_TRY(g_nccl.groupEnd());
     DGVV_CUDA_TRY(cudaEventRecord(c->ev_comm, c->comm_stream));
@@ -415,8 +429,8 @@ dgvv_status comm_sendrecv(dgvv_ctx* c, const void* sendbuf, void* ghost, int len
     for (int q = 0; q < g->R; ++q) { g->sptr[r][q] = nullptr; g->sbytes[r][q] = 0; }
     for (auto& P : c->peers) {
       g->sptr[r][P.rank] = (const char*)sendbuf + off * esz;
-      g->sbytes[r][P.rank] = (size_t)P.n_send * len * esz;
-      off += (size_t)P.n_send * len;
+      g->sbytes[r][P.rank] = (size_t)nsend(P) * len * esz;
+      off += (size_t)nsend(P) * len;
     }
     g->ev_a[r] = c->ev_pack;
   }
@@ -425,12 +439,12 @@ dgvv_status comm_sendrecv(dgvv_ctx* c, const void* sendbuf, void* ghost, int len
   // ev_pack on s), and after each peer has packed
   DGVV_CUDA_TRY(cudaStreamWaitEvent(c->comm_stream, c->ev_pack, 0));
   for (auto& P : c->peers) {
-    const size_t want = (size_t)P.n_recv * len * esz;
+    const size_t want = (size_t)nrecv(P) * len * esz;
     if (g->sbytes[P.rank][r] != want)
       return dgvv_fail(DGVV_EINVAL, "thread group: rank %d sends %zu bytes, rank %d expects %zu", P.rank, g->sbytes[P.rank][r], r, want);
     if (!want) continue;
     DGVV_CUDA_TRY(cudaStreamWaitEvent(c->comm_stream, g->ev_a[P.rank], 0));
-    DGVV_CUDA_TRY(cudaMemcpyAsync((char*)ghost + (size_t)P.recv_off * len * esz, g->sptr[P.rank][r], want,
+    DGVV_CUDA_TRY(cudaMemcpyAsync((char*)ghost + (size_t)roff(P) * len * esz, g->sptr[P.rank][r], want,
                                   cudaMemcpyDeviceToDevice, c->comm_stream));
   }
   DGVV_CUDA_TRY(cudaEventRecord(c->ev_comm, c->comm_stream));
@@ -511,6 +525,25 @@ dgvv_status exchange(dgvv_ctx* c, int l, int nc, const double* src, double* ghos
   return comm_sendrecv(c, c->d_sendbuf, ghost, len, sizeof(double), s);
 }
 
+// a5 in communicator mode: the face traces (value, d/dxi_n; 2 NC n^2 per cut face) of the owned
+// cells next to each peer instead of whole ghost cells (NC n^3): pack kernel, then the collective
+template <typename R>
+dgvv_status exchange_traces(dgvv_ctx* c, int l, int nc, const R* src, R** gtr, cudaStream_t s) {
+  const int n = c->L[l].n;
+  const int len = 2 * nc * n * n;
+  if (!*gtr) TRY(dalloc(c, gtr, (size_t)std::max(1, c->n_recv_f) * len));
+  R* sb = reinterpret_cast<R*>(c->d_sendbuf);
+  size_t off = 0;
+  for (auto& P : c->peers) {
+    cudaError_t e = sizeof(R) == 8
+        ? launch_pack_traces(nc, n, (const double*)src, P.d_fcell, P.d_fface, P.n_send_f, (double*)(sb + off), s)
+        : launch_pack_traces_f(nc, n, (const float*)src, P.d_fcell, P.d_fface, P.n_send_f, (float*)(sb + off), s);
+    if (e != cudaSuccess) return dgvv_fail(DGVV_ECUDA, "trace pack: %s", cudaGetErrorString(e));
+    off += (size_t)P.n_send_f * len;
+  }
+  return comm_sendrecv(c, sb, *gtr, len, sizeof(R), s, true);
+}
+
 dgvv_status exchange_sync(dgvv_ctx* c, int l, int nc, const double* src, double* ghost, cudaStream_t s) {
   TRY(exchange(c, l, nc, src, ghost, s));
   if (c->comm && !c->peers.empty()) DGVV_CUDA_TRY(cudaStreamWaitEvent(s, c->ev_comm, 0));
@@ -575,7 +608,14 @@ dgvv_status run_apply(dgvv_ctx* c, int op, int l, ApplyArgs a, cudaStream_t s, i
     return DGVV_OK;
   };
   if (!c->comm || c->peers.empty()) return launch(a);
-  TRY(exchange(c, l, nc, a.src, const_cast<double*>(a.ghost), s));
+  if (kind != 1) {                            // SIPG applies: face traces; Newton (K2): ghost cells
+    const int oi = op == DGVV_OP_VISCOUS ? 0 : 1;
+    TRY(exchange_traces(c, l, nc, a.src, &c->L[l].gtr[oi], s));
+    a.gtr = c->L[l].gtr[oi];
+    a.gslot = c->d_gslot;
+  } else {
+    TRY(exchange(c, l, nc, a.src, const_cast<double*>(a.ghost), s));
+  }
   ApplyArgs ai = a;
   ai.cell_list = c->d_interior;
   ai.n_proc = c->n_interior;

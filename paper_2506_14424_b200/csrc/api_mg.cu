@@ -212,9 +212,8 @@ DGVV_INTERNAL ApplyArgsT<float> base_args_f(dgvv_ctx* c, int l, int op) {
   return a;
 }
 
-// FP32 levels across ranks: the ghost cells travel in single precision (half the bytes), packed by
-// the float gather kernel and moved by the same collective as the FP64 exchange; interior cells
-// run while they move
+// FP32 levels across ranks: the ghost face traces travel in single precision, packed by the trace
+// kernel and moved by the same collective as the FP64 exchange; interior cells run while they move
 DGVV_INTERNAL dgvv_status run_apply_f(dgvv_ctx* c, int op, int l, const ApplyArgsT<float>& a, cudaStream_t s) {
   const int nc = op == DGVV_OP_VISCOUS ? 3 : 1;
   const int form = op == DGVV_OP_VISCOUS ? c->form : DGVV_FORM_LAPLACE;
@@ -224,21 +223,17 @@ DGVV_INTERNAL dgvv_status run_apply_f(dgvv_ctx* c, int op, int l, const ApplyArg
     return DGVV_OK;
   };
   if (!c->comm || c->peers.empty()) return launch(a);
-  const int n = c->L[l].n;
-  const int len = nc * n * n * n;
-  float* sb = reinterpret_cast<float*>(c->d_sendbuf);
-  size_t off = 0;
-  for (auto& P : c->peers) {
-    DGVV_CUDA_TRY(launch_gather_cells_f(a.src, P.d_send, P.n_send, len, sb + off, s));
-    off += (size_t)P.n_send * len;
-  }
-  TRY(comm_sendrecv(c, sb, const_cast<float*>(a.ghost), len, sizeof(float), s));
-  ApplyArgsT<float> ai = a;
+  const int oi = op == DGVV_OP_VISCOUS ? 0 : 1;
+  TRY(exchange_traces(c, l, nc, a.src, &c->LF[l].gtr[oi], s));   // FP32 face traces
+  ApplyArgsT<float> a2 = a;
+  a2.gtr = c->LF[l].gtr[oi];
+  a2.gslot = c->d_gslot;
+  ApplyArgsT<float> ai = a2;
   ai.cell_list = c->d_interior;
   ai.n_proc = c->n_interior;
   TRY(launch(ai));
   DGVV_CUDA_TRY(cudaStreamWaitEvent(s, c->ev_comm, 0));
-  ApplyArgsT<float> ab = a;
+  ApplyArgsT<float> ab = a2;
   ab.cell_list = c->d_boundary;
   ab.n_proc = c->n_boundary;
   return launch(ab);

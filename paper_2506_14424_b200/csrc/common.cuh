@@ -81,6 +81,11 @@ struct ApplyArgsT {  // R = double (operators) or float (FP32 multigrid levels, 
   const R* npc;        // [n_owned][7][n^3]  S0 (6), g at cell points
   const R* npf;        // [n_total][6][10][n^2]  S0 (6), g, u0 trace (3) at own face points
   double alpha_c;
+  // multi-rank with a communicator: ghost neighbours' face traces instead of whole ghost cells.
+  // gtr[((item * NC + c) * 2 + {0: value, 1: d/dxi_n}) * n^2 + face point], item = gslot[g * 6 + f]
+  // for ghost g's face f (null: traces computed from the ghost cells in `ghost`)
+  const R* gtr;
+  const int* gslot;
 };
 using ApplyArgs = ApplyArgsT<double>;
 

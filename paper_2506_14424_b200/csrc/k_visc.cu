@@ -151,6 +151,64 @@ cudaError_t launch_apply_oseen(int n, int geo, const ApplyArgs& a, cudaStream_t 
   }
 }
 
+// Face traces of owned cells for the ghost exchange: for every listed
+// (cell, face) item the value and the reference normal derivative of each component at the face's
+// n^2 points, out[((item * NC + c) * 2 + {0, 1}) * n^2 + p].  The line of point p = a + n b and the
+// fma order are those of the apply kernel's own neighbour-trace loop, so a rank that reads these
+// traces computes bit for bit what a single context computes from the neighbour's cell data.
+template <typename R, int n, int NC>
+__global__ void pack_traces_kernel(const R* __restrict__ src, const int* __restrict__ cells,
+                                   const int* __restrict__ faces, int n_items, R* __restrict__ out) {
+  constexpr int n2 = n * n, n3 = n * n * n;
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long)n_items * NC * n2) return;
+  const int p = (int)(t % n2);
+  const int c = (int)((t / n2) % NC);
+  const int it = (int)(t / ((long)n2 * NC));
+  const int f = faces[it], d = f >> 1;
+  const int a = p % n, b = p / n;
+  const R* u = src + (size_t)cells[it] * NC * n3 + c * n3;
+  const Tab1D& T = c_tab[n];
+  const double* lO = (f & 1) ? T.l1 : T.l0;
+  const double* dO = (f & 1) ? T.d1 : T.d0;
+  R x[n];
+#pragma unroll
+  for (int i = 0; i < n; ++i)
+    x[i] = d == 0 ? u[b * n2 + a * n + i] : d == 1 ? u[b * n2 + i * n + a] : u[i * n2 + p];
+  R v = R(0.0), g = R(0.0);
+#pragma unroll
+  for (int i = 0; i < n; ++i) { v = fma(R(lO[i]), x[i], v); g = fma(R(dO[i]), x[i], g); }
+  out[((size_t)(it * NC + c) * 2) * n2 + p] = v;
+  out[((size_t)(it * NC + c) * 2 + 1) * n2 + p] = g;
+}
+
+template <typename R>
+static cudaError_t pack_traces_t(int nc, int n, const R* src, const int* cells, const int* faces, int n_items,
+                                 R* out, cudaStream_t s) {
+  if (n_items <= 0) return cudaSuccess;
+  const long tot = (long)n_items * nc * n * n;
+  const int blocks = (int)((tot + 255) / 256);
+#define DGVV_PT(N)                                                                                      \
+  case N:                                                                                               \
+    if (nc == 3) pack_traces_kernel<R, N, 3><<<blocks, 256, 0, s>>>(src, cells, faces, n_items, out);   \
+    else pack_traces_kernel<R, N, 1><<<blocks, 256, 0, s>>>(src, cells, faces, n_items, out);           \
+    break;
+  switch (n) {
+    DGVV_PT(2) DGVV_PT(3) DGVV_PT(4) DGVV_PT(5) DGVV_PT(6) DGVV_PT(7)
+    default: return cudaErrorNotSupported;
+  }
+#undef DGVV_PT
+  return cudaGetLastError();
+}
+cudaError_t launch_pack_traces(int nc, int n, const double* src, const int* cells, const int* faces, int n_items,
+                               double* out, cudaStream_t s) {
+  return pack_traces_t<double>(nc, n, src, cells, faces, n_items, out, s);
+}
+cudaError_t launch_pack_traces_f(int nc, int n, const float* src, const int* cells, const int* faces, int n_items,
+                                 float* out, cudaStream_t s) {
+  return pack_traces_t<float>(nc, n, src, cells, faces, n_items, out, s);
+}
+
 cudaError_t launch_apply_visc(int n, int form, int geo, const ApplyArgs& a, cudaStream_t s) {
   return launch_visc_t<double>(n, form, geo, a, s);
 }

@@ -99,6 +99,11 @@ cudaError_t launch_lanczos_update(double* w, const double* q, const double* qpre
                                   const double* beta_prev, long n, cudaStream_t s);
 cudaError_t launch_axpy_dev(const double* coef, double sgn, const double* x, double* y, long n, cudaStream_t s);
 cudaError_t launch_scale_by_inv(const double* w, const double* s2, double* q, long n, cudaStream_t s);
+// a5: face traces (value, d/dxi_n) of listed (cell, face) items for the ghost exchange
+cudaError_t launch_pack_traces(int nc, int n, const double* src, const int* cells, const int* faces, int n_items,
+                               double* out, cudaStream_t s);
+cudaError_t launch_pack_traces_f(int nc, int n, const float* src, const int* cells, const int* faces, int n_items,
+                                 float* out, cudaStream_t s);
 cudaError_t launch_gather_cells_f(const float* src, const int* list, int ncells, int len, float* out,
                                   cudaStream_t s);
 cudaError_t launch_gather_cells(const double* src, const int* list, int ncells, int len, double* out,

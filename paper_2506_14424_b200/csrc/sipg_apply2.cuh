@@ -388,6 +388,12 @@ sipg_apply2_kernel(const ApplyArgsT<R> A) {
         const R* pn = nbv < A.n_owned ? A.src + (size_t)nbv * NC * n3
                                            : A.ghost + (size_t)(nbv - A.n_owned) * NC * n3;
         const R* ns = smem + (in_cta ? sl : 0) * Cf::CS;
+        if (A.gtr && nbv >= A.n_owned) {          // exchanged face traces of the ghost neighbour
+          const R* tr = A.gtr + (size_t)A.gslot[(nbv - A.n_owned) * 6 + ((2 * d + s) ^ 1)] * NC * 2 * n2 + p;
+#pragma unroll
+          for (int c = 0; c < NC; ++c) { up[s][c] = tr[2 * c * n2]; dp[s][c] = tr[(2 * c + 1) * n2]; }
+          continue;
+        }
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
           R x[n];

@@ -352,6 +352,12 @@ class Context:
         return out.value
 
     # ------------------------------------------------------------------ ghosts (multi-GPU)
+    def exchange_bytes(self, op=0, level=0):
+        """(sent, received) bytes of one apply's face-trace exchange (dgvv_exchange_bytes)."""
+        a, b = C.c_int64(), C.c_int64()
+        A.check(self._L.dgvv_exchange_bytes(self.h, level, op, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
     def ghost_layout(self):
         """[(peer rank, send count, recv count)] in peer order."""
         n = C.c_int32()

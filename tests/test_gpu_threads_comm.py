@@ -89,6 +89,11 @@ def test_thread_group_viscous_and_poisson_apply(name, mk, k, R):
         yp = torch.empty_like(xp)
         ctx.apply_poisson(xp, yp)
         d = ctx.dot(x, x, 3)                   # allreduced
+        # a5: the exchange moves face traces, 2 NC n^2 doubles per cut face (not NC n^3 per cell)
+        sent, recv = ctx.exchange_bytes(0)
+        cut = sum(1 for cc in range(p.n_owned) for f in range(6)
+                  if p.neighbor[cc, f] >= 0 and not (p.first <= p.neighbor[cc, f] < p.first + p.n_owned))
+        assert sent == cut * 2 * 3 * (k + 1) ** 2 * 8 and recv > 0
         return y.cpu(), yp.cpu(), d
 
     parts, out = run_ranks(m, R, k, body, visc_law=laws.C2_LAW, poisson_law=laws.C4_LAW)
