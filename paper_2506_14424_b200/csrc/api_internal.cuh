@@ -619,6 +619,7 @@ dgvv_status run_apply(dgvv_ctx* c, int op, int l, ApplyArgs a, cudaStream_t s, i
   ApplyArgs ai = a;
   ai.cell_list = c->d_interior;
   ai.n_proc = c->n_interior;
+  ai.gtr = nullptr;                           // interior cells never read a ghost: plain kernel
   TRY(launch(ai));
   DGVV_CUDA_TRY(cudaStreamWaitEvent(s, c->ev_comm, 0));
   ApplyArgs ab = a;

@@ -231,6 +231,7 @@ DGVV_INTERNAL dgvv_status run_apply_f(dgvv_ctx* c, int op, int l, const ApplyArg
   ApplyArgsT<float> ai = a2;
   ai.cell_list = c->d_interior;
   ai.n_proc = c->n_interior;
+  ai.gtr = nullptr;
   TRY(launch(ai));
   DGVV_CUDA_TRY(cudaStreamWaitEvent(s, c->ev_comm, 0));
   ApplyArgsT<float> ab = a2;

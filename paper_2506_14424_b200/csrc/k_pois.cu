@@ -66,11 +66,14 @@ static cudaError_t run(const ApplyArgsT<R>& a, cudaStream_t s) {
   const size_t smem = (size_t)CPB * Apply2Cfg<n, 1, 1, GEO>::CS * sizeof(R);
   auto k0 = sipg_apply2_kernel<R, n, 1, 1, GEO, CPB, minb_pois_t<R, n>(), false>;
   auto k1 = sipg_apply2_kernel<R, n, 1, 1, GEO, CPB, minb_pois_t<R, n>(), true>;
+  auto k0t = sipg_apply2_kernel<R, n, 1, 1, GEO, CPB, minb_pois_t<R, n>(), false, false, true>;
+  auto k1t = sipg_apply2_kernel<R, n, 1, 1, GEO, CPB, minb_pois_t<R, n>(), true, false, true>;
   static std::atomic<uint64_t> attr{0};
-  if (cudaError_t e = smem_optin(attr, smem, k0, k1); e != cudaSuccess) return e;
+  if (cudaError_t e = smem_optin(attr, smem, k0, k1, k0t, k1t); e != cudaSuccess) return e;
   if (a.n_proc <= 0) return cudaSuccess;
   const int grid = (a.n_proc + CPB - 1) / CPB;
-  if (a.mass != 0.0) k1<<<grid, CPB * n * n, smem, s>>>(a);
+  if (a.gtr) (a.mass != 0.0 ? k1t : k0t)<<<grid, CPB * n * n, smem, s>>>(a);
+  else if (a.mass != 0.0) k1<<<grid, CPB * n * n, smem, s>>>(a);
   else k0<<<grid, CPB * n * n, smem, s>>>(a);
   return cudaGetLastError();
 }

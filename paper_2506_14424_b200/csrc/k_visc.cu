@@ -100,11 +100,16 @@ static cudaError_t run(const ApplyArgsT<R>& a, cudaStream_t s) {
   // the Helmholtz mass term is a separate instantiation: the plain operator pays nothing for it
   auto k0 = sipg_apply2_kernel<R, n, NC, FORM, GEO, CPB, minb_visc_t<R, n, GEO>(), false>;
   auto k1 = sipg_apply2_kernel<R, n, NC, FORM, GEO, CPB, minb_visc_t<R, n, GEO>(), true>;
+  // ghost face traces (communicator mode, boundary cells): a separate instantiation, so the
+  // single-GPU / interior kernel carries no branch for them (measured: +4 % at C5 otherwise)
+  auto k0t = sipg_apply2_kernel<R, n, NC, FORM, GEO, CPB, minb_visc_t<R, n, GEO>(), false, false, true>;
+  auto k1t = sipg_apply2_kernel<R, n, NC, FORM, GEO, CPB, minb_visc_t<R, n, GEO>(), true, false, true>;
   static std::atomic<uint64_t> attr{0};
-  if (cudaError_t e = smem_optin(attr, smem, k0, k1); e != cudaSuccess) return e;
+  if (cudaError_t e = smem_optin(attr, smem, k0, k1, k0t, k1t); e != cudaSuccess) return e;
   if (a.n_proc <= 0) return cudaSuccess;
   const int grid = (a.n_proc + CPB - 1) / CPB;
-  if (a.mass != 0.0) k1<<<grid, CPB * n * n, smem, s>>>(a);
+  if (a.gtr) (a.mass != 0.0 ? k1t : k0t)<<<grid, CPB * n * n, smem, s>>>(a);
+  else if (a.mass != 0.0) k1<<<grid, CPB * n * n, smem, s>>>(a);
   else k0<<<grid, CPB * n * n, smem, s>>>(a);
   return cudaGetLastError();
 }
@@ -133,10 +138,11 @@ static cudaError_t run_oseen(const ApplyArgs& a, cudaStream_t s) {
   constexpr int CPB = cpb_visc<n, GEO>();
   const size_t smem = (size_t)CPB * Apply2Cfg<n, 3, 0, GEO>::CS * sizeof(double);
   auto k = sipg_apply2_kernel<double, n, 3, 0, GEO, CPB, minb_visc<n, GEO>(), true, true>;
+  auto kt = sipg_apply2_kernel<double, n, 3, 0, GEO, CPB, minb_visc<n, GEO>(), true, true, true>;
   static std::atomic<uint64_t> attr{0};
-  if (cudaError_t e = smem_optin(attr, smem, k); e != cudaSuccess) return e;
+  if (cudaError_t e = smem_optin(attr, smem, k, kt); e != cudaSuccess) return e;
   if (a.n_proc <= 0) return cudaSuccess;
-  k<<<(a.n_proc + CPB - 1) / CPB, CPB * n * n, smem, s>>>(a);
+  (a.gtr ? kt : k)<<<(a.n_proc + CPB - 1) / CPB, CPB * n * n, smem, s>>>(a);
   return cudaGetLastError();
 }
 

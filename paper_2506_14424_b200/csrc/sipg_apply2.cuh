@@ -138,7 +138,7 @@ __device__ __forceinline__ R rowdot(const R* __restrict__ r, const R (&w)[n]) {
   return s;
 }
 
-template <typename R, int n, int NC, int FORM, int GEO, int CPB, int MINB, bool MASS, bool CONV = false>
+template <typename R, int n, int NC, int FORM, int GEO, int CPB, int MINB, bool MASS, bool CONV = false, bool GTR = false>
 __global__ void __launch_bounds__(CPB * n * n, MINB)
 sipg_apply2_kernel(const ApplyArgsT<R> A) {
   static_assert(FORM == 1 || NC == 3, "divergence form needs 3 components");
@@ -388,7 +388,7 @@ sipg_apply2_kernel(const ApplyArgsT<R> A) {
         const R* pn = nbv < A.n_owned ? A.src + (size_t)nbv * NC * n3
                                            : A.ghost + (size_t)(nbv - A.n_owned) * NC * n3;
         const R* ns = smem + (in_cta ? sl : 0) * Cf::CS;
-        if (A.gtr && nbv >= A.n_owned) {          // exchanged face traces of the ghost neighbour
+        if (GTR && nbv >= A.n_owned) {            // exchanged face traces of the ghost neighbour (boundary launch)
           const R* tr = A.gtr + (size_t)A.gslot[(nbv - A.n_owned) * 6 + ((2 * d + s) ^ 1)] * NC * 2 * n2 + p;
 #pragma unroll
           for (int c = 0; c < NC; ++c) { up[s][c] = tr[2 * c * n2]; dp[s][c] = tr[(2 * c + 1) * n2]; }
