@@ -206,6 +206,7 @@ DGVV_INTERNAL dgvv_status setup_impl(const dgvv_mesh* m, int32_t degree, const d
   if (c->geo == 0) {
     TRY(dalloc(c, &c->d_cart, (size_t)c->n_total * CART_STRIDE));
     DGVV_CUDA_TRY(launch_cart_geom(c->d_nodes, c->d_nbr, c->n_total, c->d_cart, s));
+    DGVV_CUDA_TRY(launch_cart_face(c->d_nbr, c->n_owned, c->d_cart, s));
   }
 
   // ---- per level: geometry, points, coefficients

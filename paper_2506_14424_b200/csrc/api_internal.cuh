@@ -734,9 +734,9 @@ DGVV_INTERNAL dgvv_status setup_impl(const dgvv_mesh* m, int32_t degree, const d
                               const dgvv_options* opt, cudaStream_t s, dgvv_ctx* c);
 DGVV_INTERNAL dgvv_status host_pipe_setup(dgvv_ctx* c, int level);
 DGVV_INTERNAL dgvv_status cheb_impl(dgvv_ctx* c, int op, int l, double* x, const double* b, int degree, double lo,
-                             double hi, int x_is_zero, double* work, cudaStream_t s);
+                             double hi, int x_is_zero, double* work, cudaStream_t s, int start_in_work = 0);
 DGVV_INTERNAL dgvv_status transfer(dgvv_ctx* c, int op, int fl, const double* in, double* out, double beta, bool prol,
-                            cudaStream_t s);
+                            cudaStream_t s, const double* add = nullptr);
 DGVV_INTERNAL dgvv_status vcycle_rec(dgvv_ctx* c, int op, int l, const double* b, double* x, const double* his,
                               cudaStream_t s);
 DGVV_INTERNAL dgvv_status d2f_alloc(dgvv_ctx* c, float** dst, const double* src, long n, cudaStream_t s);
@@ -744,9 +744,9 @@ DGVV_INTERNAL dgvv_status ensure_fp32(dgvv_ctx* c, int op, cudaStream_t s);
 DGVV_INTERNAL ApplyArgsT<float> base_args_f(dgvv_ctx* c, int l, int op);
 DGVV_INTERNAL dgvv_status run_apply_f(dgvv_ctx* c, int op, int l, const ApplyArgsT<float>& a, cudaStream_t s);
 DGVV_INTERNAL dgvv_status cheb_impl_f(dgvv_ctx* c, int op, int l, float* x, const float* b, int degree, double lo,
-                               double hi, int x_is_zero, float* work, cudaStream_t s);
+                               double hi, int x_is_zero, float* work, cudaStream_t s, int start_in_work = 0);
 DGVV_INTERNAL dgvv_status transfer_f(dgvv_ctx* c, int op, int fl, const float* in, float* out, double beta, bool prol,
-                              cudaStream_t s);
+                              cudaStream_t s, const float* add = nullptr);
 DGVV_INTERNAL dgvv_status vcycle_rec_f(dgvv_ctx* c, int op, int l, const float* b, float* x, const double* his,
                                 cudaStream_t s);
 DGVV_INTERNAL dgvv_status vcycle_fp32_d(dgvv_ctx* c, int op, const double* r, double* z, const double* his, cudaStream_t s);

@@ -23,7 +23,8 @@ dgvv_status dgvv_inverse_diagonal(dgvv_ctx* c, int32_t op, int32_t level, double
 }
 
 DGVV_INTERNAL dgvv_status cheb_impl(dgvv_ctx* c, int op, int l, double* x, const double* b, int degree, double lo,
-                             double hi, int x_is_zero, double* work, cudaStream_t s) {
+                             double hi, int x_is_zero, double* work, cudaStream_t s,
+                             int start_in_work) {
   const int nc = op == DGVV_OP_VISCOUS ? 3 : 1;
   const long N = (long)nc * level_dofs(c, l);
   TRY(ensure_dinv(c, op, l, s));
@@ -38,10 +39,11 @@ DGVV_INTERNAL dgvv_status cheb_impl(dgvv_ctx* c, int op, int l, double* x, const
     cur = 0;
   } else {
     ApplyArgs a = base_args(c, l, op);
-    a.src = x; a.b = b; a.dinv = dinv; a.dvec = d; a.xout = work;
+    cur = start_in_work ? 1 : 0;         // the start iterate is in work (out-of-place prolongation-add)
+    a.src = bufs[cur]; a.b = b; a.dinv = dinv; a.dvec = d; a.xout = bufs[1 - cur];
     a.mode = MODE_CHEB; a.c_rho = 0.0; a.c_r = 1.0 / theta;
     TRY(run_apply(c, op, l, a, s));
-    cur = 1;
+    cur = 1 - cur;
   }
   for (int j = 1; j < degree; ++j) {
     const double rho_new = 1.0 / (2.0 * sigma - rho);
@@ -70,7 +72,7 @@ dgvv_status dgvv_chebyshev_smooth(dgvv_ctx* c, int32_t op, int32_t level, double
 }
 
 DGVV_INTERNAL dgvv_status transfer(dgvv_ctx* c, int op, int fl, const double* in, double* out, double beta, bool prol,
-                            cudaStream_t s) {
+                            cudaStream_t s, const double* add) {
   if (fl < 0 || fl + 1 >= (int)c->L.size()) return dgvv_fail(DGVV_EINVAL, "fine_level %d has no coarser level", fl);
   const int nc = op == DGVV_OP_VISCOUS ? 3 : 1;
   if (op != DGVV_OP_VISCOUS && op != DGVV_OP_POISSON) return dgvv_fail(DGVV_EINVAL, "op");
@@ -79,7 +81,7 @@ DGVV_INTERNAL dgvv_status transfer(dgvv_ctx* c, int op, int fl, const double* in
   transfer_matrix(nf, ncs, P1.data());
   if (prol) {
     M = P1;   // nout = nf, nin = nc
-    DGVV_CUDA_TRY(launch_tensor3(ncs, nf, nc, M.data(), in, out, beta, c->n_owned, s));
+    DGVV_CUDA_TRY(launch_tensor3(ncs, nf, nc, M.data(), in, out, beta, c->n_owned, s, add));
   } else {
     for (int i = 0; i < nf; ++i)
       for (int j = 0; j < ncs; ++j) M[(size_t)j * nf + i] = P1[(size_t)i * ncs + j];
@@ -127,7 +129,11 @@ DGVV_INTERNAL dgvv_status vcycle_rec(dgvv_ctx* c, int op, int l, const double* b
     auto& C = c->L[l + 1].scratch[oi];
     TRY(transfer(c, op, l, S[0], C[3], 0.0, false, s));
     TRY(vcycle_rec(c, op, l + 1, C[3], C[4], his, s));
-    TRY(transfer(c, op, l, C[4], x, 1.0, true, s));
+    // post-smoothing starts from x + P x_c written out of place into the work buffer: its 5
+    // ping-pong sweeps then end in x (no closing copy)
+    TRY(transfer(c, op, l, C[4], S[1], 1.0, true, s, x));
+    TRY(cheb_impl(c, op, l, x, b, 5, lo, hi, 0, S[1], s, 1));
+    return DGVV_OK;
   } else {                                     // h-coarsening into the coarser context
     TRY(hrestrict_impl(c, op, S[0], c->hb[oi], 0.0, s));
     TRY(vcycle_rec(c->coarse, op, 0, c->hb[oi], c->hx[oi], his + c->L.size(), s));
@@ -241,7 +247,8 @@ DGVV_INTERNAL dgvv_status run_apply_f(dgvv_ctx* c, int op, int l, const ApplyArg
 }
 
 DGVV_INTERNAL dgvv_status cheb_impl_f(dgvv_ctx* c, int op, int l, float* x, const float* b, int degree, double lo,
-                               double hi, int x_is_zero, float* work, cudaStream_t s) {
+                               double hi, int x_is_zero, float* work, cudaStream_t s,
+                             int start_in_work) {
   const int oi = op == DGVV_OP_VISCOUS ? 0 : 1;
   const int nc = op == DGVV_OP_VISCOUS ? 3 : 1;
   const long N = (long)nc * level_dofs(c, l);
@@ -256,10 +263,11 @@ DGVV_INTERNAL dgvv_status cheb_impl_f(dgvv_ctx* c, int op, int l, float* x, cons
     cur = 0;
   } else {
     ApplyArgsT<float> a = base_args_f(c, l, op);
-    a.src = x; a.b = b; a.dinv = dinv; a.dvec = d; a.xout = work;
+    cur = start_in_work ? 1 : 0;
+    a.src = bufs[cur]; a.b = b; a.dinv = dinv; a.dvec = d; a.xout = bufs[1 - cur];
     a.mode = MODE_CHEB; a.c_rho = 0.0; a.c_r = 1.0 / theta;
     TRY(run_apply_f(c, op, l, a, s));
-    cur = 1;
+    cur = 1 - cur;
   }
   for (int j = 1; j < degree; ++j) {
     const double rho_new = 1.0 / (2.0 * sigma - rho);
@@ -275,13 +283,13 @@ DGVV_INTERNAL dgvv_status cheb_impl_f(dgvv_ctx* c, int op, int l, float* x, cons
 }
 
 DGVV_INTERNAL dgvv_status transfer_f(dgvv_ctx* c, int op, int fl, const float* in, float* out, double beta, bool prol,
-                              cudaStream_t s) {
+                              cudaStream_t s, const float* add) {
   const int nc = op == DGVV_OP_VISCOUS ? 3 : 1;
   const int nf = c->L[fl].n, ncs = c->L[fl + 1].n;
   std::vector<double> P1((size_t)nf * ncs), M((size_t)nf * ncs);
   transfer_matrix(nf, ncs, P1.data());
   if (prol) {
-    DGVV_CUDA_TRY(launch_tensor3_f(ncs, nf, nc, P1.data(), in, out, beta, c->n_owned, s));
+    DGVV_CUDA_TRY(launch_tensor3_f(ncs, nf, nc, P1.data(), in, out, beta, c->n_owned, s, add));
   } else {
     for (int i = 0; i < nf; ++i)
       for (int j = 0; j < ncs; ++j) M[(size_t)j * nf + i] = P1[(size_t)i * ncs + j];
@@ -313,7 +321,9 @@ DGVV_INTERNAL dgvv_status vcycle_rec_f(dgvv_ctx* c, int op, int l, const float* 
     auto& C = c->LF[l + 1].scratch[oi];
     TRY(transfer_f(c, op, l, S[0], C[3], 0.0, false, s));
     TRY(vcycle_rec_f(c, op, l + 1, C[3], C[4], his, s));
-    TRY(transfer_f(c, op, l, C[4], x, 1.0, true, s));
+    TRY(transfer_f(c, op, l, C[4], S[1], 1.0, true, s, x));   // out of place, as vcycle_rec
+    TRY(cheb_impl_f(c, op, l, x, b, 5, lo, hi, 0, S[1], s, 1));
+    return DGVV_OK;
   } else {                                     // h-coarsening into the coarser context (f3)
     const int n = c->L.back().n;
     DGVV_CUDA_TRY(launch_hrestrict_f(n, nc, S[0], c->hbf[oi], c->d_child, 0.0, c->coarse->n_owned, s));

@@ -247,12 +247,13 @@ __global__ void diag_kernel(const DiagArgs A) {
 }
 
 // ============================================================ K7: tensor-product transfer
-// out[cell][c] = (M (x) M (x) M) in[cell][c] + beta out[cell][c];  M is nout x nin.
+// out[cell][c] = (M (x) M (x) M) in[cell][c] + beta add[cell][c];  M is nout x nin; add is out
+// (in place) or another vector (the V-cycle's out-of-place prolongation-add).
 // prolongation: M = P1 (nf x nc); restriction: M = P1^T; u_lin interpolation: M = I1.
 struct Mat8 { double m[DGVV_NMAX * DGVV_NMAX]; };
 
 template <typename R, int nin, int nout, int NC, int CPB>
-__global__ void __launch_bounds__(CPB * 64) tensor3_kernel(Mat8 M, const R* in, R* out, R beta, int n_cells) {
+__global__ void __launch_bounds__(CPB * 64) tensor3_kernel(Mat8 M, const R* in, R* out, const R* add, R beta, int n_cells) {
   constexpr int ni3 = nin * nin * nin, no3 = nout * nout * nout;
   constexpr int S1 = nin * nin * nout, S2 = nin * nout * nout;
   constexpr int CS = ni3 + S1 + S2;
@@ -291,7 +292,7 @@ __global__ void __launch_bounds__(CPB * 64) tensor3_kernel(Mat8 M, const R* in, 
 #pragma unroll
         for (int k = 0; k < nin; ++k) acc += R(M.m[zo * nin + k]) * s2[k * nout * nout + r];
         const size_t o = ((size_t)cell * NC + c) * no3 + i;
-        out[o] = (beta == R(0)) ? acc : acc + beta * out[o];
+        out[o] = (beta == R(0)) ? acc : acc + beta * add[o];
       }
     __syncthreads();
   }

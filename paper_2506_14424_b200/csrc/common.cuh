@@ -31,7 +31,11 @@ struct Tab1D {
 
 // Per-cell geometry of the Cartesian fast path (axis-aligned boxes):
 //   [0..2] 1/h_x,1/h_y,1/h_z  [3] H_K  [4] h_x h_y h_z  [5..7] x0   (8 doubles)
-#define CART_STRIDE 8
+// Cartesian cell record: [1/hx 1/hy 1/hz H V x0 y0 z0 | per face f: 1/h_d of the neighbour across f,
+// max(H, H_neighbour)] (own values on boundary faces): the face terms read their neighbour data
+// from the cell's own record instead of chasing the neighbour's (ncu: 3 % of stall samples)
+#define CART_STRIDE 20
+#define CART_FACE 8
 
 // Streamed metric terms of the general (iso-parametric) path, per level:
 //   vJi[cell][9][n^3]     : Ji[k][j] = d xi_k / d x_j at cell points (row-major k,j)
@@ -170,6 +174,18 @@ inline uint64_t current_device_bit() {
   int d = 0;
   cudaGetDevice(&d);
   return 1ull << (d & 63);
+}
+// SM count of the current device (persistent launches), cached per device
+inline int sm_count() {
+  static std::atomic<int> cache[64];
+  int d = 0;
+  cudaGetDevice(&d);
+  int v = cache[d & 63].load(std::memory_order_relaxed);
+  if (v <= 0) {
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d) != cudaSuccess || v <= 0) v = 148;
+    cache[d & 63].store(v, std::memory_order_relaxed);
+  }
+  return v;
 }
 template <typename... K>
 inline cudaError_t smem_optin(std::atomic<uint64_t>& done, size_t smem, K... ks) {

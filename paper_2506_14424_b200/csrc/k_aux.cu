@@ -71,59 +71,66 @@ cudaError_t launch_diag(int nc, int n, int form, int geo, const DiagArgs& a, cud
 #define T3CPB 2
 #endif
 template <typename R, int nin, int nout>
-static cudaError_t t3_run(int nc, const Mat8& M, const R* in, R* out, double beta, int ncells, cudaStream_t s) {
+static cudaError_t t3_run(int nc, const Mat8& M, const R* in, R* out, const R* add, double beta, int ncells, cudaStream_t s) {
   constexpr int CPB = T3CPB;   // cells per CTA (64 threads each)
   constexpr int CS = nin * nin * nin + nin * nin * nout + nin * nout * nout;
   const size_t smem = (size_t)CPB * CS * sizeof(R);
   if (ncells <= 0) return cudaSuccess;
   const int grid = (ncells + CPB - 1) / CPB;
-  if (nc == 3) tensor3_kernel<R, nin, nout, 3, CPB><<<grid, CPB * 64, smem, s>>>(M, in, out, (R)beta, ncells);
-  else tensor3_kernel<R, nin, nout, 1, CPB><<<grid, CPB * 64, smem, s>>>(M, in, out, (R)beta, ncells);
+  if (nc == 3) tensor3_kernel<R, nin, nout, 3, CPB><<<grid, CPB * 64, smem, s>>>(M, in, out, add, (R)beta, ncells);
+  else tensor3_kernel<R, nin, nout, 1, CPB><<<grid, CPB * 64, smem, s>>>(M, in, out, add, (R)beta, ncells);
   return cudaGetLastError();
 }
 
 template <typename R, int nin>
-static cudaError_t t3_in(int nout, int nc, const Mat8& M, const R* in, R* out, double beta, int ncells,
-                         cudaStream_t s) {
+static cudaError_t t3_in(int nout, int nc, const Mat8& M, const R* in, R* out, const R* add, double beta,
+                         int ncells, cudaStream_t s) {
   switch (nout) {
-    case 2: return t3_run<R, nin, 2>(nc, M, in, out, beta, ncells, s);
-    case 3: return t3_run<R, nin, 3>(nc, M, in, out, beta, ncells, s);
-    case 4: return t3_run<R, nin, 4>(nc, M, in, out, beta, ncells, s);
-    case 5: return t3_run<R, nin, 5>(nc, M, in, out, beta, ncells, s);
-    case 6: return t3_run<R, nin, 6>(nc, M, in, out, beta, ncells, s);
-    case 7: return t3_run<R, nin, 7>(nc, M, in, out, beta, ncells, s);
+    case 2: return t3_run<R, nin, 2>(nc, M, in, out, add, beta, ncells, s);
+    case 3: return t3_run<R, nin, 3>(nc, M, in, out, add, beta, ncells, s);
+    case 4: return t3_run<R, nin, 4>(nc, M, in, out, add, beta, ncells, s);
+    case 5: return t3_run<R, nin, 5>(nc, M, in, out, add, beta, ncells, s);
+    case 6: return t3_run<R, nin, 6>(nc, M, in, out, add, beta, ncells, s);
+    case 7: return t3_run<R, nin, 7>(nc, M, in, out, add, beta, ncells, s);
     default: return cudaErrorInvalidValue;
   }
 }
 
 template <typename R>
 static cudaError_t tensor3_t(int nin, int nout, int nc, const double* M, const R* in, R* out, double beta,
-                             int ncells, cudaStream_t s) {
+                             int ncells, cudaStream_t s, const R* add) {
+  if (!add) add = out;
   Mat8 m;
   for (int i = 0; i < DGVV_NMAX * DGVV_NMAX; ++i) m.m[i] = 0.0;
   for (int i = 0; i < nin * nout; ++i) m.m[i] = M[i];
   switch (nin) {
-    case 2: return t3_in<R, 2>(nout, nc, m, in, out, beta, ncells, s);
-    case 3: return t3_in<R, 3>(nout, nc, m, in, out, beta, ncells, s);
-    case 4: return t3_in<R, 4>(nout, nc, m, in, out, beta, ncells, s);
-    case 5: return t3_in<R, 5>(nout, nc, m, in, out, beta, ncells, s);
-    case 6: return t3_in<R, 6>(nout, nc, m, in, out, beta, ncells, s);
-    case 7: return t3_in<R, 7>(nout, nc, m, in, out, beta, ncells, s);
+    case 2: return t3_in<R, 2>(nout, nc, m, in, out, add, beta, ncells, s);
+    case 3: return t3_in<R, 3>(nout, nc, m, in, out, add, beta, ncells, s);
+    case 4: return t3_in<R, 4>(nout, nc, m, in, out, add, beta, ncells, s);
+    case 5: return t3_in<R, 5>(nout, nc, m, in, out, add, beta, ncells, s);
+    case 6: return t3_in<R, 6>(nout, nc, m, in, out, add, beta, ncells, s);
+    case 7: return t3_in<R, 7>(nout, nc, m, in, out, add, beta, ncells, s);
     default: return cudaErrorInvalidValue;
   }
 }
 cudaError_t launch_tensor3(int nin, int nout, int nc, const double* M, const double* in, double* out,
-                           double beta, int ncells, cudaStream_t s) {
-  return tensor3_t<double>(nin, nout, nc, M, in, out, beta, ncells, s);
+                           double beta, int ncells, cudaStream_t s, const double* add) {
+  return tensor3_t<double>(nin, nout, nc, M, in, out, beta, ncells, s, add);
 }
 cudaError_t launch_tensor3_f(int nin, int nout, int nc, const double* M, const float* in, float* out,
-                             double beta, int ncells, cudaStream_t s) {
-  return tensor3_t<float>(nin, nout, nc, M, in, out, beta, ncells, s);
+                             double beta, int ncells, cudaStream_t s, const float* add) {
+  return tensor3_t<float>(nin, nout, nc, M, in, out, beta, ncells, s, add);
 }
 
 // ---------------------------------------------------------------- setup
 cudaError_t launch_cart_geom(const double* nodes, const int* nbr, int n_total, double* cart, cudaStream_t s) {
   cart_geom_kernel<<<nblk(n_total), 256, 0, s>>>(nodes, nbr, n_total, cart);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cart_face(const int* nbr, int n_cells, double* cart, cudaStream_t s) {
+  if (n_cells <= 0) return cudaSuccess;
+  cart_face_kernel<<<nblk(n_cells), 256, 0, s>>>(nbr, n_cells, cart);
   return cudaGetLastError();
 }
 

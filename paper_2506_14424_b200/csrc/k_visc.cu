@@ -106,6 +106,13 @@ static cudaError_t run(const ApplyArgsT<R>& a, cudaStream_t s) {
   auto k1t = sipg_apply2_kernel<R, n, NC, FORM, GEO, CPB, minb_visc_t<R, n, GEO>(), true, false, true>;
   static std::atomic<uint64_t> attr{0};
   if (cudaError_t e = smem_optin(attr, smem, k0, k1, k0t, k1t); e != cudaSuccess) return e;
+#ifdef DGVV_CARVEOUT
+  static std::atomic<uint64_t> attr_co{0};
+  if (!(attr_co.load() & current_device_bit())) {
+    cudaFuncSetAttribute(k0, cudaFuncAttributePreferredSharedMemoryCarveout, DGVV_CARVEOUT);
+    attr_co.fetch_or(current_device_bit());
+  }
+#endif
   if (a.n_proc <= 0) return cudaSuccess;
   const int grid = (a.n_proc + CPB - 1) / CPB;
   if (a.gtr) (a.mass != 0.0 ? k1t : k0t)<<<grid, CPB * n * n, smem, s>>>(a);

@@ -61,14 +61,15 @@ cudaError_t launch_newton(int n, int geo, const ApplyArgs& a, cudaStream_t s);
 cudaError_t launch_carreau(int n, int geo, const NuArgs& a, cudaStream_t s);
 // K5: inverse diagonal
 cudaError_t launch_diag(int nc, int n, int form, int geo, const DiagArgs& a, cudaStream_t s);
-// K7: out = (M x M x M) in + beta out
+// K7: out = (M x M x M) in + beta add  (add = out when null)
 cudaError_t launch_tensor3(int nin, int nout, int nc, const double* M, const double* in, double* out,
-                           double beta, int ncells, cudaStream_t s);
+                           double beta, int ncells, cudaStream_t s, const double* add = nullptr);
 cudaError_t launch_tensor3_f(int nin, int nout, int nc, const double* M, const float* in, float* out,
-                             double beta, int ncells, cudaStream_t s);
+                             double beta, int ncells, cudaStream_t s, const float* add = nullptr);
 
 // setup kernels
 cudaError_t launch_cart_geom(const double* nodes, const int* nbr, int n_total, double* cart, cudaStream_t s);
+cudaError_t launch_cart_face(const int* nbr, int n_cells, double* cart, cudaStream_t s);
 cudaError_t launch_cart_points(const double* cart, int n_owned, int n_total, int n, double* xq, double* xf,
                                cudaStream_t s);
 cudaError_t launch_gen_geom(const GeoTab& g, const double* nodes, int n_total, double* vJi, double* jxw,

@@ -30,6 +30,19 @@ __global__ void cart_geom_kernel(const double* nodes, const int* nbr, int n_tota
   o[5] = x0[0]; o[6] = x0[1]; o[7] = x0[2];
 }
 
+// per-face neighbour data of the Cartesian record (after cart_geom_kernel: reads the neighbours')
+__global__ void cart_face_kernel(const int* nbr, int n_cells, double* cart) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n_cells) return;
+  double* o = cart + (size_t)c * CART_STRIDE;
+  for (int f = 0; f < 6; ++f) {
+    const int nb = nbr[c * 6 + f];
+    const double* q = cart + (size_t)(nb >= 0 ? nb : c) * CART_STRIDE;
+    o[CART_FACE + 2 * f] = q[f / 2];
+    o[CART_FACE + 2 * f + 1] = fmax(o[3], q[3]);
+  }
+}
+
 // physical points for Cartesian cells: xq [cell][n^3][3], xf [cell][6][n^2][3]
 __global__ void cart_points_kernel(const double* cart, int n_owned, int n_total, int n, Tab1D T,
                                    double* xq, double* xf) {

@@ -37,6 +37,12 @@
 #ifndef DGVV_NU_EARLY
 #define DGVV_NU_EARLY 1       // Cartesian: load the column's cell-point coefficients with the column
 #endif
+#ifndef DGVV_CARTF
+#define DGVV_CARTF 1          // Cartesian: neighbour 1/h_d and max(H, H_nb) from the cell's own record
+#endif
+#ifndef DGVV_NB_L2PF
+#define DGVV_NB_L2PF 1        // L2 prefetch (per-thread lines) of neighbours more than one resident wave ahead
+#endif
 #ifndef DGVV_QUAD_SWIZZLE
 #define DGVV_QUAD_SWIZZLE 1   // n = 4: lane quads cover 2 x 2 blocks of columns (see the kernel)
 #endif
@@ -254,6 +260,22 @@ sipg_apply2_kernel(const ApplyArgsT<R> A) {
   int nbf[6];
 #pragma unroll
   for (int f = 0; f < 6; ++f) nbf[f] = __ldg(A.nbr + cell * 6 + f);
+  if constexpr (DGVV_NB_L2PF != 0 && n != 4) {
+    // L2 prefetch of the neighbour blocks more than one resident wave (148 SMs x MINB CTAs x CPB
+    // cells) ahead in the cell order: no resident CTA has requested them yet, so their face lines
+    // would come from HBM (+z on C3's 64^3 cube, 4096 cells ahead: C3 -1.3 %).  Nearer ones are
+    // being loaded by their own CTA; prefetching those measured slower (C5 +x, 2048 ahead: +0.7 %).
+    // One 128-B line per thread.  Not built for n = 4: the code alone costs C5 1.2 % (registers).
+    constexpr int BLK = NC * n3 * (int)sizeof(R), NL = (BLK + 127) / 128, WAVE = 148 * MINB * CPB;
+#pragma unroll
+    for (int f = 0; f < 6; ++f) {
+      const int nbv = nbf[f];
+      if (nbv > cell + WAVE && nbv < A.n_owned) {
+        const char* base = reinterpret_cast<const char*>(A.src + (size_t)nbv * NC * n3);
+        for (int l = p; l < NL; l += n2) asm volatile("prefetch.global.L2 [%0];" ::"l"(base + 128 * l));
+      }
+    }
+  }
   if constexpr (Cf::STAGE) {
     if (p == 0) {
       mbar_init(&mbar[lc], 1);
@@ -362,9 +384,17 @@ sipg_apply2_kernel(const ApplyArgsT<R> A) {
     if constexpr (GEO == 0 && DGVV_NBCART_EARLY) {
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
-        const int nbv = nbf[2 * d + s];
-        const R* cg = A.cart + (size_t)(nbv >= 0 ? nbv : cell) * CART_STRIDE;
-        ihq[s][0] = cg[0]; ihq[s][1] = cg[1]; ihq[s][2] = cg[2]; Hq[s] = cg[3];
+        if constexpr (DGVV_CARTF) {
+          // from this cell's own record: the neighbour's 1/h_d and max(H, H_nb) (a conforming
+          // neighbour shares the tangential extents)
+          const R* cf = A.cart + (size_t)cell * CART_STRIDE + CART_FACE + 2 * (2 * d + s);
+          ihq[s][0] = ih[0]; ihq[s][1] = ih[1]; ihq[s][2] = ih[2];
+          ihq[s][d] = cf[0]; Hq[s] = cf[1];
+        } else {
+          const int nbv = nbf[2 * d + s];
+          const R* cg = A.cart + (size_t)(nbv >= 0 ? nbv : cell) * CART_STRIDE;
+          ihq[s][0] = cg[0]; ihq[s][1] = cg[1]; ihq[s][2] = cg[2]; Hq[s] = cg[3];
+        }
       }
     }
 
@@ -522,7 +552,6 @@ sipg_apply2_kernel(const ApplyArgsT<R> A) {
       R gt1[NT > 0 ? NT : 1], gt2[NT > 0 ? NT : 1];
       if constexpr (GEO == 0) {
         // ---------------- Cartesian: n = sgn e_d, J^-1 = diag(1/h)
-        const R sgn = s ? R(1.0) : -R(1.0);
         R num, nup, Hp = Hm;
         if constexpr (Cf::TMAC) {
           if (dd == 0 && s == 0) mbar_wait(&mbar[lc], 0);
@@ -542,38 +571,44 @@ sipg_apply2_kernel(const ApplyArgsT<R> A) {
           if constexpr (Cf::TMAC) nup = stg[(6 + f) * n2 + p];
           else nup = A.nu_face[((size_t)nbv * 6 + (f ^ 1)) * n2 + p];
         }
-        const R dA = R(T.w[a]) * R(T.w[b]) * vol * ih[d];
-        const R tau = R(A.pen) * fmax(Hm, Hp) * R(0.5) * (num + nup);
-        R Sm[NC], Sp[NC];
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          const R gnm = dm[s][c] * ih[d], gnp = dp[s][c] * ihp[d];
-          if constexpr (FORM == 0) {
-            if (c == d) { Sm[c] = gnm; Sp[c] = gnp; }
-            else {
-              const bool c_is_t1 = (c == t1);
-              const R gtm = (c_is_t1 ? tm1[0] : tm2[0]) * ih[c];
-              const R gtp = (c_is_t1 ? tp1[0] : tp2[0]) * ihp[c];
-              Sm[c] = R(0.5) * (gnm + gtm);
-              Sp[c] = R(0.5) * (gnp + gtp);
-            }
-          } else {
-            Sm[c] = R(0.5) * gnm;
-            Sp[c] = R(0.5) * gnp;
-          }
-        }
+        // The SIPG flux at this face point with every per-point product folded into six scalars
+        // (the same terms as PAPER.md:1055-1111 in the order of DESIGN.md §6 "K1 Cartesian flux"):
+        // with sdA = sgn w_a w_b |F| and tau = pen max(H-, H+) ({{nu}}):
+        //   fv_d = 2 tau dA [u_d] - (B1 du_d- + B2 du_d+),  gn_d = -B1 [u_d]      (normal component)
+        //   fv_c = tau dA [u_c] - (hB1 du_c- + hB2 du_c+ + hA1_c dt_c u_d- + hA2_c dt_c u_d+),
+        //   gn_c = -hB1 [u_c],  gt_c = -hA1_c [u_c]                              (tangential, c != d)
+        // B1 = sdA nu- /h_d, B2 = sdA nu+ /h_d+, hB = B / 2, hA1_c = sdA nu- /(2 h_c), hA2_c = sdA nu+ /(2 h_c);
+        // Laplace form: fv_c = tau dA [u_c] - (hB1 du_c- + hB2 du_c+), gn_c = -hB1 [u_c].
+        const R dA = R(T.w[a]) * R(T.w[b]) * (vol * ih[d]);
+        const R sdA = s ? dA : -dA;
+        const R Hx = (DGVV_CARTF && DGVV_NBCART_EARLY) ? Hp : fmax(Hm, Hp);   // CARTF: Hp = max(H, H_nb)
+        const R dAt = (dA * (R(0.5) * R(A.pen)) * Hx) * (num + nup);
+        const R A1 = sdA * num, A2 = sdA * nup;
+        const R hB1 = (R(0.5) * ih[d]) * A1, hB2 = (R(0.5) * ihp[d]) * A2;
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
           const R jmp = um[s][c] - up[s][c];
-          const R sbn = sgn * (num * Sm[c] + nup * Sp[c]);
-          const R pv = (FORM == 0 && c == d) ? R(2.0) * jmp : jmp;
-          fv[s][c] = dA * (-sbn + tau * pv);
-          const R Gcd = (FORM == 0 && c == d) ? -num * jmp * sgn : -R(0.5) * num * jmp * sgn;
-          gn[s][c] = dA * Gcd * ih[d];
-        }
-        if constexpr (NT > 0) {
-          gt1[0] = dA * (-R(0.5) * num * (um[s][t1] - up[s][t1]) * sgn) * ih[t1];
-          gt2[0] = dA * (-R(0.5) * num * (um[s][t2] - up[s][t2]) * sgn) * ih[t2];
+          if (FORM == 0 && c == d) {
+            const R B1 = hB1 + hB1, B2 = hB2 + hB2;
+            const R t = fma(B1, dm[s][c], B2 * dp[s][c]);
+            fv[s][c] = fma(dAt + dAt, jmp, -t);
+            gn[s][c] = -B1 * jmp;
+          } else if constexpr (FORM == 0) {
+            const bool c_is_t1 = (c == t1);
+            const R hA1 = (R(0.5) * ih[c]) * A1, hA2 = (R(0.5) * ih[c]) * A2;
+            R t = fma(hB1, dm[s][c], hB2 * dp[s][c]);
+            t = fma(hA1, c_is_t1 ? tm1[0] : tm2[0], t);
+            t = fma(hA2, c_is_t1 ? tp1[0] : tp2[0], t);
+            fv[s][c] = fma(dAt, jmp, -t);
+            gn[s][c] = -hB1 * jmp;
+            if constexpr (NT > 0) {
+              if (c_is_t1) gt1[0] = -hA1 * jmp;
+              else gt2[0] = -hA1 * jmp;
+            }
+          } else {
+            fv[s][c] = fma(dAt, jmp, -fma(hB1, dm[s][c], hB2 * dp[s][c]));
+            gn[s][c] = -hB1 * jmp;
+          }
         }
       } else {
         // ---------------- general geometry: own / neighbour J^-1 at the face point
