@@ -325,7 +325,12 @@ dgvv_status dgvv_embed_continuous(dgvv_ctx* ctx, int32_t op, int32_t transpose, 
  * level's Chebyshev smoothing in every V-cycle that ends on this context by x = A^-1 b (dense
  * matvec).  At most 4096 DoFs (ncomp x level DoFs).  Synchronous.  A later change of the
  * coefficients or mass makes it stale: V-cycles then fail with DGVV_ESTATE until it is set up
- * again.  *n_dofs (may be NULL) = the system size. */
+ * again.  *n_dofs (may be NULL) = the system size (global).  Multi-rank (communicator contexts,
+ * a collective: every rank calls it): each rank assembles its owned rows of every global column
+ * with the distributed apply, the columns are gathered on every rank (zero-padded sum-allreduce:
+ * exact) and every rank inverts the same matrix; a solve gathers b the same way and applies the
+ * rank's owned rows of the inverse.  DGVV_EUNSUPPORTED for external-exchange contexts (ghosts
+ * without a communicator). */
 dgvv_status dgvv_setup_coarse_solver(dgvv_ctx* ctx, int32_t op, int32_t* n_dofs);
 
 /* out_host = sum over all ranks of a.b over `ncomp` * level-dofs entries. Synchronous. */

@@ -362,6 +362,7 @@ DGVV_INTERNAL dgvv_status setup_impl(const dgvv_mesh* m, int32_t degree, const d
     DGVV_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_red, cudaEventDisableTiming));
     DGVV_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_red2, cudaEventDisableTiming));
     TRY(dalloc(c, &c->tg_red, 8));
+    c->tg_red_cap = 8;
     if (cm->kind == COMM_THREADS) {               // handshake: send counts vs listed ghosts
       ThreadGroup* g = cm->tg;
       {

@@ -399,12 +399,20 @@ dgvv_status dgvv_setup_coarse_solver(dgvv_ctx* c, int32_t op, int32_t* n_dofs) {
   TRY(check_ctx(c));
   if (op != DGVV_OP_VISCOUS && op != DGVV_OP_POISSON) return dgvv_fail(DGVV_EINVAL, "unknown op %d", op);
   TRY(op_ready(c, op));
-  if (c->n_ghost || c->comm) return dgvv_fail(DGVV_EUNSUPPORTED, "direct coarse solver: single-GPU contexts only");
+  if (c->n_ghost && !c->comm)
+    return dgvv_fail(DGVV_EUNSUPPORTED, "direct coarse solver: external-exchange contexts (no communicator) are not supported");
   const int oi = op == DGVV_OP_VISCOUS ? 0 : 1;
   const int nc = op == DGVV_OP_VISCOUS ? 3 : 1;
   const int l = (int)c->L.size() - 1;
   if (c->cg.on) return cg_setup_direct(c, op, n_dofs);
-  const long N = (long)nc * level_dofs(c, l);
+  // multi-rank (communicator): every rank assembles its owned rows of every global column with the
+  // distributed apply (ghost exchange included), the columns are gathered (exact zero-padded sum)
+  // and every rank inverts the same matrix; a solve applies this rank's rows to the gathered b
+  const bool mr = c->comm != nullptr;
+  const long Nown = (long)nc * level_dofs(c, l);
+  const long len = c->n_owned ? Nown / c->n_owned : 0;
+  const long N = mr ? (long)nc * (long)c->n_global * ((long)c->L[l].n * c->L[l].n * c->L[l].n) : Nown;
+  const long off = mr ? (long)c->first * (len ? len : (long)nc * c->L[l].n * c->L[l].n * c->L[l].n) : 0;
   if (N > 4096) return dgvv_fail(DGVV_EINVAL, "direct coarse solver: %ld DoFs on the coarsest level (max 4096)", N);
   cudaStream_t s = 0;
   double *cols = nullptr, *W = nullptr, *fac = nullptr, *e = nullptr;
@@ -412,14 +420,16 @@ dgvv_status dgvv_setup_coarse_solver(dgvv_ctx* c, int32_t op, int32_t* n_dofs) {
   DGVV_CUDA_TRY(cudaMalloc(&cols, (size_t)N * N * sizeof(double)));
   DGVV_CUDA_TRY(cudaMalloc(&W, (size_t)2 * N * N * sizeof(double)));
   DGVV_CUDA_TRY(cudaMalloc(&fac, (size_t)N * sizeof(double)));
-  DGVV_CUDA_TRY(cudaMalloc(&e, (size_t)N * sizeof(double)));
+  DGVV_CUDA_TRY(cudaMalloc(&e, (size_t)(Nown > 0 ? Nown : 1) * sizeof(double)));
+  if (mr) DGVV_CUDA_TRY(cudaMemsetAsync(cols, 0, (size_t)N * N * sizeof(double), s));
   for (long j = 0; j < N; ++j) {               // column j = A e_j (the level's matrix-free apply)
-    DGVV_CUDA_TRY(launch_set_unit(e, N, j, s));
+    DGVV_CUDA_TRY(launch_set_unit(e, Nown, j - off, s));
     ApplyArgs a = base_args(c, l, op);
     a.src = e;
-    a.dst = cols + (size_t)j * N;
+    a.dst = cols + (size_t)j * N + off;        // this rank's rows of column j
     TRY(run_apply(c, op, l, a, s));
   }
+  if (mr) TRY(comm_allreduce(c, cols, N * N, s));
   if (!c->Ainv[oi]) TRY(dalloc(c, &c->Ainv[oi], (size_t)N * N));
   DGVV_CUDA_TRY(cudaMemsetAsync(c->d_flag, 0, sizeof(int), s));
   DGVV_CUDA_TRY(launch_gauss_jordan_inverse(cols, W, fac, c->Ainv[oi], (int)N, c->d_flag, s));
@@ -433,6 +443,9 @@ dgvv_status dgvv_setup_coarse_solver(dgvv_ctx* c, int32_t op, int32_t* n_dofs) {
     return dgvv_fail(DGVV_EDOMAIN, "direct coarse solver: %d non-positive pivots (operator not SPD?)", bad);
   }
   c->direct_n[oi] = (int)N;
+  c->direct_off[oi] = off;
+  c->direct_rows[oi] = (int)Nown;
+  if (mr && !c->direct_bf[oi]) TRY(dalloc(c, &c->direct_bf[oi], (size_t)4096));
   c->direct_epoch[oi] = c->coef_epoch;
   if (n_dofs) *n_dofs = (int32_t)N;
   return DGVV_OK;

@@ -264,6 +264,11 @@ struct dgvv_ctx {
   double* Ainv[2] = {nullptr, nullptr};      // dense inverse of the coarsest level per op
   int direct_n[2] = {0, 0};
   int direct_epoch[2] = {-1, -1};            // coef_epoch the inverse was built at
+  // multi-rank direct solve: the inverse is replicated on every rank; this rank's owned DoFs are
+  // rows [direct_off, direct_off + direct_rows) and b is gathered into direct_bf (global length)
+  long direct_off[2] = {0, 0};
+  int direct_rows[2] = {0, 0};
+  double* direct_bf[2] = {nullptr, nullptr};
   float* hbf[2] = {nullptr, nullptr};        // FP32 V-cycle: coarse-level b / x per op
   float* hxf[2] = {nullptr, nullptr};
   std::vector<int> h_parent;                 // host copies of the h-maps (c-level transfers)
@@ -298,7 +303,8 @@ struct dgvv_ctx {
   std::vector<Peer> peers;
   int* d_gslot = nullptr;                    // [n_ghost][6] trace item of ghost g's face f (-1: none)
   int n_recv_f = 0;                          // trace items received in total
-  double* tg_red = nullptr;                  // thread group: allreduce staging (8 doubles)
+  double* tg_red = nullptr;                  // thread group: allreduce staging (tg_red_cap doubles)
+  long tg_red_cap = 0;
   cudaEvent_t ev_red = nullptr, ev_red2 = nullptr;
   double* d_sendbuf = nullptr;
   size_t sendbuf_len = 0;
@@ -460,16 +466,22 @@ dgvv_status comm_sendrecv(dgvv_ctx* c, const void* sendbuf, void* ghost, int len
 }
 
 // sum-allreduce of `count` doubles in place (device pointer, stream-ordered on s)
-dgvv_status comm_allreduce(dgvv_ctx* c, double* ptr, int count, cudaStream_t s) {
+dgvv_status comm_allreduce(dgvv_ctx* c, double* ptr, long count, cudaStream_t s) {
   DgvvComm* cm = (DgvvComm*)c->comm;
   if (!cm) return DGVV_OK;
   if (cm->kind == COMM_NCCL) {
-    NCCL_TRY(g_nccl.allReduce(ptr, ptr, count, ncclDouble, ncclSum, cm->nccl, s));
+    NCCL_TRY(g_nccl.allReduce(ptr, ptr, (size_t)count, ncclDouble, ncclSum, cm->nccl, s));
     return DGVV_OK;
   }
   ThreadGroup* g = cm->tg;
   const int r = cm->rank;
-  if (count > 8) return dgvv_fail(DGVV_EINVAL, "thread group allreduce: count %d > 8", count);
+  if (count > c->tg_red_cap) {                 // staging grows on demand (the coarse-solver gathers)
+    DGVV_CUDA_TRY(cudaStreamSynchronize(s));
+    double* nb = nullptr;
+    TRY(dalloc(c, &nb, (size_t)count));
+    c->tg_red = nb;                            // the old block stays in c->allocs until destroy
+    c->tg_red_cap = count;
+  }
   DGVV_CUDA_TRY(cudaMemcpyAsync(c->tg_red, ptr, count * sizeof(double), cudaMemcpyDeviceToDevice, s));
   DGVV_CUDA_TRY(cudaEventRecord(c->ev_red, s));
   {
@@ -488,6 +500,39 @@ dgvv_status comm_allreduce(dgvv_ctx* c, double* ptr, int count, cudaStream_t s) 
   tg_barrier(g);
   for (int q = 0; q < g->R; ++q) DGVV_CUDA_TRY(cudaStreamWaitEvent(s, g->ev_b[q], 0));   // staging reusable
   tg_barrier(g);
+  return DGVV_OK;
+}
+
+// full[0:N] = every rank's owned segment (this rank's at `off`): a sum-allreduce over zero-padded
+// copies, exact (each entry is one rank's value plus zeros) and identical on every rank
+dgvv_status comm_gather_full(dgvv_ctx* c, const double* own, long n_own, long off, double* full, long N,
+                             cudaStream_t s) {
+  DGVV_CUDA_TRY(cudaMemsetAsync(full, 0, (size_t)N * sizeof(double), s));
+  if (n_own > 0) DGVV_CUDA_TRY(cudaMemcpyAsync(full + off, own, (size_t)n_own * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  return comm_allreduce(c, full, N, s);
+}
+
+// the coarsest level's direct solve x = A^-1 b (single context, or this rank's rows of the
+// replicated inverse applied to the gathered b)
+template <typename R>
+dgvv_status direct_solve(dgvv_ctx* c, int oi, const R* b, R* x, cudaStream_t s) {
+  const int N = c->direct_n[oi];
+  if (!c->comm) {
+    if constexpr (sizeof(R) == 8) DGVV_CUDA_TRY(launch_dense_matvec(c->Ainv[oi], b, x, N, s));
+    else DGVV_CUDA_TRY(launch_dense_matvec_f(c->Ainv[oi], b, x, N, s));
+    return DGVV_OK;
+  }
+  const long off = c->direct_off[oi], rows = c->direct_rows[oi];
+  double* bf = c->direct_bf[oi];
+  if constexpr (sizeof(R) == 8) {
+    TRY(comm_gather_full(c, b, rows, off, bf, N, s));
+    DGVV_CUDA_TRY(launch_dense_matvec(c->Ainv[oi] + (size_t)off * N, bf, x, N, s, (int)rows));
+  } else {
+    DGVV_CUDA_TRY(cudaMemsetAsync(bf, 0, (size_t)N * sizeof(double), s));
+    if (rows) DGVV_CUDA_TRY(launch_f2d(b, bf + off, rows, s));
+    TRY(comm_allreduce(c, bf, N, s));
+    DGVV_CUDA_TRY(launch_dense_matvec_df(c->Ainv[oi] + (size_t)off * N, bf, x, N, s, (int)rows));
+  }
   return DGVV_OK;
 }
 

@@ -114,8 +114,7 @@ DGVV_INTERNAL dgvv_status vcycle_rec(dgvv_ctx* c, int op, int l, const double* b
   if (l == last && !c->coarse && !c->cg.on && c->Ainv[oi]) {   // the c-level, when enabled, comes first
     if (c->direct_epoch[oi] != c->coef_epoch)
       return dgvv_fail(DGVV_ESTATE, "direct coarse solver is stale (coefficients or mass changed): call dgvv_setup_coarse_solver again");
-    DGVV_CUDA_TRY(launch_dense_matvec(c->Ainv[oi], b, x, c->direct_n[oi], s));
-    return DGVV_OK;
+    return direct_solve(c, oi, b, x, s);
   }
   const double hi = his[l], lo = hi / 20.0;
   TRY(cheb_impl(c, op, l, x, b, 5, lo, hi, 1, S[1], s));
@@ -308,8 +307,7 @@ DGVV_INTERNAL dgvv_status vcycle_rec_f(dgvv_ctx* c, int op, int l, const float* 
   if (l == last && !c->coarse && !c->cg.on && c->Ainv[oi]) {   // direct coarse solve, FP64 arithmetic; the c-level, when enabled, comes first
     if (c->direct_epoch[oi] != c->coef_epoch)
       return dgvv_fail(DGVV_ESTATE, "direct coarse solver is stale (coefficients or mass changed): call dgvv_setup_coarse_solver again");
-    DGVV_CUDA_TRY(launch_dense_matvec_f(c->Ainv[oi], b, x, c->direct_n[oi], s));
-    return DGVV_OK;
+    return direct_solve(c, oi, b, x, s);
   }
   const double hi = his[l], lo = hi / 20.0;
   TRY(cheb_impl_f(c, op, l, x, b, 5, lo, hi, 1, S[1], s));

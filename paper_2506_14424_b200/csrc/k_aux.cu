@@ -4,6 +4,8 @@
 #include "aux_kernels.cuh"
 #include "launch.h"
 
+#include <algorithm>
+
 namespace dgvv {
 
 cudaError_t upload_tables_aux(const Tab1D* tabs) { return tu_upload_tables(tabs); }
@@ -179,17 +181,18 @@ cudaError_t launch_range(const double* v, long n, double* bmin, double* bmax, in
 // thread-group allreduce: out[i] = sum over ranks (in rank order) of ranks[r][i] — every rank sums
 // the same operands in the same order, so every rank holds the same bits
 struct RankPtrs { const double* p[64]; };
-__global__ void sum_ranks_kernel(RankPtrs P, int R, int count, double* out) {
-  const int i = threadIdx.x;
-  if (i >= count) return;
-  double s = 0.0;
-  for (int r = 0; r < R; ++r) s += P.p[r][i];
-  out[i] = s;
+__global__ void sum_ranks_kernel(RankPtrs P, int R, long count, double* out) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (long)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int r = 0; r < R; ++r) s += P.p[r][i];     // rank order: the same sum on every rank
+    out[i] = s;
+  }
 }
-cudaError_t launch_sum_ranks(const double* const* ranks, int R, int count, double* out, cudaStream_t s) {
+cudaError_t launch_sum_ranks(const double* const* ranks, int R, long count, double* out, cudaStream_t s) {
   RankPtrs P;
   for (int r = 0; r < R && r < 64; ++r) P.p[r] = ranks[r];
-  sum_ranks_kernel<<<1, 32, 0, s>>>(P, R, count, out);
+  const int blocks = (int)std::min<long>(148L * 8, std::max<long>(1, (count + 255) / 256));
+  sum_ranks_kernel<<<blocks, 256, 0, s>>>(P, R, count, out);
   return cudaGetLastError();
 }
 

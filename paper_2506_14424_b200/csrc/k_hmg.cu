@@ -240,10 +240,11 @@ __global__ void gj_extract_kernel(const double* W, double* Ainv, int N) {
 
 // x = Ainv b, one warp per row (row-major, coalesced); FP64 accumulation for FP32 vectors too
 // (the paper's coarse solver runs in double precision)
-template <typename R>
-__global__ void dense_matvec_kernel(const double* Ainv, const R* b, R* x, int N) {
+// (multi-rank: rows = this rank's owned DoFs of the replicated inverse, b the gathered full vector)
+template <typename RB, typename R>
+__global__ void dense_matvec_kernel(const double* Ainv, const RB* b, R* x, int N, int rows) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (warp >= N) return;
+  if (warp >= rows) return;
   const double* row = Ainv + (size_t)warp * N;
   double acc = 0.0;
   for (int c = lane; c < N; c += 32) acc = fma(row[c], (double)b[c], acc);
@@ -271,12 +272,22 @@ cudaError_t launch_gauss_jordan_inverse(const double* cols, double* W, double* f
   return cudaGetLastError();
 }
 
-cudaError_t launch_dense_matvec(const double* Ainv, const double* b, double* x, int N, cudaStream_t s) {
-  dense_matvec_kernel<double><<<(N * 32 + 255) / 256, 256, 0, s>>>(Ainv, b, x, N);
+cudaError_t launch_dense_matvec(const double* Ainv, const double* b, double* x, int N, cudaStream_t s, int rows) {
+  if (rows < 0) rows = N;
+  if (rows == 0) return cudaSuccess;
+  dense_matvec_kernel<double, double><<<(rows * 32 + 255) / 256, 256, 0, s>>>(Ainv, b, x, N, rows);
   return cudaGetLastError();
 }
-cudaError_t launch_dense_matvec_f(const double* Ainv, const float* b, float* x, int N, cudaStream_t s) {
-  dense_matvec_kernel<float><<<(N * 32 + 255) / 256, 256, 0, s>>>(Ainv, b, x, N);
+cudaError_t launch_dense_matvec_df(const double* Ainv, const double* b, float* x, int N, cudaStream_t s, int rows) {
+  if (rows < 0) rows = N;
+  if (rows == 0) return cudaSuccess;
+  dense_matvec_kernel<double, float><<<(rows * 32 + 255) / 256, 256, 0, s>>>(Ainv, b, x, N, rows);
+  return cudaGetLastError();
+}
+cudaError_t launch_dense_matvec_f(const double* Ainv, const float* b, float* x, int N, cudaStream_t s, int rows) {
+  if (rows < 0) rows = N;
+  if (rows == 0) return cudaSuccess;
+  dense_matvec_kernel<float, float><<<(rows * 32 + 255) / 256, 256, 0, s>>>(Ainv, b, x, N, rows);
   return cudaGetLastError();
 }
 

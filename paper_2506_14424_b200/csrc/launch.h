@@ -38,8 +38,10 @@ cudaError_t launch_hrestrict_f(int n, int nc, const float* fine, float* coarse, 
 cudaError_t launch_set_unit(double* v, long n, long j, cudaStream_t s);
 cudaError_t launch_gauss_jordan_inverse(const double* cols, double* W, double* fac, double* Ainv, int N, int* bad,
                                         cudaStream_t s);
-cudaError_t launch_dense_matvec(const double* Ainv, const double* b, double* x, int N, cudaStream_t s);
-cudaError_t launch_dense_matvec_f(const double* Ainv, const float* b, float* x, int N, cudaStream_t s);
+// x[0:rows] = Ainv[0:rows][0:N] b  (rows < 0: N)
+cudaError_t launch_dense_matvec(const double* Ainv, const double* b, double* x, int N, cudaStream_t s, int rows = -1);
+cudaError_t launch_dense_matvec_f(const double* Ainv, const float* b, float* x, int N, cudaStream_t s, int rows = -1);
+cudaError_t launch_dense_matvec_df(const double* Ainv, const double* b, float* x, int N, cudaStream_t s, int rows = -1);
 // f3 c-level: continuous Q1 level (embedding, transpose, CSR transfers, diagonal probing, Chebyshev)
 cudaError_t launch_cg_embed(const double* cg, double* dg, const int* vid, int n_cells, int nv, int nc, double beta,
                             cudaStream_t s);
@@ -83,7 +85,7 @@ cudaError_t launch_range(const double* v, long n, double* bmin, double* bmax, in
                          cudaStream_t s);
 
 // vector kernels
-cudaError_t launch_sum_ranks(const double* const* ranks, int R, int count, double* out, cudaStream_t s);
+cudaError_t launch_sum_ranks(const double* const* ranks, int R, long count, double* out, cudaStream_t s);
 cudaError_t launch_dot(const double* a, const double* b, long n, double* part, int nblocks, double* out,
                        cudaStream_t s);
 cudaError_t launch_cheb_first(const double* b, const double* dinv, double c_r, double* d, double* x, long n,

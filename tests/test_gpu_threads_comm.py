@@ -284,3 +284,109 @@ def test_thread_group_cph_vcycle_h_levels():
     assert torch.equal(torch.cat([o[0] for o in out]), v1.cpu())
     assert all(abs(o[2] - it1) <= 1 for o in out)
     assert rel(torch.cat([o[1] for o in out]).numpy(), x1.cpu().numpy()) < 1e-6
+
+
+@pytest.mark.parametrize("op,R", [(A.OP_VISCOUS, 2), (A.OP_POISSON, 3)])
+def test_thread_group_direct_coarse_solver(op, R):
+    """The direct coarse solve across ranks (dgvv_setup_coarse_solver on communicator contexts):
+    x = V(b) on a single-level context == numpy's solve of the dense ORACLE matrix (viscous: cube(2)
+    k=1 + mass, 192 DoFs on 2 ranks; Poisson: cube(3) k=1, 216 DoFs on 3 ranks), FP64 and FP32."""
+    from oracle import dense
+    if op == A.OP_VISCOUS:
+        m, k, law, mass, kw = cube(2), 1, laws.C1_LAW, 3.0, {"visc_law": laws.C1_LAW}
+        d = dg.Disc(m, k)
+        Ad = dense.assemble_viscous(d, dg.AnalyticNu(d, law)) + mass * np.diag(dg.mass_apply(d, np.ones(m.n_cells * 3 * d.N)))
+        per = 3 * 8
+    else:
+        m, k, law, mass, kw = cube(3), 1, laws.C4_LAW, 0.0, {"poisson_law": laws.C4_LAW}
+        d = dg.Disc(m, k)
+        Ad = dense.assemble_poisson(d, dg.AnalyticNu(d, law))
+        per = 8
+    b = uniform(0, Ad.shape[0])
+    ref = np.linalg.solve(Ad, b)
+
+    def body(r, ctx, p):
+        ctx.set_mass(op, mass)
+        n = ctx.setup_coarse_solver(op)
+        bb = torch.from_numpy(b[p.first * per:(p.first + p.n_owned) * per].copy()).cuda()
+        x = torch.zeros_like(bb)
+        ctx.vcycle(op, bb, x, [1.0])
+        xf = torch.zeros_like(bb)
+        ctx.vcycle_fp32(op, bb, xf, [1.0])
+        return n, x.cpu(), xf.cpu()
+
+    parts, out = run_ranks(m, R, k, body, **kw)
+    assert all(o[0] == Ad.shape[0] for o in out)
+    x = torch.cat([o[1] for o in out]).numpy()
+    xf = torch.cat([o[2] for o in out]).numpy()
+    cond = np.linalg.cond(Ad)
+    assert rel(x, ref) < 1e-10 * max(1.0, cond / 1e4)
+    assert rel(xf, ref) < 1e-5 * max(1.0, cond / 1e4)      # b and x in FP32, the solve in FP64 (reading F1)
+
+
+def test_thread_group_cph_direct_solve():
+    """cph V-cycle whose coarsest h-level ends in the direct solve, on 2 ranks (nested slabs):
+    equal to the one-context V-cycle to rounding (the gathered solve sums the same terms)."""
+    from inputs import cube_parent_map
+    from paper_2506_14424_b200.dgvv import Context, ThreadGroup
+    R = 2
+    law = laws.C4_LAW
+    meshes = [cube(4), cube(2)]
+    b = uniform(0, meshes[0].n_cells * 27)
+
+    def chain(ctxs, parts):
+        par, octa = cube_parent_map(4)
+        pf, pc = parts[0], parts[1]
+        sl = slice(pf.first, pf.first + pf.n_owned)
+        ctxs[0].set_coarse_context(ctxs[1], par[sl] - pc.first, octa[sl])
+
+    class _P:
+        first, n_owned = 0, None
+    full = []
+    for mm in meshes:
+        p = _P()
+        p.n_owned = mm.n_cells
+        full.append(p)
+    one = [Context(meshes[0], 2, poisson_law=law, degrees=[2, 1]), Context(meshes[1], 1, poisson_law=law)]
+    assert one[1].setup_coarse_solver(A.OP_POISSON) == 64
+    chain(one, full)
+    v0 = [uniform(2, meshes[0].n_cells * 27), uniform(2, meshes[0].n_cells * 8)]
+    lams = [1.2 * one[0].estimate_lambda_max(1, torch.from_numpy(v0[0]).cuda(), level=0, steps=15),
+            1.2 * one[0].estimate_lambda_max(1, torch.from_numpy(v0[1]).cuda(), level=1, steps=15), 1.0]
+    v1 = torch.zeros(len(b), dtype=torch.float64, device="cuda")
+    one[0].vcycle(A.OP_POISSON, torch.from_numpy(b).cuda(), v1, lams)
+
+    g = ThreadGroup(R)
+    parts = [[slab_partition(mm, R, r) for mm in meshes] for r in range(R)]
+    out, err = [None] * R, [None] * R
+
+    def worker(r):
+        try:
+            torch.cuda.set_device(0)
+            with torch.cuda.stream(torch.cuda.Stream()):
+                ps = parts[r]
+                ctxs = [Context(p, k, poisson_law=law, n_owned=p.n_owned, n_ghost=p.n_ghost, ghost_global_id=p.ghost_global_id,
+                                ghost_owner=p.ghost_owner, first_global_cell=p.first, nccl_comm=g.comm(r), **kw)
+                        for p, k, kw in zip(ps, [2, 1], [dict(degrees=[2, 1]), {}])]
+                ctxs[1].setup_coarse_solver(A.OP_POISSON)
+                chain(ctxs, ps)
+                bb = torch.from_numpy(b[ps[0].first * 27:(ps[0].first + ps[0].n_owned) * 27].copy()).cuda()
+                v = torch.zeros_like(bb)
+                ctxs[0].vcycle(A.OP_POISSON, bb, v, lams)
+                torch.cuda.current_stream().synchronize()
+                out[r] = v.cpu()
+                for c in ctxs:
+                    c.close()
+        except BaseException as e:          # noqa: BLE001
+            err[r] = e
+
+    ts = [threading.Thread(target=worker, args=(r,)) for r in range(R)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=600)
+    g.close()
+    for e in err:
+        if e is not None:
+            raise e
+    assert rel(torch.cat(out).numpy(), v1.cpu().numpy()) < 1e-12
