@@ -305,6 +305,8 @@ struct dgvv_ctx {
   int n_recv_f = 0;                          // trace items received in total
   double* tg_red = nullptr;                  // thread group: allreduce staging (tg_red_cap doubles)
   long tg_red_cap = 0;
+  double* align_buf = nullptr;               // aligned copy of a misaligned apply source
+  long align_cap = 0;
   cudaEvent_t ev_red = nullptr, ev_red2 = nullptr;
   double* d_sendbuf = nullptr;
   size_t sendbuf_len = 0;
@@ -643,6 +645,20 @@ dgvv_status op_ready(dgvv_ctx* c, int op) {
 // kind: 0 plain operator, 1 Newton-linearised (K2), 2 viscous + fused convective term (f4)
 dgvv_status run_apply(dgvv_ctx* c, int op, int l, ApplyArgs a, cudaStream_t s, int kind = 0) {
   const int nc = op == DGVV_OP_VISCOUS ? 3 : 1;
+  if (reinterpret_cast<uintptr_t>(a.src) & 31) {
+    // the kernels read neighbour rows with 256-bit loads: a source vector that is not 32-byte
+    // aligned (a slice of a larger tensor) is staged through an aligned copy (16 B/DoF extra)
+    const size_t N = (size_t)(kind == 1 ? 3 : nc) * level_dofs(c, l);
+    if ((long)N > c->align_cap) {
+      DGVV_CUDA_TRY(cudaStreamSynchronize(s));
+      double* nb = nullptr;
+      TRY(dalloc(c, &nb, N));
+      c->align_buf = nb;
+      c->align_cap = (long)N;
+    }
+    DGVV_CUDA_TRY(cudaMemcpyAsync(c->align_buf, a.src, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    a.src = c->align_buf;
+  }
   const int form = op == DGVV_OP_VISCOUS ? c->form : DGVV_FORM_LAPLACE;
   auto launch = [&](const ApplyArgs& x) -> dgvv_status {
     cudaError_t e = kind == 1 ? launch_newton(c->L[l].n, c->geo, x, s)

@@ -220,6 +220,8 @@ DGVV_INTERNAL ApplyArgsT<float> base_args_f(dgvv_ctx* c, int l, int op) {
 // FP32 levels across ranks: the ghost face traces travel in single precision, packed by the trace
 // kernel and moved by the same collective as the FP64 exchange; interior cells run while they move
 DGVV_INTERNAL dgvv_status run_apply_f(dgvv_ctx* c, int op, int l, const ApplyArgsT<float>& a, cudaStream_t s) {
+  if (reinterpret_cast<uintptr_t>(a.src) & 15)    // float4 neighbour rows (internal FP32 buffers are aligned)
+    return dgvv_fail(DGVV_EINVAL, "FP32 source vector %p is not 16-byte aligned", (const void*)a.src);
   const int nc = op == DGVV_OP_VISCOUS ? 3 : 1;
   const int form = op == DGVV_OP_VISCOUS ? c->form : DGVV_FORM_LAPLACE;
   auto launch = [&](const ApplyArgsT<float>& x) -> dgvv_status {

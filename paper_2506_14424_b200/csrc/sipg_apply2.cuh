@@ -126,6 +126,23 @@ __device__ __forceinline__ void ld_row(const R* __restrict__ r, R (&x)[n]) {
 }
 template <int n, typename R>
 __device__ __forceinline__ void ldg_row(const R* __restrict__ r, R (&x)[n]) {
+  if constexpr (sizeof(R) == 8 && n % 4 == 0) {
+    // 256-bit loads (sm_100: LDG.E.ENL2.256): one instruction and one pass over each 32-byte
+    // sector per 4 doubles (two 128-bit loads touched every sector twice); rows are 32-B aligned
+    // (vectors 32-B aligned, checked by the ABI)
+#pragma unroll
+    for (int k = 0; k < n; k += 4)
+      asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+          : "=d"(x[k]), "=d"(x[k + 1]), "=d"(x[k + 2]), "=d"(x[k + 3]) : "l"(r + k));
+    return;
+  } else if constexpr (sizeof(R) == 4 && n % 4 == 0) {
+#pragma unroll
+    for (int k = 0; k < n; k += 4) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(r + k));
+      x[k] = v.x; x[k + 1] = v.y; x[k + 2] = v.z; x[k + 3] = v.w;
+    }
+    return;
+  }
 #pragma unroll
   for (int k = 0; k + 1 < n; k += 2) {
     const typename V2<R>::t v = __ldg(reinterpret_cast<const typename V2<R>::t*>(r + k));
