@@ -93,6 +93,16 @@ def run_c2(reps):
     it = iter(range(10 ** 9))
     ms = timeit(lambda: ctx.apply_viscous(src[next(it) % 4], dst[0]), 100, reps)
     report("C2", "apply_viscous", ms, N, visc_bytes(m.n_cells, 4, True), visc_flops(N, 4, True))
+    # the C2 (deformed, iso-parametric) geometry with C3's Carreau law: Picard and Newton applies
+    # of the general-geometry kernels (VERDICT r1 "Hygiene": the general-geometry Newton is the
+    # v1 kernel that recomputes nu'(gamma) per point; Cartesian meshes use v3 with stored point data)
+    cc = Context(m, 3, visc_law=C3_LAW)
+    cc.update_viscosity(dev(c3_linearization(cube(32), 3)))   # the field at the undeformed positions
+    ms = timeit(lambda: cc.apply_viscous(src[0], dst[0]), 50, reps)
+    report("C2-Carreau", "apply_viscous", ms, N, visc_bytes(m.n_cells, 4, True), visc_flops(N, 4, True))
+    ms = timeit(lambda: cc.apply_linearized_viscous(src[0], dst[0]), 50, reps)
+    report("C2-Carreau", "apply_linearized_viscous", ms, N, None, None,
+           "general-geometry Newton (v1: recomputes the Carreau derivative at every point)")
 
 
 def run_c3(reps):
