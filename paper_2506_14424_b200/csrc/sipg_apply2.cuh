@@ -793,24 +793,36 @@ sipg_apply2_kernel(const ApplyArgsT<R> A) {
     }
   }
   if (active) {
-    const size_t off = (size_t)cell * NC * n3;
+    // the epilogue mode is uniform: branch once, not per element (per-element tests compiled to a
+    // jump table per store, ncu: 12 indirect branches per thread)
+    const size_t off = (size_t)cell * NC * n3 + p;
+    if (A.mode == MODE_APPLY) {
 #pragma unroll
-    for (int c = 0; c < NC; ++c)
+      for (int c = 0; c < NC; ++c)
 #pragma unroll
-      for (int z = 0; z < n; ++z) {
-        const size_t i = off + c * n3 + z * n2 + p;
-        if (A.mode == MODE_APPLY) {
-          A.dst[i] = y[c][z];
-        } else if (A.mode == MODE_RESID) {
+        for (int z = 0; z < n; ++z) A.dst[off + c * n3 + z * n2] = y[c][z];
+    } else if (A.mode == MODE_RESID) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+#pragma unroll
+        for (int z = 0; z < n; ++z) {
+          const size_t i = off + c * n3 + z * n2;
           A.dst[i] = __ldg(A.b + i) - y[c][z];
-        } else {
+        }
+    } else {
+      const R cr = R(A.c_r), crho = R(A.c_rho);
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+#pragma unroll
+        for (int z = 0; z < n; ++z) {
+          const size_t i = off + c * n3 + z * n2;
           const R r = __ldg(A.b + i) - y[c][z];
-          R dn = R(A.c_r) * __ldg(A.dinv + i) * r;
-          if (R(A.c_rho) != R(0.0)) dn += R(A.c_rho) * A.dvec[i];
+          R dn = cr * __ldg(A.dinv + i) * r;
+          if (crho != R(0.0)) dn += crho * A.dvec[i];
           A.dvec[i] = dn;
           A.xout[i] = su[c * CST + z * PS + b * RS + a] + dn;
         }
-      }
+    }
   }
 }
 
