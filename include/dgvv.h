@@ -26,7 +26,7 @@
  * library never frees or retains (except u_lin, see dgvv_update_viscosity).  The operator
  * kernels read source vectors with 256-bit loads: a source that is not 32-byte aligned (a slice
  * of a larger allocation) is first copied into an aligned library buffer (correct, 16 B/DoF of
- * extra traffic; cudaMalloc and torch allocations are aligned).  All compute
+ * extra traffic; cudaMalloc and PyTorch caching-allocator blocks are aligned).  All compute
  * calls are asynchronous on the caller's stream unless stated otherwise.  Status codes are
  * returned, never thrown; dgvv_last_error gives a message for the last failure.
  * One context is used by one host thread at a time; distinct contexts are independent.
