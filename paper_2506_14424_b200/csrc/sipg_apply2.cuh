@@ -46,6 +46,9 @@
 #ifndef DGVV_NUF_EARLY
 #define DGVV_NUF_EARLY 1      // Cartesian without the TMA stage: a direction's face coefficients loaded at its start
 #endif
+#ifndef DGVV_ZTR
+#define DGVV_ZTR 1            // Cartesian divergence form: z-face own tangential derivatives from the volume term
+#endif
 #ifndef DGVV_QUAD_SWIZZLE
 #define DGVV_QUAD_SWIZZLE 1   // n = 4: lane quads cover 2 x 2 blocks of columns (see the kernel)
 #endif
@@ -306,6 +309,13 @@ sipg_apply2_kernel(const ApplyArgsT<R> A) {
   }
   __syncthreads();
 
+  // Cartesian divergence form: the tangential derivatives of the own trace of u_z on the two
+  // z faces are the z-traces of the reference x- and y-derivatives of u_z the volume term computes
+  // along this thread's own column (linearity of the trace): accumulated there, they replace the
+  // z-faces' own trace round trip through shared memory (store + row and column contractions).
+  // Measured C5 2605 -> 2589 us
+  constexpr bool ZTR = (GEO == 0) && (FORM == 0) && (n % 2 == 0) && (DGVV_ZTR != 0);   // n = 5: +0.5 % (C3), not built
+  R ztr[2][2] = {{R(0.0), R(0.0)}, {R(0.0), R(0.0)}};   // [face s][x / y derivative]
   // =============================================================== volume term
   {
     R Da[n], Db[n];
@@ -331,6 +341,13 @@ sipg_apply2_kernel(const ApplyArgsT<R> A) {
 #pragma unroll
         for (int k = 0; k < n; ++k) sz = fma(R(T.D[z * DGVV_NMAX + k]), ucol[c][k], sz);
         gxi[c][2] = sz;
+      }
+      if constexpr (ZTR) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          ztr[0][j] = fma(R(T.l0[z]), gxi[2][j], ztr[0][j]);
+          ztr[1][j] = fma(R(T.l1[z]), gxi[2][j], ztr[1][j]);
+        }
       }
       R Ji[9], w;
       if constexpr (GEO == 0) {
@@ -514,7 +531,7 @@ sipg_apply2_kernel(const ApplyArgsT<R> A) {
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
           const int c = (GEO == 1) ? t : d;
-          WK[VOL + ((s * 4 + 0) * NT + t) * FA + b * RS + a] = um[s][c];
+          if (!(ZTR && d == 2)) WK[VOL + ((s * 4 + 0) * NT + t) * FA + b * RS + a] = um[s][c];
           WK[VOL + ((s * 4 + 1) * NT + t) * FA + b * RS + a] = up[s][c];
         }
       __syncthreads();
@@ -565,10 +582,15 @@ sipg_apply2_kernel(const ApplyArgsT<R> A) {
         ld_row<n>(sD + b * RS, Db);
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
-          tm1[t] = rowdot<n>(Tm + t * FA + b * RS, Da);
           R m2 = R(0.0), p2 = R(0.0);
+          if (ZTR && d == 2) {
+            tm1[t] = ztr[s][0];
+            m2 = ztr[s][1];
+          } else {
+            tm1[t] = rowdot<n>(Tm + t * FA + b * RS, Da);
 #pragma unroll
-          for (int k = 0; k < n; ++k) m2 = fma(Db[k], Tm[t * FA + k * RS + a], m2);
+            for (int k = 0; k < n; ++k) m2 = fma(Db[k], Tm[t * FA + k * RS + a], m2);
+          }
           tm2[t] = m2;
           if (inter) {
             tp1[t] = rowdot<n>(Tp + t * FA + b * RS, Da);
