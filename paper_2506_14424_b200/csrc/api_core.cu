@@ -8,6 +8,7 @@ const char* dgvv_last_error(void) { return g_err.c_str(); }
 const char* dgvv_version(void) { return "dgvv 0.1 (sm_100a, fp64)"; }
 
 dgvv_status dgvv_nccl_get_unique_id(char out_id[128]) {
+  DGVV_RANGE();
   TRY(nccl_load());
   ncclUniqueId id;
   NCCL_TRY(g_nccl.getUniqueId(&id));
@@ -16,6 +17,7 @@ dgvv_status dgvv_nccl_get_unique_id(char out_id[128]) {
 }
 
 dgvv_status dgvv_nccl_comm_init(const char id_bytes[128], int32_t nranks, int32_t rank, void** comm) {
+  DGVV_RANGE();
   TRY(nccl_load());
   ncclUniqueId id;
   std::memcpy(id.internal, id_bytes, 128);
@@ -30,6 +32,7 @@ dgvv_status dgvv_nccl_comm_init(const char id_bytes[128], int32_t nranks, int32_
 }
 
 dgvv_status dgvv_nccl_comm_destroy(void* comm) {
+  DGVV_RANGE();
   if (!comm) return DGVV_OK;
   DgvvComm* cm = (DgvvComm*)comm;
   if (cm->kind != COMM_NCCL) return dgvv_fail(DGVV_EINVAL, "not an NCCL communicator");
@@ -40,6 +43,7 @@ dgvv_status dgvv_nccl_comm_destroy(void* comm) {
 }
 
 dgvv_status dgvv_thread_group_create(int32_t nranks, void** group) {
+  DGVV_RANGE();
   if (nranks < 1 || nranks > 64 || !group) return dgvv_fail(DGVV_EINVAL, "thread group: 1 <= nranks <= 64");
   ThreadGroup* g = new ThreadGroup;
   g->R = nranks;
@@ -60,6 +64,7 @@ dgvv_status dgvv_thread_group_create(int32_t nranks, void** group) {
 }
 
 dgvv_status dgvv_thread_group_comm(void* group, int32_t rank, void** comm) {
+  DGVV_RANGE();
   ThreadGroup* g = (ThreadGroup*)group;
   if (!g || !comm || rank < 0 || rank >= g->R) return dgvv_fail(DGVV_EINVAL, "thread group: bad rank %d", rank);
   *comm = (void*)&g->comms[rank];
@@ -67,6 +72,7 @@ dgvv_status dgvv_thread_group_comm(void* group, int32_t rank, void** comm) {
 }
 
 dgvv_status dgvv_thread_group_destroy(void* group) {
+  DGVV_RANGE();
   delete (ThreadGroup*)group;
   return DGVV_OK;
 }
@@ -412,6 +418,7 @@ DGVV_INTERNAL dgvv_status setup_impl(const dgvv_mesh* m, int32_t degree, const d
 
 dgvv_status dgvv_setup(const dgvv_mesh* m, int32_t degree, const dgvv_law* vl, const dgvv_law* pl,
                        const dgvv_options* opt, dgvv_stream stream, dgvv_ctx** out) {
+  DGVV_RANGE();
   if (!out) return dgvv_fail(DGVV_EINVAL, "out is null");
   *out = nullptr;
   int ndev = 0;
@@ -429,6 +436,7 @@ dgvv_status dgvv_setup(const dgvv_mesh* m, int32_t degree, const dgvv_law* vl, c
 }
 
 dgvv_status dgvv_update_viscosity(dgvv_ctx* c, const double* u_lin, dgvv_stream stream) {
+  DGVV_RANGE();
   TRY(check_ctx(c));
   if (!c->carreau) return dgvv_fail(DGVV_EUNSUPPORTED, "update_viscosity needs the Carreau law");
   if (!u_lin) return dgvv_fail(DGVV_EINVAL, "u_lin is null");
@@ -489,6 +497,7 @@ dgvv_status dgvv_update_viscosity(dgvv_ctx* c, const double* u_lin, dgvv_stream 
 }
 
 dgvv_status dgvv_apply_viscous(dgvv_ctx* c, int32_t level, const double* src, double* dst, dgvv_stream stream) {
+  DGVV_RANGE();
   TRY(check_level(c, level));
   TRY(op_ready(c, DGVV_OP_VISCOUS));
   if (!src || !dst) return dgvv_fail(DGVV_EINVAL, "null vector");
@@ -551,6 +560,7 @@ DGVV_INTERNAL dgvv_status host_pipe_setup(dgvv_ctx* c, int level) {
 
 dgvv_status dgvv_apply_viscous_host(dgvv_ctx* c, int32_t level, const double* src_host, double* dst_host,
                                     dgvv_stream stream) {
+  DGVV_RANGE();
   TRY(check_level(c, level));
   TRY(op_ready(c, DGVV_OP_VISCOUS));
   if (!src_host || !dst_host) return dgvv_fail(DGVV_EINVAL, "null vector");
@@ -598,6 +608,7 @@ dgvv_status dgvv_apply_viscous_host(dgvv_ctx* c, int32_t level, const double* sr
 }
 
 dgvv_status dgvv_apply_poisson(dgvv_ctx* c, int32_t level, const double* src, double* dst, dgvv_stream stream) {
+  DGVV_RANGE();
   TRY(check_level(c, level));
   TRY(op_ready(c, DGVV_OP_POISSON));
   if (!src || !dst) return dgvv_fail(DGVV_EINVAL, "null vector");
@@ -609,6 +620,7 @@ dgvv_status dgvv_apply_poisson(dgvv_ctx* c, int32_t level, const double* src, do
 }
 
 dgvv_status dgvv_apply_linearized_viscous(dgvv_ctx* c, const double* src, double* dst, dgvv_stream stream) {
+  DGVV_RANGE();
   TRY(check_ctx(c));
   if (!c->has_visc || !c->carreau) return dgvv_fail(DGVV_EUNSUPPORTED, "linearised apply needs the Carreau law");
   if (!c->nu_ready || !c->ulin) return dgvv_fail(DGVV_ESTATE, "call dgvv_update_viscosity first");
@@ -638,6 +650,7 @@ dgvv_status dgvv_apply_linearized_viscous(dgvv_ctx* c, const double* src, double
 
 
 dgvv_status dgvv_set_mass(dgvv_ctx* c, int32_t op, double mass) {
+  DGVV_RANGE();
   TRY(check_ctx(c));
   if (op != DGVV_OP_VISCOUS && op != DGVV_OP_POISSON) return dgvv_fail(DGVV_EINVAL, "unknown op %d", op);
   if (!std::isfinite(mass) || mass < 0.0) return dgvv_fail(DGVV_EDOMAIN, "mass coefficient %g must be finite and >= 0", mass);
@@ -650,6 +663,7 @@ dgvv_status dgvv_set_mass(dgvv_ctx* c, int32_t op, double mass) {
 
 dgvv_status dgvv_dot(dgvv_ctx* c, int32_t level, int32_t ncomp, const double* a, const double* b, double* out,
                      dgvv_stream stream) {
+  DGVV_RANGE();
   TRY(check_level(c, level));
   if (!a || !b || !out || ncomp < 1) return dgvv_fail(DGVV_EINVAL, "bad argument");
   cudaStream_t s = (cudaStream_t)stream;
@@ -660,6 +674,7 @@ dgvv_status dgvv_dot(dgvv_ctx* c, int32_t level, int32_t ncomp, const double* a,
 }
 
 dgvv_status dgvv_sizes(const dgvv_ctx* c, int32_t level, int64_t* nl, int64_t* ng) {
+  DGVV_RANGE();
   TRY(check_level(c, level));
   const long long n3 = (long long)c->L[level].n * c->L[level].n * c->L[level].n;
   if (nl) *nl = (int64_t)c->n_owned * n3;
@@ -670,6 +685,7 @@ dgvv_status dgvv_sizes(const dgvv_ctx* c, int32_t level, int64_t* nl, int64_t* n
 }
 
 dgvv_status dgvv_coefficient_range(dgvv_ctx* c, int32_t op, int32_t level, double* lo, double* hi) {
+  DGVV_RANGE();
   TRY(check_level(c, level));
   TRY(op_ready(c, op));
   Level& L = c->L[level];
@@ -687,6 +703,7 @@ dgvv_status dgvv_coefficient_range(dgvv_ctx* c, int32_t op, int32_t level, doubl
 }
 
 dgvv_status dgvv_exchange_bytes(const dgvv_ctx* c, int32_t level, int32_t op, int64_t* sent, int64_t* received) {
+  DGVV_RANGE();
   TRY(check_level(c, level));
   if (!sent || !received) return dgvv_fail(DGVV_EINVAL, "null output");
   const int nc = op == DGVV_OP_POISSON ? 1 : 3;
@@ -700,6 +717,7 @@ dgvv_status dgvv_exchange_bytes(const dgvv_ctx* c, int32_t level, int32_t op, in
 
 dgvv_status dgvv_ghost_layout(const dgvv_ctx* c, int32_t* n_peers, int32_t* peer_ranks, int32_t* send_counts,
                               int32_t* recv_counts) {
+  DGVV_RANGE();
   if (!c || !n_peers) return dgvv_fail(DGVV_EINVAL, "null argument");
   *n_peers = (int32_t)c->peers.size();
   for (size_t i = 0; i < c->peers.size(); ++i) {
@@ -712,6 +730,7 @@ dgvv_status dgvv_ghost_layout(const dgvv_ctx* c, int32_t* n_peers, int32_t* peer
 
 dgvv_status dgvv_pack_ghosts(dgvv_ctx* c, int32_t level, int32_t kind, const double* src, double* sendbuf,
                              dgvv_stream stream) {
+  DGVV_RANGE();
   TRY(check_level(c, level));
   if (!src || !sendbuf) return dgvv_fail(DGVV_EINVAL, "null vector");
   const int nc = kind == DGVV_GHOST_POISSON ? 1 : 3;
@@ -719,6 +738,7 @@ dgvv_status dgvv_pack_ghosts(dgvv_ctx* c, int32_t level, int32_t kind, const dou
 }
 
 dgvv_status dgvv_ghost_buffer(dgvv_ctx* c, int32_t level, int32_t kind, double** out) {
+  DGVV_RANGE();
   TRY(check_level(c, level));
   if (!out) return dgvv_fail(DGVV_EINVAL, "null out");
   Level& L = c->L[level];

@@ -209,6 +209,7 @@ DGVV_INTERNAL dgvv_status cg_setup_direct(dgvv_ctx* c, int op, int32_t* n_dofs) 
 }
 
 dgvv_status dgvv_set_continuous_level(dgvv_ctx* c, int32_t enable) {
+  DGVV_RANGE();
   TRY(check_ctx(c));
   if (!enable) { c->cg.on = false; return DGVV_OK; }
   if (c->L.back().k != 1) return dgvv_fail(DGVV_EINVAL, "continuous level: the coarsest degree must be 1 (is %d)", c->L.back().k);
@@ -276,6 +277,7 @@ dgvv_status dgvv_set_continuous_level(dgvv_ctx* c, int32_t enable) {
 }
 
 dgvv_status dgvv_continuous_level_info(const dgvv_ctx* c, int32_t* n_vertices, int32_t* n_colors) {
+  DGVV_RANGE();
   TRY(check_ctx(c));
   if (!c->cg.on) return dgvv_fail(DGVV_ESTATE, "continuous level not enabled");
   if (n_vertices) *n_vertices = c->cg.nv;
@@ -284,6 +286,7 @@ dgvv_status dgvv_continuous_level_info(const dgvv_ctx* c, int32_t* n_vertices, i
 }
 
 dgvv_status dgvv_apply_continuous(dgvv_ctx* c, int32_t op, const double* src, double* dst, dgvv_stream stream) {
+  DGVV_RANGE();
   if (!c || !src || !dst) return dgvv_fail(DGVV_EINVAL, "null argument");
   if (!c->cg.on) return dgvv_fail(DGVV_ESTATE, "continuous level not enabled");
   if (op != DGVV_OP_VISCOUS && op != DGVV_OP_POISSON) return dgvv_fail(DGVV_EINVAL, "unknown op %d", op);
@@ -294,6 +297,7 @@ dgvv_status dgvv_apply_continuous(dgvv_ctx* c, int32_t op, const double* src, do
 
 dgvv_status dgvv_embed_continuous(dgvv_ctx* c, int32_t op, int32_t transpose, const double* src, double* dst,
                                   double beta, dgvv_stream stream) {
+  DGVV_RANGE();
   if (!c || !src || !dst) return dgvv_fail(DGVV_EINVAL, "null argument");
   if (!c->cg.on) return dgvv_fail(DGVV_ESTATE, "continuous level not enabled");
   if (op != DGVV_OP_VISCOUS && op != DGVV_OP_POISSON) return dgvv_fail(DGVV_EINVAL, "unknown op %d", op);
@@ -324,6 +328,7 @@ DGVV_INTERNAL dgvv_status hrestrict_impl(dgvv_ctx* c, int op, const double* fine
 }
 
 dgvv_status dgvv_set_coarse_context(dgvv_ctx* c, dgvv_ctx* cc, const int32_t* parent, const int8_t* octant) {
+  DGVV_RANGE();
   if (!c || !cc || !parent || !octant) return dgvv_fail(DGVV_EINVAL, "null argument");
   if (c == cc) return dgvv_fail(DGVV_EINVAL, "a context cannot be its own coarse level");
   for (dgvv_ctx* q = cc; q; q = q->coarse)
@@ -383,6 +388,7 @@ DGVV_INTERNAL dgvv_status h_ready(dgvv_ctx* c, int op) {
 
 dgvv_status dgvv_prolongate_h(dgvv_ctx* c, int32_t op, const double* coarse, double* fine, double beta,
                               dgvv_stream stream) {
+  DGVV_RANGE();
   TRY(h_ready(c, op));
   if (!coarse || !fine) return dgvv_fail(DGVV_EINVAL, "null vector");
   return hprolong_impl(c, op, coarse, fine, beta, (cudaStream_t)stream);
@@ -390,12 +396,14 @@ dgvv_status dgvv_prolongate_h(dgvv_ctx* c, int32_t op, const double* coarse, dou
 
 dgvv_status dgvv_restrict_h(dgvv_ctx* c, int32_t op, const double* fine, double* coarse, double beta,
                             dgvv_stream stream) {
+  DGVV_RANGE();
   TRY(h_ready(c, op));
   if (!coarse || !fine) return dgvv_fail(DGVV_EINVAL, "null vector");
   return hrestrict_impl(c, op, fine, coarse, beta, (cudaStream_t)stream);
 }
 
 dgvv_status dgvv_setup_coarse_solver(dgvv_ctx* c, int32_t op, int32_t* n_dofs) {
+  DGVV_RANGE();
   TRY(check_ctx(c));
   if (op != DGVV_OP_VISCOUS && op != DGVV_OP_POISSON) return dgvv_fail(DGVV_EINVAL, "unknown op %d", op);
   TRY(op_ready(c, op));

@@ -23,10 +23,24 @@
 #include <unordered_map>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/dgvv.h"
 #include "launch.h"
 
 using namespace dgvv;
+
+// ------------------------------------------------------------------ NVTX ranges
+// Every C-ABI entry point opens a range named after itself, so a timeline tool (nsys, ncu
+// --nvtx) shows which call launched which kernels.  NVTX v3 is header-only: without a tool
+// attached a push/pop is a null function-pointer test.
+struct DgvvNvtxRange {
+  explicit DgvvNvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~DgvvNvtxRange() { nvtxRangePop(); }
+  DgvvNvtxRange(const DgvvNvtxRange&) = delete;
+  DgvvNvtxRange& operator=(const DgvvNvtxRange&) = delete;
+};
+#define DGVV_RANGE() DgvvNvtxRange dgvv_nvtx_range_(__func__)
 
 // ------------------------------------------------------------------ errors
 inline thread_local std::string g_err;

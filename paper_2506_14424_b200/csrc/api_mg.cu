@@ -5,6 +5,7 @@
 extern "C" {
 
 dgvv_status dgvv_inverse_diagonal(dgvv_ctx* c, int32_t op, int32_t level, double* dst, dgvv_stream stream) {
+  DGVV_RANGE();
   TRY(check_level(c, level));
   TRY(op_ready(c, op));
   if (!dst) return dgvv_fail(DGVV_EINVAL, "null dst");
@@ -61,6 +62,7 @@ DGVV_INTERNAL dgvv_status cheb_impl(dgvv_ctx* c, int op, int l, double* x, const
 dgvv_status dgvv_chebyshev_smooth(dgvv_ctx* c, int32_t op, int32_t level, double* x, const double* b,
                                   int32_t degree, double lambda_lo, double lambda_hi, int32_t x_is_zero,
                                   double* work, dgvv_stream stream) {
+  DGVV_RANGE();
   TRY(check_level(c, level));
   TRY(op_ready(c, op));
   if (!x || !b || !work) return dgvv_fail(DGVV_EINVAL, "null vector");
@@ -92,12 +94,14 @@ DGVV_INTERNAL dgvv_status transfer(dgvv_ctx* c, int op, int fl, const double* in
 
 dgvv_status dgvv_prolongate(dgvv_ctx* c, int32_t op, int32_t fine_level, const double* coarse, double* fine,
                             double beta, dgvv_stream stream) {
+  DGVV_RANGE();
   if (!c || !coarse || !fine) return dgvv_fail(DGVV_EINVAL, "null argument");
   return transfer(c, op, fine_level, coarse, fine, beta, true, (cudaStream_t)stream);
 }
 
 dgvv_status dgvv_restrict(dgvv_ctx* c, int32_t op, int32_t fine_level, const double* fine, double* coarse,
                           double beta, dgvv_stream stream) {
+  DGVV_RANGE();
   if (!c || !coarse || !fine) return dgvv_fail(DGVV_EINVAL, "null argument");
   return transfer(c, op, fine_level, fine, coarse, beta, false, (cudaStream_t)stream);
 }
@@ -350,6 +354,7 @@ DGVV_INTERNAL dgvv_status vcycle_fp32_d(dgvv_ctx* c, int op, const double* r, do
 
 dgvv_status dgvv_vcycle_fp32(dgvv_ctx* c, int32_t op, const double* b, double* x, const double* his,
                              dgvv_stream stream) {
+  DGVV_RANGE();
   if (!c || !b || !x || !his) return dgvv_fail(DGVV_EINVAL, "null argument");
   TRY(op_ready(c, op));
   return vcycle_fp32_d(c, op, b, x, his, (cudaStream_t)stream);
@@ -358,6 +363,7 @@ dgvv_status dgvv_vcycle_fp32(dgvv_ctx* c, int32_t op, const double* b, double* x
 
 dgvv_status dgvv_vcycle(dgvv_ctx* c, int32_t op, const double* b, double* x, const double* his,
                         dgvv_stream stream) {
+  DGVV_RANGE();
   if (!c || !b || !x || !his) return dgvv_fail(DGVV_EINVAL, "null argument");
   TRY(op_ready(c, op));
   if (op == DGVV_OP_PENALTY) {                 // f2: p-levels of this context
@@ -421,6 +427,7 @@ DGVV_INTERNAL dgvv_status dot_host(dgvv_ctx* c, const double* a, const double* b
 dgvv_status dgvv_cg_solve(dgvv_ctx* c, int32_t op, const double* b, double* x, double rtol, int32_t maxit,
                           int32_t precond, const double* lambda_hi_per_level, int32_t* iters, double* relres,
                           dgvv_stream stream) {
+  DGVV_RANGE();
   if (!c || !b || !x) return dgvv_fail(DGVV_EINVAL, "null argument");
   TRY(op_ready(c, op));
   if (b == x) return dgvv_fail(DGVV_EINVAL, "b and x alias");
@@ -498,6 +505,7 @@ dgvv_status dgvv_cg_solve(dgvv_ctx* c, int32_t op, const double* b, double* x, d
 
 dgvv_status dgvv_estimate_lambda_max(dgvv_ctx* c, int32_t op, int32_t level, int32_t steps, const double* v0,
                                      double* out, dgvv_stream stream) {
+  DGVV_RANGE();
   TRY(check_ctx(c));
   const bool cgl = c->cg.on && level == (int)c->L.size();      // the continuous (c-) level
   if (!cgl) TRY(check_level(c, level));

@@ -51,6 +51,7 @@ DGVV_INTERNAL dgvv_status launch_conv(dgvv_ctx* c, const double* src, double* ds
 }
 
 dgvv_status dgvv_set_transport(dgvv_ctx* c, const double* w, dgvv_stream stream) {
+  DGVV_RANGE();
   if (!c || !w) return dgvv_fail(DGVV_EINVAL, "null argument");
   cudaStream_t s = (cudaStream_t)stream;
   const size_t N = (size_t)3 * level_dofs(c, 0);
@@ -71,6 +72,7 @@ dgvv_status dgvv_set_transport(dgvv_ctx* c, const double* w, dgvv_stream stream)
 }
 
 dgvv_status dgvv_apply_convective(dgvv_ctx* c, const double* src, double* dst, dgvv_stream stream) {
+  DGVV_RANGE();
   if (!c || !src || !dst) return dgvv_fail(DGVV_EINVAL, "null argument");
   if (src == dst) return dgvv_fail(DGVV_EINVAL, "src and dst alias");
   if (!c->has_wtr) return dgvv_fail(DGVV_ESTATE, "convective term: call dgvv_set_transport first");
@@ -99,6 +101,7 @@ DGVV_INTERNAL dgvv_status apply_oseen(dgvv_ctx* c, double alpha_c, const double*
 }
 
 dgvv_status dgvv_apply_oseen(dgvv_ctx* c, double alpha_c, const double* src, double* dst, dgvv_stream stream) {
+  DGVV_RANGE();
   if (!c || !src || !dst) return dgvv_fail(DGVV_EINVAL, "null argument");
   if (src == dst) return dgvv_fail(DGVV_EINVAL, "src and dst alias");
   if (!std::isfinite(alpha_c)) return dgvv_fail(DGVV_EINVAL, "alpha_c must be finite");
@@ -110,6 +113,7 @@ dgvv_status dgvv_apply_oseen(dgvv_ctx* c, double alpha_c, const double* src, dou
 dgvv_status dgvv_gmres_solve(dgvv_ctx* c, double alpha_c, const double* b, double* x, double rtol,
                              int32_t restart, int32_t maxit, int32_t precond, const double* lambda_hi_per_level,
                              int32_t* iters, double* relres, dgvv_stream stream) {
+  DGVV_RANGE();
   if (!c || !b || !x) return dgvv_fail(DGVV_EINVAL, "null argument");
   if (b == x) return dgvv_fail(DGVV_EINVAL, "b and x alias");
   TRY(op_ready(c, DGVV_OP_VISCOUS));

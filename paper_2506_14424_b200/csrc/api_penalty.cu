@@ -115,6 +115,7 @@ DGVV_INTERNAL dgvv_status vcycle_pen_rec(dgvv_ctx* c, int l, const double* b, do
 }
 
 dgvv_status dgvv_set_penalty_parameters(dgvv_ctx* c, const double* tau_div, const double* tau_cont) {
+  DGVV_RANGE();
   if (!c || !tau_div || !tau_cont) return dgvv_fail(DGVV_EINVAL, "null argument");
   const int nt = c->n_total;
   std::vector<double> td(nt), tc(nt);
@@ -135,6 +136,7 @@ dgvv_status dgvv_set_penalty_parameters(dgvv_ctx* c, const double* tau_div, cons
 }
 
 dgvv_status dgvv_apply_penalty(dgvv_ctx* c, const double* src, double* dst, dgvv_stream stream) {
+  DGVV_RANGE();
   if (!c || !src || !dst) return dgvv_fail(DGVV_EINVAL, "null argument");
   if (src == dst) return dgvv_fail(DGVV_EINVAL, "src and dst alias");
   TRY(op_ready(c, DGVV_OP_PENALTY));
@@ -143,6 +145,7 @@ dgvv_status dgvv_apply_penalty(dgvv_ctx* c, const double* src, double* dst, dgvv
 
 dgvv_status dgvv_apply_penalty_level(dgvv_ctx* c, int32_t level, const double* src, double* dst,
                                      dgvv_stream stream) {
+  DGVV_RANGE();
   TRY(check_level(c, level));
   if (!src || !dst) return dgvv_fail(DGVV_EINVAL, "null argument");
   if (src == dst) return dgvv_fail(DGVV_EINVAL, "src and dst alias");

@@ -252,49 +252,81 @@ __global__ void diag_kernel(const DiagArgs A) {
 // prolongation: M = P1 (nf x nc); restriction: M = P1^T; u_lin interpolation: M = I1.
 struct Mat8 { double m[DGVV_NMAX * DGVV_NMAX]; };
 
+// One team of TS = max(nin, nout)^2 threads per cell, CPB cells per CTA.  HBM-bound (§8(d): read
+// nin^3, write nout^3 [+ read nout^3 of add] per component), so the kernel is organised around the
+// memory system: thread (x, y) reads its z-column with nin independent coalesced loads and
+// contracts it in registers (z first, coefficients as immediate constant-bank operands); the y
+// and x contractions go through two small shared arrays with the thread's row of M in registers;
+// the output planes are written coalesced.  Two barriers per component.
+template <int nin, int nout>
+struct T3Cfg {
+  static constexpr int NMAXIO = nin > nout ? nin : nout;
+  static constexpr int TS = NMAXIO * NMAXIO;
+  static constexpr int S1 = nout * nin * nin, S2 = nout * nout * nin;
+  static constexpr int CS = S1 + S2;
+  static constexpr int CPB = (256 / TS) < 1 ? 1 : ((256 / TS) > 16 ? 16 : (256 / TS));
+};
+
 template <typename R, int nin, int nout, int NC, int CPB>
-__global__ void __launch_bounds__(CPB * 64) tensor3_kernel(Mat8 M, const R* in, R* out, const R* add, R beta, int n_cells) {
-  constexpr int ni3 = nin * nin * nin, no3 = nout * nout * nout;
-  constexpr int S1 = nin * nin * nout, S2 = nin * nout * nout;
-  constexpr int CS = ni3 + S1 + S2;
+__global__ void __launch_bounds__(CPB * T3Cfg<nin, nout>::TS) tensor3_kernel(Mat8 M, const R* in, R* out, const R* add, R beta, int n_cells) {
+  using Cf = T3Cfg<nin, nout>;
+  constexpr int ni2 = nin * nin, ni3 = ni2 * nin, no2 = nout * nout, no3 = no2 * nout, nio = nin * nout;
+  constexpr int TS = Cf::TS;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   R* smem = reinterpret_cast<R*>(smem_raw);
-  const int lc = threadIdx.x / 64, t = threadIdx.x % 64;
+  const int lc = threadIdx.x / TS, t = threadIdx.x - lc * TS;
   const int cell = blockIdx.x * CPB + lc;
   const bool active = cell < n_cells;
-  R* sin_ = smem + lc * CS;
-  R* s1 = sin_ + ni3;
-  R* s2 = s1 + S1;
+  R* s1 = smem + lc * Cf::CS;      // [z_o][y_i][x_i]
+  R* s2 = s1 + Cf::S1;             // [z_o][y_o][x_i]
+  R my[nin], mx[nin];              // this thread's rows of M for the y (t < nin nout) and x (t < nout^2) steps
+#pragma unroll
+  for (int k = 0; k < nin; ++k) {
+    my[k] = (t < nio) ? R(M.m[(t / nin) * nin + k]) : R(0);
+    mx[k] = (t < no2) ? R(M.m[(t % nout) * nin + k]) : R(0);
+  }
   for (int c = 0; c < NC; ++c) {
-    if (active)
-      for (int i = t; i < ni3; i += 64) sin_[i] = in[((size_t)cell * NC + c) * ni3 + i];
-    __syncthreads();
-    for (int i = t; i < S1; i += 64) {           // [z_i][y_i][x_o]
-      const int xo = i % nout, r = i / nout;
-      R acc = R(0);
+    if (t < ni2) {
+      R col[nin];
+      const R* g = in + ((size_t)(active ? cell : 0) * NC + c) * ni3 + t;
 #pragma unroll
-      for (int k = 0; k < nin; ++k) acc += R(M.m[xo * nin + k]) * sin_[r * nin + k];
-      s1[i] = acc;
-    }
-    __syncthreads();
-    for (int i = t; i < S2; i += 64) {           // [z_i][y_o][x_o]
-      const int xo = i % nout, yo = (i / nout) % nout, zi = i / (nout * nout);
-      R acc = R(0);
+      for (int k = 0; k < nin; ++k) col[k] = g[k * ni2];
 #pragma unroll
-      for (int k = 0; k < nin; ++k) acc += R(M.m[yo * nin + k]) * s1[(zi * nin + k) * nout + xo];
-      s2[i] = acc;
-    }
-    __syncthreads();
-    if (active)
-      for (int i = t; i < no3; i += 64) {        // [z_o][y_o][x_o]
-        const int r = i % (nout * nout), zo = i / (nout * nout);
+      for (int zo = 0; zo < nout; ++zo) {
         R acc = R(0);
 #pragma unroll
-        for (int k = 0; k < nin; ++k) acc += R(M.m[zo * nin + k]) * s2[k * nout * nout + r];
-        const size_t o = ((size_t)cell * NC + c) * no3 + i;
-        out[o] = (beta == R(0)) ? acc : acc + beta * add[o];
+        for (int k = 0; k < nin; ++k) acc += R(M.m[zo * nin + k]) * col[k];
+        s1[zo * ni2 + t] = acc;
       }
+    }
     __syncthreads();
+    if (t < nio) {
+      const int xi = t % nin;
+#pragma unroll
+      for (int zo = 0; zo < nout; ++zo) {
+        R acc = R(0);
+#pragma unroll
+        for (int k = 0; k < nin; ++k) acc += my[k] * s1[(zo * nin + k) * nin + xi];
+        s2[zo * nio + t] = acc;
+      }
+    }
+    __syncthreads();
+    if (t < no2 && active) {
+      const int yo = t / nout;
+      const size_t o = ((size_t)cell * NC + c) * no3 + t;
+      R av[nout];
+      if (beta != R(0)) {
+#pragma unroll
+        for (int zo = 0; zo < nout; ++zo) av[zo] = add[o + zo * no2];
+      }
+#pragma unroll
+      for (int zo = 0; zo < nout; ++zo) {
+        R acc = R(0);
+#pragma unroll
+        for (int k = 0; k < nin; ++k) acc += mx[k] * s2[(zo * nout + yo) * nin + k];
+        out[o + zo * no2] = (beta == R(0)) ? acc : acc + beta * av[zo];
+      }
+    }
   }
 }
 

@@ -69,18 +69,15 @@ cudaError_t launch_diag(int nc, int n, int form, int geo, const DiagArgs& a, cud
 }
 
 // ---------------------------------------------------------------- K7
-#ifndef T3CPB
-#define T3CPB 2
-#endif
 template <typename R, int nin, int nout>
 static cudaError_t t3_run(int nc, const Mat8& M, const R* in, R* out, const R* add, double beta, int ncells, cudaStream_t s) {
-  constexpr int CPB = T3CPB;   // cells per CTA (64 threads each)
-  constexpr int CS = nin * nin * nin + nin * nin * nout + nin * nout * nout;
-  const size_t smem = (size_t)CPB * CS * sizeof(R);
+  using Cf = T3Cfg<nin, nout>;
+  constexpr int CPB = Cf::CPB;   // cells per CTA (teams of max(nin, nout)^2 threads)
+  const size_t smem = (size_t)CPB * Cf::CS * sizeof(R);
   if (ncells <= 0) return cudaSuccess;
   const int grid = (ncells + CPB - 1) / CPB;
-  if (nc == 3) tensor3_kernel<R, nin, nout, 3, CPB><<<grid, CPB * 64, smem, s>>>(M, in, out, add, (R)beta, ncells);
-  else tensor3_kernel<R, nin, nout, 1, CPB><<<grid, CPB * 64, smem, s>>>(M, in, out, add, (R)beta, ncells);
+  if (nc == 3) tensor3_kernel<R, nin, nout, 3, CPB><<<grid, CPB * Cf::TS, smem, s>>>(M, in, out, add, (R)beta, ncells);
+  else tensor3_kernel<R, nin, nout, 1, CPB><<<grid, CPB * Cf::TS, smem, s>>>(M, in, out, add, (R)beta, ncells);
   return cudaGetLastError();
 }
 

@@ -207,12 +207,16 @@ def run_f1(reps):
 def run_f2(reps):
     """f2: penalty-step operator on the C2 mesh (32^3 deformed, k=3) and on C3's 64^3 k=4 mesh,
     tau ~ |u| h dt (Fehn2018b-sized, P1), apply + Jacobi-PCG to rtol 1e-10."""
-    for name, m, k in (("C2", deformed_cube(32, 3), 3), ("C3", cube(64), 4)):
+    # dt scales both penalty parameters (tau_D dt, tau_C dt): 1e-3 is a CFL-sized step (the operator
+    # stays close to the mass matrix, Jacobi suffices), 1e-1 the large steps of the paper's
+    # steady cavity runs, where "a multigrid preconditioner is necessary" (PAPER.md:2229-2233)
+    for name, m, k, dt in (("C2", deformed_cube(32, 3), 3, 1e-3), ("C3", cube(64), 4, 1e-3),
+                           ("C3 dt=1e-1", cube(64), 4, 1e-1)):
         ctx = Context(m, k, visc_law=C2_LAW)
         rng = np.random.default_rng(11)
         h = 1.0 / round(m.n_cells ** (1 / 3))
         speed = rng.uniform(0.1, 2.0, m.n_cells)
-        ctx.set_penalty_parameters(speed * h * 1e-3, speed * 1e-3)
+        ctx.set_penalty_parameters(speed * h * dt, speed * dt)
         N = 3 * ctx.n_dofs(0)
         src = dev(uniform(0, N))
         dst = torch.empty_like(src)
@@ -222,12 +226,12 @@ def run_f2(reps):
         ms = timeit(lambda: ctx.apply_penalty(src, dst), 20, reps)
         report(name + "+f2", "apply_penalty", ms, N, byt, None, "mass + div-div + continuity penalty")
         x = torch.zeros_like(src)
-        ctx.cg_solve(A.OP_PENALTY, src, x, rtol=1e-10, maxit=500, precond="jacobi")
+        ctx.cg_solve(A.OP_PENALTY, src, x, rtol=1e-10, maxit=2000, precond="jacobi")
         x.zero_()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        it, rr = ctx.cg_solve(A.OP_PENALTY, src, x, rtol=1e-10, maxit=500, precond="jacobi")
+        it, rr = ctx.cg_solve(A.OP_PENALTY, src, x, rtol=1e-10, maxit=2000, precond="jacobi")
         e1.record()
         e1.synchronize()
         ms = e0.elapsed_time(e1)
@@ -236,13 +240,13 @@ def run_f2(reps):
         # f2 multigrid: V-cycle-PCG over the p-levels k -> 2 -> 1
         degs = [k, 2, 1]
         cm = Context(m, k, visc_law=C2_LAW, degrees=degs)
-        cm.set_penalty_parameters(speed * h * 1e-3, speed * 1e-3)
+        cm.set_penalty_parameters(speed * h * dt, speed * dt)
         t_l, lams = _timed(lambda: [1.2 * cm.estimate_lambda_max(A.OP_PENALTY, dev(uniform(2, 3 * cm.n_dofs(l))),
                                                                  level=l, steps=20) for l in range(3)])
         x = torch.zeros_like(src)
-        cm.cg_solve(A.OP_PENALTY, src, x, rtol=1e-10, maxit=500, precond="vcycle", lam_hi_per_level=lams)
+        cm.cg_solve(A.OP_PENALTY, src, x, rtol=1e-10, maxit=2000, precond="vcycle", lam_hi_per_level=lams)
         x.zero_()
-        ms, (it, rr) = _timed(lambda: cm.cg_solve(A.OP_PENALTY, src, x, rtol=1e-10, maxit=500, precond="vcycle",
+        ms, (it, rr) = _timed(lambda: cm.cg_solve(A.OP_PENALTY, src, x, rtol=1e-10, maxit=2000, precond="vcycle",
                                                   lam_hi_per_level=lams))
         report(name + "+f2", "penalty_pcg_vcycle", ms, N, None, None,
                f"{it} iterations to rtol 1e-10 (relres {rr:.2e}); {ms / max(it, 1):.3f} ms/iteration; "
