@@ -82,7 +82,7 @@ __global__ void K3_BOUNDS(CPB * n * n) carreau_nu_kernel(const NuArgs A) {
       if (GEO == 1) {
         const double* vm = A.vJi + (size_t)cell * 9 * n3 + q;
 #pragma unroll
-        for (int r = 0; r < 9; ++r) Ji[r] = vm[r * n3];
+        for (int r = 0; r < 9; ++r) Ji[r] = __ldg(vm + r * n3);   // read-only path: may be hoisted above the nu stores
       }
       if (active) {
         const double e = eta_of(gx, Ji);
@@ -131,7 +131,7 @@ __global__ void K3_BOUNDS(CPB * n * n) carreau_nu_kernel(const NuArgs A) {
       if (GEO == 1) {
         const double* fm = A.fJi + ((size_t)cell * 6 + f) * 9 * n2 + p;
 #pragma unroll
-        for (int r = 0; r < 9; ++r) Ji[r] = fm[r * n2];
+        for (int r = 0; r < 9; ++r) Ji[r] = __ldg(fm + r * n2);
       }
       const double e = eta_of(gx, Ji);
       if (active) {

@@ -832,15 +832,38 @@ sipg_apply2_kernel(const ApplyArgsT<R> A) {
           A.dst[i] = __ldg(A.b + i) - y[c][z];
         }
     } else {
+      // every load of the update (b, D^-1, d) is issued before the first store: d is read and
+      // written in place, so a load of d placed after a store to d / x_out in program order cannot
+      // be hoisted above it (possible aliasing) and the NC * n iterations would each pay a full
+      // DRAM round trip (measured: C5 Chebyshev apply 4.5 ms against 2.7 ms for the plain apply)
       const R cr = R(A.c_r), crho = R(A.c_rho);
+      R bv[NC][n], dv[NC][n], dd[NC][n];
 #pragma unroll
       for (int c = 0; c < NC; ++c)
 #pragma unroll
         for (int z = 0; z < n; ++z) {
           const size_t i = off + c * n3 + z * n2;
-          const R r = __ldg(A.b + i) - y[c][z];
-          R dn = cr * __ldg(A.dinv + i) * r;
-          if (crho != R(0.0)) dn += crho * A.dvec[i];
+          bv[c][z] = __ldg(A.b + i);
+          dv[c][z] = __ldg(A.dinv + i);
+        }
+      if (crho != R(0.0)) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+#pragma unroll
+          for (int z = 0; z < n; ++z) dd[c][z] = crho * A.dvec[off + c * n3 + z * n2];
+      } else {
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+#pragma unroll
+          for (int z = 0; z < n; ++z) dd[c][z] = R(0.0);
+      }
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+#pragma unroll
+        for (int z = 0; z < n; ++z) {
+          const size_t i = off + c * n3 + z * n2;
+          const R r = bv[c][z] - y[c][z];
+          const R dn = cr * dv[c][z] * r + dd[c][z];
           A.dvec[i] = dn;
           A.xout[i] = su[c * CST + z * PS + b * RS + a] + dn;
         }

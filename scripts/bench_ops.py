@@ -487,6 +487,18 @@ def run_c5(reps):
     lams = [1.2 * ctx2.estimate_lambda_max(A.OP_VISCOUS, dev(uniform(2, 3 * ctx2.n_dofs(l))), level=l, steps=15)
             for l in range(3)]
     x = torch.zeros_like(src)
+    # where the V-cycle's time goes: the Helmholtz apply and Chebyshev(5) from zero on each p-level
+    for l, kk in enumerate((3, 2, 1)):
+        Nl = 3 * ctx2.n_dofs(l)
+        sl, dl = dev(uniform(3 + l, Nl)), torch.empty(Nl, dtype=torch.float64, device="cuda")
+        ms = timeit(lambda: ctx2.apply_viscous(sl, dl, level=l), 20, reps)
+        report("C5", f"level{l}_k{kk}_apply_helmholtz", ms, Nl, visc_bytes(m.n_cells, kk + 1, False),
+               visc_flops(Nl, kk + 1, False))
+        wk = torch.empty(2 * Nl, dtype=torch.float64, device="cuda")
+        ms = timeit(lambda: ctx2.chebyshev_smooth(A.OP_VISCOUS, dl, sl, lams[l] / 20.0, lams[l], degree=5,
+                                                  x_is_zero=True, work=wk, level=l), 5, reps)
+        report("C5", f"level{l}_k{kk}_chebyshev5_from_zero", ms, Nl, None, None, "4 applies with fused epilogue + first step")
+        del sl, dl, wk
     ms = timeit(lambda: ctx2.vcycle(A.OP_VISCOUS, src, x, lams), 5, reps)
     report("C5", "viscous_vcycle_3_2_1", ms, N, None, None, "Helmholtz (mass 1e3) Carreau V-cycle, FP64 levels")
     ms = timeit(lambda: ctx2.vcycle_fp32(A.OP_VISCOUS, src, x, lams), 5, reps)
