@@ -9,6 +9,7 @@ import concurrent.futures as cf
 import os
 import subprocess
 import sys
+import time
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
@@ -35,9 +36,11 @@ def _compile(src):
     cmd = [NVCC] + ARCH + FLAGS + ["-c", src, "-o", obj]
     if src.endswith(".cpp"):
         cmd = [NVCC] + FLAGS[:3] + ["-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-x", "c++", "-c", src, "-o", obj]
+    t0 = time.time()
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
+    os.utime(obj, (t0, t0))     # stamp with the compile's start: a header edited meanwhile makes it stale
     return obj, r.stderr
 
 

@@ -135,7 +135,7 @@ def test_inverse_diagonal(op, mk):
 
 
 # ------------------------------------------------------------------ transfer
-@pytest.mark.parametrize("pair", [(5, 3), (3, 2), (2, 1)])
+@pytest.mark.parametrize("pair", [(5, 3), (3, 2), (2, 1), (4, 2), (3, 1), (5, 1)])
 def test_transfer_parity(pair):
     kf, kc = pair
     m = cube(3)
@@ -150,6 +150,26 @@ def test_transfer_parity(pair):
     c = dev(np.zeros(m.n_cells * nc))
     ctx.restrict(1, 0, dev(r), c, beta=0.0)
     assert rel(host(c), mg.restrict(r, kf, kc, m.n_cells)) < TOL
+
+
+@pytest.mark.parametrize("pair", [(4, 2), (3, 2), (2, 1)])
+def test_transfer_parity_vector(pair):
+    """Three-component transfer (the viscous operator's levels): each component block is transferred
+    on its own, cell-major [cell][c][point]; ragged last CTA (5^3 cells); beta != 0 on both sides."""
+    kf, kc = pair
+    m = cube(5)
+    ctx = Ctx(m, kf, visc_law=laws.C1_LAW, degrees=[kf, kc])
+    nf, nc = (kf + 1) ** 3, (kc + 1) ** 3
+    xc = uniform(1, 3 * m.n_cells * nc)
+    xf0 = uniform(2, 3 * m.n_cells * nf)
+    f = dev(xf0.copy())
+    ctx.prolongate(0, 0, dev(xc), f, beta=0.5)
+    assert rel(host(f), mg.prolongate(xc, kf, kc, 3 * m.n_cells) + 0.5 * xf0) < TOL
+    r = uniform(3, 3 * m.n_cells * nf)
+    c0 = uniform(4, 3 * m.n_cells * nc)
+    c = dev(c0.copy())
+    ctx.restrict(0, 0, dev(r), c, beta=-2.0)
+    assert rel(host(c), mg.restrict(r, kf, kc, 3 * m.n_cells) - 2.0 * c0) < TOL
 
 
 # ------------------------------------------------------------------ smoother / V-cycle
