@@ -10,8 +10,12 @@ cudaError_t launch_apply_visc_f(int n, int form, int geo, const ApplyArgsT<float
 
 cudaError_t upload_tables_pois(const Tab1D* tabs) { return tu_upload_tables(tabs); }
 
+// n = 6 (C4, k = 5) FP64: 4 cells x 4 CTAs/SM.  With the Chebyshev epilogue's loads issued together
+// (sipg_apply2.cuh) the smaller CTA wins everywhere: apply 1.110 -> 1.057 ms, Chebyshev(5) 5.72 ->
+// 5.25 ms, V-cycle 19.98 -> 18.67 ms against 6 x 4 (5 x 4: 1.111 / 5.66 / 19.8); before that fix its
+// apply-only gain was lost in the epilogue
 #ifndef PCPB6
-#define PCPB6 6
+#define PCPB6 4
 #endif
 #ifndef PMINB6
 #define PMINB6 4
