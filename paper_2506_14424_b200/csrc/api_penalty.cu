@@ -1,6 +1,11 @@
 // api_penalty.cu — C ABI: the divergence/continuity penalty-step operator and its multigrid (f2).
 #include "api_internal.cuh"
 
+namespace dgvv {
+cudaError_t launch_cheb_vec_resid(const double* Ax, const double* b, const double* dinv, double c_rho, double c_r,
+                                  double* d, double* x, long n, cudaStream_t s);   // k_cg.cu
+}
+
 extern "C" {
 
 // ------------------------------------------------------------------ f2: penalty-step operator
@@ -52,7 +57,7 @@ DGVV_INTERNAL dgvv_status ensure_dinv_pen(dgvv_ctx* c, int l, cudaStream_t s) {
 }
 
 // Chebyshev-Jacobi smoother of SURVEY §8(c) c1.6 for the penalty operator on level l:
-// r = b - A x by the penalty kernel, then d = c_rho d + c_r D^-1 r, x += d (cheb_vec kernel).
+// A x by the penalty kernel, then r = b - A x, d = c_rho d + c_r D^-1 r, x += d in one vector kernel.
 // work holds 2 N doubles (r | d).
 DGVV_INTERNAL dgvv_status cheb_pen(dgvv_ctx* c, int l, double* x, const double* b, int degree, double lo, double hi,
                             int x_is_zero, double* work, cudaStream_t s) {
@@ -65,15 +70,13 @@ DGVV_INTERNAL dgvv_status cheb_pen(dgvv_ctx* c, int l, double* x, const double* 
   if (x_is_zero) {
     DGVV_CUDA_TRY(launch_cheb_first(b, dinv, 1.0 / theta, d, x, N, s));
   } else {
-    TRY(apply_penalty_impl(c, l, x, r, s));
-    DGVV_CUDA_TRY(launch_axpby(1.0, b, -1.0, r, N, s));          // r = b - A x
-    DGVV_CUDA_TRY(launch_cheb_vec(r, dinv, 0.0, 1.0 / theta, d, x, N, s));
+    TRY(apply_penalty_impl(c, l, x, r, s));                       // r = A x; b - A x in the update kernel
+    DGVV_CUDA_TRY(launch_cheb_vec_resid(r, b, dinv, 0.0, 1.0 / theta, d, x, N, s));
   }
   for (int j = 1; j < degree; ++j) {
     const double rho_new = 1.0 / (2.0 * sigma - rho);
     TRY(apply_penalty_impl(c, l, x, r, s));
-    DGVV_CUDA_TRY(launch_axpby(1.0, b, -1.0, r, N, s));
-    DGVV_CUDA_TRY(launch_cheb_vec(r, dinv, rho_new * rho, 2.0 * rho_new / delta, d, x, N, s));
+    DGVV_CUDA_TRY(launch_cheb_vec_resid(r, b, dinv, rho_new * rho, 2.0 * rho_new / delta, d, x, N, s));
     rho = rho_new;
   }
   return DGVV_OK;

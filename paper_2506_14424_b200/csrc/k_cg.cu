@@ -125,6 +125,23 @@ cudaError_t launch_cg_probe_set(double* sv, const int* color, int k, int comp, i
   cg_probe_set_kernel<<<gblocks((long)nv * nc), 256, 0, s>>>(sv, color, k, comp, nv, nc);
   return cudaGetLastError();
 }
+// The same step from an operator product: r = b - Ax formed in the kernel (the penalty smoother's
+// residual axpby and Chebyshev update in one pass: 7 instead of 9 vector streams per step)
+__global__ void cheb_vec_resid_kernel(const double* __restrict__ Ax, const double* __restrict__ b,
+                                      const double* __restrict__ dinv, double c_rho, double c_r, double* d, double* x,
+                                      long n) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    const double r = 1.0 * b[i] + (-1.0) * Ax[i];
+    const double dn = c_r * dinv[i] * r + (c_rho != 0.0 ? c_rho * d[i] : 0.0);
+    d[i] = dn;
+    x[i] += dn;
+  }
+}
+cudaError_t launch_cheb_vec_resid(const double* Ax, const double* b, const double* dinv, double c_rho, double c_r,
+                                  double* d, double* x, long n, cudaStream_t s) {
+  cheb_vec_resid_kernel<<<gblocks(n), 256, 0, s>>>(Ax, b, dinv, c_rho, c_r, d, x, n);
+  return cudaGetLastError();
+}
 cudaError_t launch_cg_probe_get(const double* y, double* diag, const int* color, int k, int comp, int nv,
                                 cudaStream_t s) {
   cg_probe_get_kernel<<<gblocks(nv), 256, 0, s>>>(y, diag, color, k, comp, nv);
